@@ -1,0 +1,359 @@
+"""Benchmark: APR-native 3x3x3 convolution (restricted Gaussian pyramid) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1] [--stencil 3|5]
+                    [--impl ours|reference]
+
+A "step" is one convolve_apr pass (conv-only protocol, bench.hpp:158-169) over
+the whole APR of the configuration, values and interior-node values resident in
+HBM.  value = pixel-equivalent GB/s (4 * N_pixels / t, metrics.hpp:15-21);
+particles/s, the roofline of the conv pass, the paper protocol (row index +
+tree fill + conv) and the end-to-end host-buffer number through
+the C-ABI are reported beside it.  --impl reference times the reference's own
+CPU convolve_apr (oracle/_ref, all host threads) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+for _p in (ROOT, os.path.join(ROOT, "tests")):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
+
+METRIC = "pixel-equivalent GB/s and particles/s for APR 3x3x3 conv; HBM % of peak"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self._stop = gpu, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workload --
+def workload(cfg: str):
+    """Returns (APR, leaf values, description dict)."""
+    import paper_2112_03592_b200 as P
+    if cfg == "c1":
+        import goldens as G
+        d = G.load("c1_256")
+        return G.product_apr(d), d["values"], {"workload": "C1: 256^3 spheres (12, r 6-20, blur 2, seed 42) -> "
+                                                            "APR E=0.1 (reference-built, committed fixture)"}
+    if cfg == "c3":
+        from paper_2112_03592_b200 import synth
+        apr, values = synth.build_spheres_apr(1024, count=48, rmin=24.0, rmax=80.0, blur=2.0, seed=42,
+                                              rel_error=0.1)
+        return apr, values, {"workload": "C3: 1024^3 spheres (48, r 24-80, blur 2, seed 42) -> APR E=0.1 "
+                                         "(built on the GPU by paper_2112_03592_b200.synth)"}
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def algorithmic_bytes(apr) -> int:
+    """Per conv pass: y_idx u16 + value in f32 + out f32 per particle, y_idx u16 +
+    value f32 per interior node, one u32 row begin per row (device layout)."""
+    n_p = apr.access.particle_count()
+    n_t = apr.tree_access.particle_count()
+    rows = apr.access.row_count() + apr.tree_access.row_count()
+    return 10 * n_p + 6 * n_t + 4 * rows
+
+
+# ------------------------------------------------------------------ our arm ---
+def run_ours(args, rank, world):
+    import torch
+    import paper_2112_03592_b200 as P
+    from paper_2112_03592_b200 import _lib as L
+
+    dev_id = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev_id)
+    ctx = P.default_context(dev_id)
+    apr, values, desc = workload(args.config)
+    t0 = time.time()
+    dapr = apr.device(ctx)
+    k = args.stencil
+    w = P.gaussian_stencil(1.0, k)
+    pyr = P.make_pyramid(w, apr.access.l_min, apr.access.l_max, P.PyramidMode.Restricted)
+    dpyr = pyr.device(ctx)
+    setup_s = time.time() - t0
+    accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
+
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+    v = torch.from_numpy(np.ascontiguousarray(values, np.float32)).cuda()
+    tv = torch.empty(max(dapr.n_tree, 1), dtype=torch.float32, device="cuda")
+    out = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")
+    dapr.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    def conv():
+        dapr.convolve_ptr(v.data_ptr(), tv.data_ptr(), dpyr, 1, accum, out.data_ptr(), s)
+
+    def paper_step():
+        dapr.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
+        conv()
+
+    def timed(fn, steps):
+        times = []
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        return times
+
+    for _ in range(args.warmup):
+        conv()
+        paper_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count()
+    with ClockSampler(dev_id) as clk:
+        t_conv = timed(conv, args.steps)
+        launches = ctx.launch_count() - l0
+        t_paper = timed(paper_step, args.steps)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+
+    # end to end through the C-ABI with pinned host buffers (H2D + conv + D2H per step)
+    hv = torch.from_numpy(np.ascontiguousarray(values, np.float32)).pin_memory()
+    htv = tv[:dapr.n_tree].cpu().pin_memory() if dapr.n_tree else torch.zeros(1).pin_memory()
+    hout = torch.empty(dapr.n_particles, dtype=torch.float32).pin_memory()
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        L.check(L.lib().aprgpu_convolve(dapr.handle, hv.data_ptr(), htv.data_ptr(), dpyr.handle, 1, accum,
+                                        hout.data_ptr(), L.HOST, None))
+        b = time.perf_counter()
+        if i >= args.warmup:
+            e2e.append(b - a)
+
+    def agg(x):
+        t = float(np.mean(x))
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    tc, tp, te = agg(t_conv), agg(t_paper), agg(e2e)
+    n_pix = apr.pixel_count()
+    n_p = apr.access.particle_count()
+    B = algorithmic_bytes(apr)
+    peak, peak_kind = peaks()
+    achieved = B / tc / 1e9
+    res = {
+        "metric": METRIC,
+        "value": round(world * 4 * n_pix / tc / 1e9, 3),
+        "unit": "GB/s (pixel-equivalent)",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(tc * 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 values, " + ("f64 accumulate (bit-exact)" if accum == L.ACCUM_EXACT else "f32 accumulate"),
+        "data": "synthetic",
+        "config": dict(desc, stencil=f"gaussian(1.0,{k}) restricted pyramid", pad="reflect",
+                       particles=n_p, interior_nodes=apr.tree_access.particle_count(), pixels=n_pix,
+                       cr=round(n_pix / n_p, 2), l2="flushed between timed steps (256 MB write)",
+                       protocol="conv-only (tree filled outside the timed region, bench.hpp:158-169)",
+                       parallelism=f"{world} independent replicas" if world > 1 else "single GPU"),
+        "particles_per_s": round(world * n_p / tc, 1),
+        "paper_protocol": {"ms_per_step": round(tp * 1e3, 4), "gbps_pixel_equiv": round(4 * n_pix / tp / 1e9, 3),
+                           "includes": "fill_tree + convolve_apr (row index prebuilt at upload)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "note": f"algorithmic bytes {B} per pass (10/particle + 6/node + 4/row) / conv-pass time; "
+                             f"peak {peak_kind}"},
+        "e2e": {"value": round(world * 4 * n_pix / te / 1e9, 3), "unit": "GB/s (pixel-equivalent)",
+                "ms_per_step": round(te * 1e3, 4),
+                "h2d_bytes_per_step": int(4 * n_p + 4 * dapr.n_tree), "d2h_bytes_per_step": int(4 * n_p)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "setup_s": round(setup_s, 2),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(apr, values, tv[:dapr.n_tree].cpu().numpy(), pyr, args)
+    return res
+
+
+# -------------------------------------------------------------- CPU baseline --
+def _ref_objects(apr, pyr):
+    from pyoracle import Ref
+    R = Ref()
+    rapr = R.apr_from_arrays(apr.access, apr.source_dims)
+    levels = [((s.kz, s.kx, s.ky), s.weights) for s in pyr.stencils]
+    rpyr = R.explicit_pyramid(levels, pyr.l_min)
+    return R, rapr, rpyr
+
+
+def cpu_baseline(apr, values, tree_values, pyr, args):
+    """The reference's own convolve_apr (oracle/_ref, all host threads) timed
+    with its time_median protocol (bench.hpp:106-117) on the full workload."""
+    from pyoracle import ref_available
+    n_pix = apr.pixel_count()
+    if ref_available():
+        R, rapr, rpyr = _ref_objects(apr, pyr)
+        threads = R.resolve_threads(0)
+        R.convolve(rapr, values, tree_values, rpyr, 1, threads)  # cold run discarded
+        times = []
+        budget = time.time() + args.cpu_seconds
+        while len(times) < 3 or (time.time() < budget and len(times) < 15):
+            a = time.perf_counter()
+            R.convolve(rapr, values, tree_values, rpyr, 1, threads)
+            times.append(time.perf_counter() - a)
+        t = statistics.median(times)
+        return {"value": round(4 * n_pix / t / 1e9, 4), "unit": "GB/s (pixel-equivalent)", "cores": threads,
+                "kind": "reference", "ms_per_step": round(t * 1e3, 2),
+                "particles_per_s": round(apr.access.particle_count() / t, 1),
+                "sample": f"full workload convolve_apr, median of {len(times)} after a discarded cold run"}
+    from pyoracle import Oracle
+    O = Oracle()
+    levels = [((s.kz, s.kx, s.ky), s.weights) for s in pyr.stencils]
+    a = time.perf_counter()
+    O.convolve(apr.access, apr.tree_access, values, tree_values, levels, apr.access.l_min, 1)
+    t = time.perf_counter() - a
+    return {"value": round(4 * n_pix / t / 1e9, 4), "unit": "GB/s (pixel-equivalent)", "cores": 1, "kind": "port",
+            "ms_per_step": round(t * 1e3, 2), "sample": "full workload, one pass of the C oracle"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU convolve_apr on the same workload."""
+    from pyoracle import Oracle, Ref, ref_available
+    apr, values, desc = workload(args.config)  # input generation only
+    n_pix = apr.pixel_count()
+    k = args.stencil
+    if ref_available():
+        # everything below is the unmodified reference: tree, gaussian, make_pyramid, convolve_apr
+        R = Ref()
+        rapr = R.apr_from_arrays(apr.access, apr.source_dims)
+        k3, w = R.gaussian_stencil(1.0, k)
+        rpyr = R.make_pyramid(w, k3, apr.access.l_min, apr.access.l_max, 0)
+        threads = R.resolve_threads(0)
+        tv = R.fill_tree(rapr, values, threads)
+        kind = "reference"
+        fn = lambda: R.convolve(rapr, values, tv, rpyr, 1, threads)  # noqa: E731
+    else:
+        O = Oracle()
+        g = O  # the C restatement of the reference (single-threaded)
+        import paper_2112_03592_b200 as P
+        w = P.gaussian_stencil(1.0, k).weights
+        levels = O.restricted_levels(w, (k, k, k), apr.access.l_min, apr.access.l_max)
+        tree = apr.tree_access if apr.tree_access is not None else O.init_tree_structure(apr.access, apr.source_dims)
+        tv = g.fill_tree(apr.access, tree, apr.source_dims, values)
+        threads, kind = 1, "port"
+        fn = lambda: O.convolve(apr.access, tree, values, tv, levels, apr.access.l_min, 1)  # noqa: E731
+    fn()
+    for _ in range(args.warmup):
+        fn()
+    times = []
+    for _ in range(args.steps):
+        a = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - a)
+    t = float(np.mean(times))
+    v = round(4 * n_pix / t / 1e9, 4)
+    return {"metric": METRIC, "value": v, "unit": "GB/s (pixel-equivalent)", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 values, f64 accumulate", "data": "synthetic", "impl": "reference",
+            "config": dict(desc, stencil=f"gaussian(1.0,{args.stencil}) restricted pyramid", pad="reflect"),
+            "particles_per_s": round(apr.access.particle_count() / t, 1),
+            "cpu_baseline": {"value": v, "unit": "GB/s (pixel-equivalent)", "cores": threads, "kind": kind,
+                             "sample": "full workload convolve_apr per step"},
+            "e2e": {"value": v, "unit": "GB/s (pixel-equivalent)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c1"))
+    ap.add_argument("--stencil", type=int, default=3)
+    ap.add_argument("--accum", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args, rank, world)), flush=True)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        torch.distributed.init_process_group("nccl")
+    res = run_ours(args, rank, world)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/* include/aprgpu.h -- C-ABI of the B200-native APR convolution path.
+ *
+ * This is the drop-in boundary for the reference's hot path (aprkit,
+ * /root/reference/proj/include/aprkit).  Every entry point names the reference
+ * interface it replaces.  Plain pointers, sizes and status codes only: no C++
+ * types, no exceptions, no torch types cross this boundary.  The C++ shim a
+ * maintainer adds on the reference side (include/aprkit_gpu.hpp) maps the
+ * status codes back onto aprkit's exception taxonomy (errors.hpp:9-41).
+ *
+ * Conventions
+ *  - Every function returns an aprgpu_status.  On failure the thread-local
+ *    message is available from aprgpu_last_error().
+ *  - Buffers flagged APRGPU_HOST are host memory (the call stages them through
+ *    device memory and is synchronous); APRGPU_DEVICE buffers are device
+ *    pointers on the APR's GPU and the call is stream-ordered on `stream`
+ *    (a cudaStream_t; NULL = the context's own stream).
+ *  - Thread-safe per context; one context per GPU.
+ */
+#ifndef APRGPU_H
+#define APRGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    APRGPU_OK = 0,
+    APRGPU_ERR_RANGE = 1,      /* aprkit::RangeError      (errors.hpp:9-13)  */
+    APRGPU_ERR_CAPABILITY = 2, /* aprkit::CapabilityError (errors.hpp:21-25) */
+    APRGPU_ERR_INTEGRITY = 3,  /* aprkit::IntegrityError  (errors.hpp:15-19) */
+    APRGPU_ERR_CUDA = 4,
+    APRGPU_ERR_NCCL = 5,
+    APRGPU_ERR_OOM = 6,
+    APRGPU_ERR_INVALID = 7 /* bad argument (null pointer, unknown enum, ...) */
+} aprgpu_status;
+
+enum { APRGPU_HOST = 0, APRGPU_DEVICE = 1 };
+/* PadMode (reconstruct.hpp:13) */
+enum { APRGPU_PAD_ZERO = 0, APRGPU_PAD_REFLECT = 1 };
+/* Accumulation: EXACT = fp64 in the reference's (az,ax,ay) order, bit-identical
+ * to convolve_apr; FAST = fp32 FMA in the same order (tolerance 1e-5 rel with
+ * scale max(|e|,|g|,1) for non-negative stencils, acceptance.cpp:271-276). */
+enum { APRGPU_ACCUM_EXACT = 0, APRGPU_ACCUM_FAST = 1 };
+/* PyramidMode (stencil.hpp:162) */
+enum { APRGPU_PYR_RESTRICTED = 0, APRGPU_PYR_RESCALED = 1, APRGPU_PYR_UNIFORM = 2, APRGPU_PYR_EXPLICIT = 3 };
+/* which access structure */
+enum { APRGPU_LEAF = 0, APRGPU_TREE = 1 };
+
+#define APRGPU_MAX_LEVELS 20
+#define APRGPU_MAX_EXTENT 13 /* kMaxStencilExtent, convolve.hpp:18 */
+
+typedef struct aprgpu_ctx aprgpu_ctx;
+typedef struct aprgpu_apr aprgpu_apr;
+typedef struct aprgpu_pyramid aprgpu_pyramid;
+
+/* Host view of aprkit::LinearAccess (linear_access.hpp:52-96): per-level dims
+ * indexed by absolute level (l_max+1 entries), u16 y indices, u64 cumulative
+ * row ends (one per (l,z,x) row), u64 level row offsets. */
+typedef struct {
+    int32_t l_min, l_max;
+    const int32_t* z_dim;
+    const int32_t* x_dim;
+    const int32_t* y_dim;
+    const uint16_t* y_idx;
+    uint64_t n_particles;
+    const uint64_t* xz_end;
+    uint64_t n_rows;
+    const uint64_t* level_offset;
+} aprgpu_access_desc;
+
+typedef struct {
+    int32_t l_min, l_max;
+    uint64_t n_particles, n_rows;
+} aprgpu_access_info;
+
+/* ---- context ------------------------------------------------------------- */
+int aprgpu_init(int device, aprgpu_ctx** out);
+int aprgpu_ctx_free(aprgpu_ctx* ctx);
+int aprgpu_ctx_stream(aprgpu_ctx* ctx, void** stream_out);
+const char* aprgpu_last_error(void);
+int aprgpu_version(void);
+
+/* ---- structure ----------------------------------------------------------- */
+/* Uploads the leaf access (aprkit::APR::access, apr.hpp:36) into the device
+ * layout and builds everything the convolution needs (row-begin u32 prefix,
+ * per-level non-empty row lists).  tree may be NULL: the interior-node
+ * structure is then built on the GPU (replaces init_tree_structure,
+ * tree.hpp:26-82, bit-exact); otherwise it is uploaded and its parent links are
+ * verified (IntegrityError semantics of synchronized_parent_pass, tree.hpp:98). */
+int aprgpu_upload_access(aprgpu_ctx* ctx, const aprgpu_access_desc* leaf, const aprgpu_access_desc* tree,
+                         const int32_t source_dims[3], aprgpu_apr** out);
+int aprgpu_apr_free(aprgpu_apr* apr);
+int aprgpu_apr_dims(const aprgpu_apr* apr, int32_t dims_out[3]);
+int aprgpu_access_get_info(const aprgpu_apr* apr, int which, aprgpu_access_info* out);
+/* Downloads an access structure back into the reference layout (bit-exact
+ * round trip).  Arrays sized by aprgpu_access_get_info: y_idx[n_particles],
+ * xz_end[n_rows], level_offset/z_dim/x_dim/y_dim[l_max+1]. */
+int aprgpu_download_access(const aprgpu_apr* apr, int which, uint16_t* y_idx, uint64_t* xz_end,
+                           uint64_t* level_offset, int32_t* z_dim, int32_t* x_dim, int32_t* y_dim);
+/* nonempty_row_index (convolve.hpp:32-44) for one level: writes up to cap rows
+ * (z, x, y_min, y_max) and returns the row count in *count. */
+int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, uint16_t* y_min,
+                     uint16_t* y_max, uint64_t cap, uint64_t* count);
+
+/* ---- tree ----------------------------------------------------------------- */
+/* fill_tree (tree.hpp:110-150): leaf[n_particles] -> tree[n_tree]; fp64
+ * accumulation in the reference's per-parent order, bit-exact. */
+int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream);
+
+/* ---- stencils (host) ------------------------------------------------------ */
+/* restrict_stencil (stencil.hpp:127-160).  out_k3 gets the restricted extents;
+ * out (may be NULL to query) gets the weights, bit-identical to the reference
+ * wherever the reference's O(8^delta k^3) loop is tractable. */
+int aprgpu_restrict_stencil(const float* w, int kz, int kx, int ky, int delta, int32_t out_k3[3], float* out);
+/* gaussian_stencil (stencil.hpp:59-79), box_stencil (:52), sobel_stencil (:83) */
+int aprgpu_gaussian_stencil(double sigma, int size, int32_t* k_out, float* out);
+int aprgpu_box_stencil(int k, float* out);
+int aprgpu_sobel_stencil(int axis, float* out);
+
+/* make_pyramid (stencil.hpp:176-191) / explicit_pyramid (:193-202), held on
+ * the device for the convolution.  For explicit pyramids w holds the stencils
+ * level by level, k3 their extents (3 ints per level). */
+int aprgpu_pyramid_create(aprgpu_ctx* ctx, const float* w, int kz, int kx, int ky, int l_min, int l_max,
+                          int mode, aprgpu_pyramid** out);
+int aprgpu_pyramid_create_explicit(aprgpu_ctx* ctx, const float* w, const int32_t* k3, int l_min, int l_max,
+                                   aprgpu_pyramid** out);
+int aprgpu_pyramid_free(aprgpu_pyramid* p);
+/* StencilPyramid::at (stencil.hpp:170-173): extents and (optionally) weights */
+int aprgpu_pyramid_level(const aprgpu_pyramid* p, int level, int32_t k3[3], float* w);
+
+/* ---- convolution ---------------------------------------------------------- */
+/* convolve_apr (convolve.hpp:220-303): out[n_particles] from values[n_particles]
+ * and tree_values[n_tree].  accum: APRGPU_ACCUM_EXACT (bit-identical to the
+ * reference) or APRGPU_ACCUM_FAST.  Errors: RANGE if the pyramid does not cover
+ * the APR levels (:224-225), CAPABILITY if an extent exceeds 13 (:226-230). */
+int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
+                    int pad_mode, int accum, float* out, int ptr_kind, void* stream);
+
+/* rl_apr (deconv.hpp:75-107): iterations of fill_tree -> conv(w) -> ratio ->
+ * fill_tree -> conv(flip w) -> multiply, all on the device.  psf is normalised
+ * like normalized_psf (:26-34).  epsilon <= 0 selects 1e-6 x mean(observed)
+ * (rl_epsilon, :36-38).  out[n_particles]. */
+int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, int kx, int ky, int iterations,
+              double epsilon, int accum, float* out, int ptr_kind, void* stream);
+
+/* Number of kernel launches this context issued since creation (bench.py's
+ * gpu_launches evidence). */
+int aprgpu_launch_count(aprgpu_ctx* ctx, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif

@@ -1,0 +1,537 @@
+// The C-ABI (include/aprgpu.h): contexts, structure upload/download, stencil
+// pyramids, and the host/device-pointer front doors of fill_tree, convolve_apr
+// and rl_apr.  Exceptions never cross this boundary; aprgpu::Error carries the
+// status code that the reference-side shim maps back to aprkit's exceptions.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return APRGPU_OK;
+    } catch (const aprgpu::Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = e.what();
+        return APRGPU_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return APRGPU_ERR_INVALID;
+    }
+}
+
+using aprgpu::fail;
+
+void need(bool cond, const char* what) {
+    if (!cond) fail(APRGPU_ERR_INVALID, what);
+}
+
+struct DeviceGuard {  // make the context's device current for the call
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int host_compute_l_max(int nz, int nx, int ny) {
+    const int m = std::max(nz, std::max(nx, ny));
+    int l = 0;
+    while ((1 << l) < m) ++l;
+    return l;
+}
+
+void upload_one(aprgpu_ctx* ctx, const aprgpu_access_desc* d, aprgpu::DevAccess& a) {
+    need(d != nullptr, "null access descriptor");
+    need(d->l_min >= 0 && d->l_min <= d->l_max, "l_min > l_max");
+    if (d->l_max >= aprgpu::kMaxLevels) fail(APRGPU_ERR_CAPABILITY, "too many levels");
+    need(d->z_dim && d->x_dim && d->y_dim && d->level_offset, "null dims");
+    need(d->n_rows == 0 || d->xz_end, "null xz_end");
+    need(d->n_particles == 0 || d->y_idx, "null y_idx");
+    a.l_min = d->l_min;
+    a.l_max = d->l_max;
+    a.zd.assign(d->z_dim, d->z_dim + d->l_max + 1);
+    a.xd.assign(d->x_dim, d->x_dim + d->l_max + 1);
+    a.yd.assign(d->y_dim, d->y_dim + d->l_max + 1);
+    a.level_offset.assign(d->level_offset, d->level_offset + d->l_max + 1);
+    uint64_t expect = 0;
+    for (int l = a.l_min; l <= a.l_max; ++l) {  // validate, apr.hpp:66-73
+        if (a.level_offset[l] != expect) fail(APRGPU_ERR_INTEGRITY, "level_offset mismatch");
+        if (a.yd[l] > 65536) fail(APRGPU_ERR_CAPABILITY, "y dimension exceeds the 16-bit index limit");
+        expect += static_cast<uint64_t>(a.zd[l]) * a.xd[l];
+    }
+    if (expect != d->n_rows) fail(APRGPU_ERR_INTEGRITY, "xz_end length does not match level grids");
+    if (d->n_rows >= (1ull << 32) - 1) fail(APRGPU_ERR_CAPABILITY, "row count exceeds u32");
+    a.n_particles = d->n_particles;
+    a.n_rows = d->n_rows;
+    APR_CUDA(cudaMalloc(&a.y, 2 * a.n_particles + 2));
+    if (a.n_particles)
+        APR_CUDA(cudaMemcpyAsync(a.y, d->y_idx, 2 * a.n_particles, cudaMemcpyHostToDevice, ctx->stream));
+    if (a.n_rows == 0 && a.n_particles) fail(APRGPU_ERR_INTEGRITY, "particles present but no rows");
+    aprgpu::build_row_begin(ctx, a, d->xz_end);
+    aprgpu::build_work_lists(ctx, a);
+}
+
+void free_apr(aprgpu_apr* apr) {
+    apr->leaf.release();
+    apr->tree.release();
+    for (aprgpu::GpuBuf* b : {&apr->vsum, &apr->wsum, &apr->h_in, &apr->h_tree, &apr->h_out, &apr->rl_u,
+                              &apr->rl_ratio, &apr->rl_tv, &apr->tmp})
+        b->release();
+}
+
+aprgpu::HostStencil make_host_stencil(const float* w, int kz, int kx, int ky) {
+    if (kz < 1 || kx < 1 || ky < 1 || kz % 2 == 0 || kx % 2 == 0 || ky % 2 == 0)
+        fail(APRGPU_ERR_RANGE, "stencil extents must be odd and positive");  // Stencil ctor, stencil.hpp:24-25
+    need(w != nullptr, "null stencil weights");
+    aprgpu::HostStencil s;
+    s.kz = kz;
+    s.kx = kx;
+    s.ky = ky;
+    s.w.assign(w, w + static_cast<size_t>(kz) * kx * ky);
+    return s;
+}
+
+void pyramid_upload(aprgpu_pyramid* p) {
+    DeviceGuard g(p->ctx->device);
+    const size_t n = p->w_host.size();
+    APR_CUDA(cudaMalloc(&p->w_dev, sizeof(float) * (n + 1)));
+    APR_CUDA(cudaMalloc(&p->wd_dev, sizeof(double) * (n + 1)));
+    std::vector<double> wd(p->w_host.begin(), p->w_host.end());
+    APR_CUDA(cudaMemcpy(p->w_dev, p->w_host.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+    APR_CUDA(cudaMemcpy(p->wd_dev, wd.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+}
+
+void push_level(aprgpu_pyramid* p, const aprgpu::HostStencil& s) {
+    p->off.push_back(p->w_host.size());
+    p->k3.insert(p->k3.end(), {s.kz, s.kx, s.ky});
+    p->w_host.insert(p->w_host.end(), s.w.begin(), s.w.end());
+}
+
+__global__ void k_clamp_copy(const float* __restrict__ in, float* __restrict__ u, float* __restrict__ est, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = in[i];
+        const float c = v < 0.0f ? 0.0f : v;  // std::max(v, 0.0f), deconv.hpp:89
+        u[i] = c;
+        est[i] = c;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* aprgpu_last_error(void) { return g_last_error.c_str(); }
+int aprgpu_version(void) { return 1; }
+
+int aprgpu_init(int device, aprgpu_ctx** out) {
+    return guard([&] {
+        need(out != nullptr, "null out");
+        int n = 0;
+        APR_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(APRGPU_ERR_RANGE, "no such CUDA device");
+        DeviceGuard g(device);
+        auto* c = new aprgpu_ctx;
+        c->device = device;
+        APR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        APR_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+        *out = c;
+    });
+}
+
+int aprgpu_ctx_free(aprgpu_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        DeviceGuard g(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int aprgpu_ctx_stream(aprgpu_ctx* ctx, void** stream_out) {
+    return guard([&] {
+        need(ctx && stream_out, "null argument");
+        *stream_out = ctx->stream;
+    });
+}
+
+int aprgpu_launch_count(aprgpu_ctx* ctx, uint64_t* out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        *out = ctx->launches.load();
+    });
+}
+
+int aprgpu_upload_access(aprgpu_ctx* ctx, const aprgpu_access_desc* leaf, const aprgpu_access_desc* tree,
+                         const int32_t source_dims[3], aprgpu_apr** out) {
+    aprgpu_apr* apr = nullptr;
+    int st = guard([&] {
+        need(ctx && leaf && source_dims && out, "null argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        apr = new aprgpu_apr;
+        apr->ctx = ctx;
+        for (int i = 0; i < 3; ++i) apr->dims[i] = source_dims[i];
+        if (source_dims[2] > 65536) fail(APRGPU_ERR_CAPABILITY, "y dimension exceeds the 16-bit index limit");
+        upload_one(ctx, leaf, apr->leaf);
+        apr->geom_l_max = std::max(apr->leaf.l_max, host_compute_l_max(source_dims[0], source_dims[1], source_dims[2]));
+        if (tree) {
+            upload_one(ctx, tree, apr->tree);
+            aprgpu::verify_tree_links(ctx, apr);
+        } else {
+            aprgpu::build_tree_structure(ctx, apr);
+        }
+        APR_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = apr;
+    });
+    if (st != APRGPU_OK && apr) {
+        free_apr(apr);
+        delete apr;
+    }
+    return st;
+}
+
+int aprgpu_apr_free(aprgpu_apr* apr) {
+    return guard([&] {
+        if (!apr) return;
+        DeviceGuard g(apr->ctx->device);
+        cudaStreamSynchronize(apr->ctx->stream);
+        free_apr(apr);
+        delete apr;
+    });
+}
+
+int aprgpu_apr_dims(const aprgpu_apr* apr, int32_t dims_out[3]) {
+    return guard([&] {
+        need(apr && dims_out, "null argument");
+        for (int i = 0; i < 3; ++i) dims_out[i] = apr->dims[i];
+    });
+}
+
+int aprgpu_access_get_info(const aprgpu_apr* apr, int which, aprgpu_access_info* out) {
+    return guard([&] {
+        need(apr && out, "null argument");
+        need(which == APRGPU_LEAF || which == APRGPU_TREE, "bad access selector");
+        const aprgpu::DevAccess& a = which == APRGPU_LEAF ? apr->leaf : apr->tree;
+        out->l_min = a.l_min;
+        out->l_max = a.l_max;
+        out->n_particles = a.n_particles;
+        out->n_rows = a.n_rows;
+    });
+}
+
+int aprgpu_download_access(const aprgpu_apr* apr, int which, uint16_t* y_idx, uint64_t* xz_end,
+                           uint64_t* level_offset, int32_t* z_dim, int32_t* x_dim, int32_t* y_dim) {
+    return guard([&] {
+        need(apr != nullptr, "null argument");
+        need(which == APRGPU_LEAF || which == APRGPU_TREE, "bad access selector");
+        DeviceGuard g(apr->ctx->device);
+        const aprgpu::DevAccess& a = which == APRGPU_LEAF ? apr->leaf : apr->tree;
+        cudaStream_t s = apr->ctx->stream;
+        if (y_idx && a.n_particles) APR_CUDA(cudaMemcpyAsync(y_idx, a.y, 2 * a.n_particles, cudaMemcpyDeviceToHost, s));
+        if (xz_end && a.n_rows) {
+            std::vector<uint32_t> rb(a.n_rows + 1);
+            APR_CUDA(cudaMemcpyAsync(rb.data(), a.rb, 4 * (a.n_rows + 1), cudaMemcpyDeviceToHost, s));
+            APR_CUDA(cudaStreamSynchronize(s));
+            for (uint64_t r = 0; r < a.n_rows; ++r) xz_end[r] = rb[r + 1];
+        }
+        APR_CUDA(cudaStreamSynchronize(s));
+        for (int l = 0; l <= a.l_max; ++l) {
+            if (level_offset) level_offset[l] = a.level_offset[l];
+            if (z_dim) z_dim[l] = a.zd[l];
+            if (x_dim) x_dim[l] = a.xd[l];
+            if (y_dim) y_dim[l] = a.yd[l];
+        }
+    });
+}
+
+int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, uint16_t* y_min, uint16_t* y_max,
+                     uint64_t cap, uint64_t* count) {
+    return guard([&] {
+        need(apr && count, "null argument");
+        const aprgpu::DevAccess& a = apr->leaf;
+        if (level < a.l_min || level > a.l_max) fail(APRGPU_ERR_RANGE, "row_index: level out of range");
+        DeviceGuard g(apr->ctx->device);
+        *count = a.work_off[level + 1] - a.work_off[level];
+        if (z && x && y_min && y_max && cap) aprgpu::row_spans(apr->ctx, a, level, z, x, y_min, y_max, cap);
+    });
+}
+
+int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream) {
+    return guard([&] {
+        need(apr && leaf && (tree || apr->tree.n_particles == 0), "null argument");
+        DeviceGuard g(apr->ctx->device);
+        cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
+        const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
+        if (ptr_kind == APRGPU_DEVICE) {
+            aprgpu::fill_tree_device(apr, leaf, tree, s);
+            return;
+        }
+        need(ptr_kind == APRGPU_HOST, "bad pointer kind");
+        apr->h_in.ensure(4 * np + 4);
+        apr->h_tree.ensure(4 * nt + 4);
+        APR_CUDA(cudaMemcpyAsync(apr->h_in.p, leaf, 4 * np, cudaMemcpyHostToDevice, s));
+        aprgpu::fill_tree_device(apr, apr->h_in.as<float>(), apr->h_tree.as<float>(), s);
+        if (nt) APR_CUDA(cudaMemcpyAsync(tree, apr->h_tree.p, 4 * nt, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int aprgpu_restrict_stencil(const float* w, int kz, int kx, int ky, int delta, int32_t out_k3[3], float* out) {
+    return guard([&] {
+        need(out_k3 != nullptr, "null argument");
+        const aprgpu::HostStencil r = aprgpu::restrict_stencil_host(make_host_stencil(w, kz, kx, ky), delta);
+        out_k3[0] = r.kz;
+        out_k3[1] = r.kx;
+        out_k3[2] = r.ky;
+        if (out) std::memcpy(out, r.w.data(), sizeof(float) * r.w.size());
+    });
+}
+
+int aprgpu_gaussian_stencil(double sigma, int size, int32_t* k_out, float* out) {
+    return guard([&] {
+        const aprgpu::HostStencil s = aprgpu::gaussian_stencil_host(sigma, size);
+        if (k_out) *k_out = s.kz;
+        if (out) std::memcpy(out, s.w.data(), sizeof(float) * s.w.size());
+    });
+}
+
+int aprgpu_box_stencil(int k, float* out) {
+    return guard([&] {
+        if (k < 1 || k % 2 == 0) fail(APRGPU_ERR_RANGE, "stencil extents must be odd and positive");
+        need(out != nullptr, "null argument");
+        const float v = 1.0f / static_cast<float>(k) / k / k;  // stencil.hpp:52-55
+        for (int i = 0; i < k * k * k; ++i) out[i] = v;
+    });
+}
+
+int aprgpu_sobel_stencil(int axis, float* out) {
+    return guard([&] {
+        if (axis < 0 || axis > 2) fail(APRGPU_ERR_RANGE, "sobel axis must be 0, 1 or 2");
+        need(out != nullptr, "null argument");
+        static const double smooth[3] = {0.25, 0.5, 0.25};
+        static const double diff[3] = {-0.5, 0.0, 0.5};
+        for (int a = 0; a < 3; ++a)  // stencil.hpp:83-98
+            for (int b = 0; b < 3; ++b)
+                for (int c = 0; c < 3; ++c) {
+                    const double wz = axis == 0 ? diff[a] : smooth[a];
+                    const double wx = axis == 1 ? diff[b] : smooth[b];
+                    const double wy = axis == 2 ? diff[c] : smooth[c];
+                    out[(a * 3 + b) * 3 + c] = static_cast<float>(wz * wx * wy);
+                }
+    });
+}
+
+int aprgpu_pyramid_create(aprgpu_ctx* ctx, const float* w, int kz, int kx, int ky, int l_min, int l_max, int mode,
+                          aprgpu_pyramid** out) {
+    aprgpu_pyramid* p = nullptr;
+    int st = guard([&] {
+        need(ctx && out, "null argument");
+        need(l_min >= 0 && l_min <= l_max && l_max < aprgpu::kMaxLevels, "bad level range");
+        const aprgpu::HostStencil base = make_host_stencil(w, kz, kx, ky);
+        p = new aprgpu_pyramid;
+        p->ctx = ctx;
+        p->l_min = l_min;
+        p->l_max = l_max;
+        p->mode = mode;
+        for (int l = l_min; l <= l_max; ++l) {  // make_pyramid, stencil.hpp:176-191
+            const int delta = l_max - l;
+            if (mode == APRGPU_PYR_RESTRICTED) {
+                push_level(p, aprgpu::restrict_stencil_host(base, delta));
+            } else if (mode == APRGPU_PYR_RESCALED) {
+                aprgpu::HostStencil r = base;  // rescale_stencil, stencil.hpp:114-120
+                const float scale = std::ldexp(1.0f, -delta);
+                for (float& v : r.w) v *= scale;
+                push_level(p, r);
+            } else if (mode == APRGPU_PYR_UNIFORM || mode == APRGPU_PYR_EXPLICIT) {
+                push_level(p, base);
+            } else {
+                fail(APRGPU_ERR_INVALID, "unknown pyramid mode");
+            }
+        }
+        pyramid_upload(p);
+        *out = p;
+    });
+    if (st != APRGPU_OK && p) aprgpu_pyramid_free(p);
+    return st;
+}
+
+int aprgpu_pyramid_create_explicit(aprgpu_ctx* ctx, const float* w, const int32_t* k3, int l_min, int l_max,
+                                   aprgpu_pyramid** out) {
+    aprgpu_pyramid* p = nullptr;
+    int st = guard([&] {
+        need(ctx && w && k3 && out, "null argument");
+        need(l_min >= 0 && l_min <= l_max && l_max < aprgpu::kMaxLevels, "bad level range");
+        p = new aprgpu_pyramid;
+        p->ctx = ctx;
+        p->l_min = l_min;
+        p->l_max = l_max;
+        p->mode = APRGPU_PYR_EXPLICIT;
+        size_t off = 0;
+        for (int l = l_min; l <= l_max; ++l) {
+            const int32_t* k = k3 + 3 * (l - l_min);
+            aprgpu::HostStencil s = make_host_stencil(w + off, k[0], k[1], k[2]);
+            off += s.w.size();
+            push_level(p, s);
+        }
+        pyramid_upload(p);
+        *out = p;
+    });
+    if (st != APRGPU_OK && p) aprgpu_pyramid_free(p);
+    return st;
+}
+
+int aprgpu_pyramid_free(aprgpu_pyramid* p) {
+    return guard([&] {
+        if (!p) return;
+        cudaFree(p->w_dev);
+        cudaFree(p->wd_dev);
+        delete p;
+    });
+}
+
+int aprgpu_pyramid_level(const aprgpu_pyramid* p, int level, int32_t k3[3], float* w) {
+    return guard([&] {
+        need(p && k3, "null argument");
+        if (level < p->l_min || level > p->l_max) fail(APRGPU_ERR_RANGE, "StencilPyramid: level out of range");
+        const int li = level - p->l_min;
+        for (int i = 0; i < 3; ++i) k3[i] = p->k3[3 * li + i];
+        if (w) {
+            const size_t n = static_cast<size_t>(k3[0]) * k3[1] * k3[2];
+            std::memcpy(w, p->w_host.data() + p->off[li], sizeof(float) * n);
+        }
+    });
+}
+
+int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
+                    int pad_mode, int accum, float* out, int ptr_kind, void* stream) {
+    return guard([&] {
+        need(apr && values && pyr && out, "null argument");
+        need(tree_values || apr->tree.n_particles == 0, "tree values are required");
+        need(pad_mode == APRGPU_PAD_ZERO || pad_mode == APRGPU_PAD_REFLECT, "bad pad mode");
+        need(accum == APRGPU_ACCUM_EXACT || accum == APRGPU_ACCUM_FAST, "bad accumulation mode");
+        need(pyr->ctx == apr->ctx, "pyramid belongs to another context");
+        DeviceGuard g(apr->ctx->device);
+        aprgpu::check_pyramid(apr, pyr);
+        cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
+        const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
+        aprgpu::EpiArgs epi;
+        if (ptr_kind == APRGPU_DEVICE) {
+            aprgpu::convolve_device(apr, values, tree_values, pyr, pad_mode, accum, out, epi, s);
+            return;
+        }
+        need(ptr_kind == APRGPU_HOST, "bad pointer kind");
+        apr->h_in.ensure(4 * np + 4);
+        apr->h_tree.ensure(4 * nt + 4);
+        apr->h_out.ensure(4 * np + 4);
+        APR_CUDA(cudaMemcpyAsync(apr->h_in.p, values, 4 * np, cudaMemcpyHostToDevice, s));
+        if (nt) APR_CUDA(cudaMemcpyAsync(apr->h_tree.p, tree_values, 4 * nt, cudaMemcpyHostToDevice, s));
+        aprgpu::convolve_device(apr, apr->h_in.as<float>(), apr->h_tree.as<float>(), pyr, pad_mode, accum,
+                                apr->h_out.as<float>(), epi, s);
+        APR_CUDA(cudaMemcpyAsync(out, apr->h_out.p, 4 * np, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, int kx, int ky, int iterations,
+              double epsilon, int accum, float* out, int ptr_kind, void* stream) {
+    return guard([&] {
+        need(apr && observed && psf && out, "null argument");
+        need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
+        need(accum == APRGPU_ACCUM_EXACT || accum == APRGPU_ACCUM_FAST, "bad accumulation mode");
+        DeviceGuard g(apr->ctx->device);
+        aprgpu_ctx* ctx = apr->ctx;
+        cudaStream_t s = aprgpu::pick_stream(ctx, stream);
+        // normalized_psf (deconv.hpp:26-34)
+        aprgpu::HostStencil w = make_host_stencil(psf, kz, kx, ky);
+        for (float v : w.w)
+            if (v < 0.0f) fail(APRGPU_ERR_RANGE, "RL psf weights must be non-negative");
+        double sum = 0.0;
+        for (float v : w.w) sum += v;
+        if (sum <= 0.0) fail(APRGPU_ERR_RANGE, "RL psf must have positive sum");
+        for (float& v : w.w) v = static_cast<float>(v / sum);
+        aprgpu::HostStencil wt = w;  // flip_stencil, stencil.hpp:101-110
+        for (int a = 0; a < kz; ++a)
+            for (int b = 0; b < kx; ++b)
+                for (int c = 0; c < ky; ++c)
+                    wt.w[(static_cast<size_t>(kz - 1 - a) * kx + (kx - 1 - b)) * ky + (ky - 1 - c)] =
+                        w.w[(static_cast<size_t>(a) * kx + b) * ky + c];
+        const int l_min = apr->leaf.l_min, l_max = apr->leaf.l_max;
+        aprgpu_pyramid *pw = nullptr, *pwt = nullptr;
+        int st = aprgpu_pyramid_create(ctx, w.w.data(), kz, kx, ky, l_min, l_max, APRGPU_PYR_RESTRICTED, &pw);
+        if (st) fail(st, g_last_error);
+        st = aprgpu_pyramid_create(ctx, wt.w.data(), kz, kx, ky, l_min, l_max, APRGPU_PYR_RESTRICTED, &pwt);
+        if (st) {
+            aprgpu_pyramid_free(pw);
+            fail(st, g_last_error);
+        }
+        const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
+        // clamped observations u and the running estimate
+        apr->rl_u.ensure(4 * np + 4);
+        apr->rl_ratio.ensure(4 * np + 4);
+        apr->rl_tv.ensure(4 * nt + 4);
+        apr->h_out.ensure(4 * np + 4);
+        std::vector<float> host_obs;
+        const float* obs_dev = observed;
+        if (ptr_kind == APRGPU_HOST) {
+            apr->h_in.ensure(4 * np + 4);
+            APR_CUDA(cudaMemcpyAsync(apr->h_in.p, observed, 4 * np, cudaMemcpyHostToDevice, s));
+            obs_dev = apr->h_in.as<float>();
+        }
+        float* est = ptr_kind == APRGPU_DEVICE ? out : apr->h_out.as<float>();
+        float* u = apr->rl_u.as<float>();
+        k_clamp_copy<<<std::min<unsigned>(aprgpu::blocks_for(np, 256), ctx->sm_count * 8), 256, 0, s>>>(obs_dev, u, est,
+                                                                                                       np);
+        aprgpu::count_launch(ctx);
+        APR_CUDA(cudaGetLastError());
+        // mean of the clamped observations in the reference's sequential order (deconv.hpp:90-92)
+        host_obs.resize(np);
+        APR_CUDA(cudaMemcpyAsync(host_obs.data(), u, 4 * np, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+        double mean = 0.0;
+        for (float v : host_obs) mean += v;
+        mean /= static_cast<double>(std::max<uint64_t>(np, 1));
+        const double eps = epsilon > 0.0 ? epsilon : 1e-6 * std::max(mean, 1e-30);  // rl_epsilon, deconv.hpp:36-38
+        float* ratio = apr->rl_ratio.as<float>();
+        float* tv = apr->rl_tv.as<float>();
+        try {
+            for (int k = 1; k <= iterations; ++k) {
+                aprgpu::fill_tree_device(apr, est, tv, s);
+                aprgpu::EpiArgs e1;
+                e1.mode = aprgpu::EPI_RL_RATIO;
+                e1.u = u;
+                e1.eps = eps;
+                aprgpu::convolve_device(apr, est, tv, pw, APRGPU_PAD_REFLECT, accum, ratio, e1, s);
+                aprgpu::fill_tree_device(apr, ratio, tv, s);
+                aprgpu::EpiArgs e2;
+                e2.mode = aprgpu::EPI_RL_MULT;
+                e2.est = est;
+                aprgpu::convolve_device(apr, ratio, tv, pwt, APRGPU_PAD_REFLECT, accum, nullptr, e2, s);
+            }
+        } catch (...) {
+            aprgpu_pyramid_free(pw);
+            aprgpu_pyramid_free(pwt);
+            throw;
+        }
+        if (ptr_kind == APRGPU_HOST) APR_CUDA(cudaMemcpyAsync(out, est, 4 * np, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+        aprgpu_pyramid_free(pw);
+        aprgpu_pyramid_free(pwt);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// Internal declarations shared by the aprgpu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "aprgpu.h"
+
+namespace aprgpu {
+
+constexpr int kMaxLevels = APRGPU_MAX_LEVELS;
+constexpr int kMaxExtent = APRGPU_MAX_EXTENT;
+
+// ---- errors: thrown inside the library, converted to status at the C-ABI ----
+struct Error : std::runtime_error {
+    int status;
+    Error(int st, const std::string& m) : std::runtime_error(m), status(st) {}
+};
+[[noreturn]] inline void fail(int st, const std::string& m) { throw Error(st, m); }
+
+#define APR_CUDA(expr)                                                                             \
+    do {                                                                                           \
+        cudaError_t e__ = (expr);                                                                  \
+        if (e__ != cudaSuccess) {                                                                  \
+            if (e__ == cudaErrorMemoryAllocation)                                                  \
+                ::aprgpu::fail(APRGPU_ERR_OOM, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+            ::aprgpu::fail(APRGPU_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__));  \
+        }                                                                                          \
+    } while (0)
+
+// ---- device-resident access structure ---------------------------------------
+// Per level: grid dims and the index of the level's first row.  Row r of the
+// structure covers particles [rb[r], rb[r+1]) -- the reference's xz_end shifted
+// by one with a leading 0 (so no row-0 branch), narrowed to u32.
+struct LevelG {
+    int zd, xd, yd;
+    uint32_t row0;
+};
+
+struct AccessView {  // passed by value to kernels
+    const uint16_t* y;
+    const uint32_t* rb;
+    int l_min, l_max;
+    LevelG g[kMaxLevels];
+};
+
+struct DevAccess {
+    int l_min = 0, l_max = 0;
+    std::vector<int> zd, xd, yd;           // l_max+1
+    std::vector<uint64_t> level_offset;    // l_max+1
+    uint64_t n_particles = 0, n_rows = 0;
+    uint16_t* y = nullptr;                 // device [n_particles]
+    uint32_t* rb = nullptr;                // device [n_rows+1]
+    // per-level non-empty rows (global row ids), ascending == (z,x) order
+    uint32_t* work = nullptr;              // device
+    std::vector<uint64_t> work_off;        // l_max+2 offsets into work
+    AccessView view() const;
+    void release();
+};
+
+struct GpuBuf {  // trivially owned device allocation
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t n);
+    void release();
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace aprgpu
+
+struct aprgpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    std::atomic<uint64_t> launches{0};
+    int sm_count = 148;
+};
+
+struct aprgpu_apr {
+    aprgpu_ctx* ctx = nullptr;
+    int dims[3] = {0, 0, 0};
+    int geom_l_max = 0;
+    aprgpu::DevAccess leaf, tree;
+    // scratch (grown on demand)
+    aprgpu::GpuBuf vsum, wsum;             // fill_tree fp64 sums [n_tree]
+    aprgpu::GpuBuf h_in, h_tree, h_out;    // staging for host-pointer calls
+    aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
+    aprgpu::GpuBuf tmp;                    // misc
+};
+
+struct aprgpu_pyramid {
+    aprgpu_ctx* ctx = nullptr;
+    int l_min = 0, l_max = 0, mode = 0;
+    std::vector<int> k3;                   // 3 per level
+    std::vector<float> w_host;             // all weights, level by level
+    std::vector<uint64_t> off;             // per level offset into w_host
+    float* w_dev = nullptr;                // device copy (float)
+    double* wd_dev = nullptr;              // device copy (double)
+};
+
+namespace aprgpu {
+
+// launches.cu / index.cu
+void build_row_begin(aprgpu_ctx* ctx, DevAccess& a, const uint64_t* xz_end_host);
+void build_work_lists(aprgpu_ctx* ctx, DevAccess& a);
+void row_spans(aprgpu_ctx* ctx, const DevAccess& a, int level, int32_t* z, int32_t* x, uint16_t* ymin,
+               uint16_t* ymax, uint64_t cap);
+
+// tree.cu
+void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr);
+void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr);
+void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s);
+
+// conv.cu
+enum Epilogue { EPI_STORE = 0, EPI_RL_RATIO = 1, EPI_RL_MULT = 2 };
+struct EpiArgs {
+    int mode = EPI_STORE;
+    const float* u = nullptr;  // RL observed (ratio epilogue)
+    double eps = 0.0;
+    float* est = nullptr;      // RL estimate (multiply epilogue; also the output)
+};
+void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
+                     int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s);
+void check_pyramid(const aprgpu_apr* apr, const aprgpu_pyramid* pyr);
+
+// stencil.cpp (host)
+struct HostStencil {
+    int kz = 1, kx = 1, ky = 1;
+    std::vector<float> w;
+};
+HostStencil restrict_stencil_host(const HostStencil& w, int delta);
+HostStencil gaussian_stencil_host(double sigma, int size);
+
+inline void count_launch(aprgpu_ctx* ctx, uint64_t n = 1) { ctx->launches.fetch_add(n, std::memory_order_relaxed); }
+
+inline cudaStream_t pick_stream(aprgpu_ctx* ctx, void* s) {
+    return s ? static_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+inline unsigned blocks_for(uint64_t n, unsigned per) { return static_cast<unsigned>((n + per - 1) / per); }
+
+}  // namespace aprgpu

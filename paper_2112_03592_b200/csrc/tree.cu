@@ -1,0 +1,432 @@
+// APR tree on the device: structure (init_tree_structure, tree.hpp:26-82),
+// parent-link verification (synchronized_parent_pass, tree.hpp:88-103) and the
+// footprint-weighted fill (fill_tree, tree.hpp:110-150).
+//
+// Structure: level by level from l_max-1 down, one warp per parent row merges
+// the y/2 values of its <= 8 child rows (4 leaf rows + 4 interior rows of the
+// level below) through a shared-memory bitmap; a count pass, an exclusive scan
+// and a fill pass produce the CSR rows.  Sets are order-free, so the result is
+// bit-identical to the reference's push/sort/unique.
+//
+// Fill: level by level from the finest interior level, one warp per non-empty
+// parent row, one lane per parent node.  Each node gathers its children in the
+// reference's exact accumulation order -- for (cz,cx) in lexicographic order:
+// leaf children y=2py, 2py+1, then interior children y=2py, 2py+1 -- with
+// explicit fp64 round-to-nearest multiplies/adds (no FMA contraction), so the
+// fp64 sums and the final float(vsum/wsum) are bit-identical to the reference.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+namespace aprgpu {
+namespace {
+
+constexpr int kTreeWarps = 8;
+constexpr int kBitmapWords = 1024;  // 32768 bits: every parent y (< 32768) fits
+
+struct ChildSrc {
+    AccessView leaf;
+    int leaf_ok;                 // child level is a leaf level
+    const uint32_t* trb;         // interior child level (level-local row begins), or null
+    const uint16_t* ty;
+    int czd, cxd;                // child grid dims (reference geometry, glm)
+    int ctxd;                    // x dim of the interior child level
+};
+
+// mode 0: counts[r] = |row|; mode 1: out_y[prb[r] ...] = sorted row
+__global__ void __launch_bounds__(kTreeWarps * 32) k_tree_level(int mode, ChildSrc cs, int child_l, int zd, int xd,
+                                                                  uint32_t* __restrict__ counts,
+                                                                  const uint32_t* __restrict__ prb,
+                                                                  uint16_t* __restrict__ out_y) {
+    __shared__ uint32_t bm_all[kTreeWarps][kBitmapWords];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    uint32_t* bm = bm_all[wib];
+    const uint64_t n_rows = static_cast<uint64_t>(zd) * xd;
+    for (uint64_t r = blockIdx.x * (uint64_t)kTreeWarps + wib; r < n_rows; r += (uint64_t)gridDim.x * kTreeWarps) {
+        const int z = static_cast<int>(r / xd), x = static_cast<int>(r % xd);
+        // lanes 0..7 describe the child lists: k<4 leaf rows, k>=4 interior rows
+        uint32_t lb = 0, le = 0;
+        int src = 0;
+        if (lane < 8) {
+            const int k = lane & 3;
+            const int cz = 2 * z + (k >> 1), cx = 2 * x + (k & 1);
+            if (cz < cs.czd && cx < cs.cxd) {
+                if (lane < 4 && cs.leaf_ok) {
+                    const uint32_t row = cs.leaf.g[child_l].row0 + static_cast<uint32_t>(cz) * cs.leaf.g[child_l].xd + cx;
+                    lb = cs.leaf.rb[row];
+                    le = cs.leaf.rb[row + 1];
+                    src = 0;
+                } else if (lane >= 4 && cs.trb) {
+                    const uint32_t row = static_cast<uint32_t>(cz) * cs.ctxd + cx;
+                    lb = cs.trb[row];
+                    le = cs.trb[row + 1];
+                    src = 1;
+                }
+            }
+        }
+        int mn = 1 << 30, mx = -1;
+        if (le > lb) {
+            const uint16_t* ys = src ? cs.ty : cs.leaf.y;
+            mn = ys[lb] >> 1;
+            mx = ys[le - 1] >> 1;
+        }
+        mn = warp_min(mn);
+        mx = warp_max(mx);
+        if (mx < 0) {
+            if (mode == 0 && lane == 0) counts[r] = 0;
+            continue;
+        }
+        const int nwords = ((mx - mn) >> 5) + 1;
+        for (int w = lane; w < nwords; w += 32) bm[w] = 0;
+        __syncwarp();
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t b = __shfl_sync(kFull, lb, k), e = __shfl_sync(kFull, le, k);
+            const int sk = __shfl_sync(kFull, src, k);
+            const uint16_t* ys = sk ? cs.ty : cs.leaf.y;
+            for (uint32_t i = b + lane; i < e; i += 32) {
+                const int v = (ys[i] >> 1) - mn;
+                atomicOr(&bm[v >> 5], 1u << (v & 31));
+            }
+        }
+        __syncwarp();
+        if (mode == 0) {
+            int c = 0;
+            for (int w = lane; w < nwords; w += 32) c += __popc(bm[w]);
+            c = warp_sum(c);
+            if (lane == 0) counts[r] = static_cast<uint32_t>(c);
+        } else {
+            uint32_t base = prb[r];
+            for (int w0 = 0; w0 < nwords; w0 += 32) {
+                const int w = w0 + lane;
+                uint32_t word = w < nwords ? bm[w] : 0u;
+                const int pc = __popc(word);
+                const int incl = warp_incl_scan(pc, lane);
+                uint32_t pos = base + incl - pc;
+                while (word) {
+                    const int bit = __ffs(word) - 1;
+                    out_y[pos++] = static_cast<uint16_t>(mn + (w << 5) + bit);
+                    word &= word - 1;
+                }
+                base += __shfl_sync(kFull, incl, 31);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_assemble_rb(const uint32_t* __restrict__ local, uint64_t rows, uint32_t row0, uint32_t poff,
+                              uint32_t* __restrict__ rb) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x)
+        rb[row0 + r + 1] = poff + local[r + 1];
+}
+
+// IntegrityError check of synchronized_parent_pass (tree.hpp:96-100): every
+// child (leaf at level c, or interior node at level c) has its parent y/2 in
+// interior row (c-1, z/2, x/2).
+__global__ void k_verify_links(AccessView child, AccessView tree, int c, uint64_t n_rows, int* bad) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const LevelG g = child.g[c];
+    const LevelG pg = tree.g[c - 1];
+    for (uint64_t r = warp; r < n_rows; r += nwarps) {
+        const int z = static_cast<int>(r / g.xd), x = static_cast<int>(r % g.xd);
+        const uint32_t b = child.rb[g.row0 + r], e = child.rb[g.row0 + r + 1];
+        if (b == e) continue;
+        if ((z >> 1) >= pg.zd || (x >> 1) >= pg.xd) {
+            if (lane == 0) atomicOr(bad, 1);
+            continue;
+        }
+        const uint32_t prow = pg.row0 + static_cast<uint32_t>(z >> 1) * pg.xd + (x >> 1);
+        const uint32_t pb = tree.rb[prow], pe = tree.rb[prow + 1];
+        for (uint32_t i = b + lane; i < e; i += 32) {
+            const int t = child.y[i] >> 1;
+            const uint32_t j = lower_bound_u16(tree.y, pb, pe, t);
+            if (j == pe || tree.y[j] != t) atomicOr(bad, 1);
+        }
+    }
+}
+
+__device__ __forceinline__ double footprint_dev(int l, int iz, int ix, int iy, int glm, int nz, int nx, int ny) {
+    // cell_footprint_volume (tree.hpp:15-22)
+    const int s = 1 << (glm - l);
+    const double dz = min((iz + 1) * s, nz) - iz * s;
+    const double dx = min((ix + 1) * s, nx) - ix * s;
+    const double dy = min((iy + 1) * s, ny) - iy * s;
+    return __dmul_rn(__dmul_rn(dz, dx), dy);
+}
+
+struct FillArgs {
+    AccessView leaf, tree;
+    const float* leaf_v;
+    double* vsum;
+    double* wsum;
+    const uint32_t* work;  // non-empty interior rows at level lt
+    uint64_t n_work;
+    int lt, c, leaf_ok, tree_ok;  // c = lt+1; children are leaves / interior nodes
+    int czd, cxd, glm, nz, nx, ny;
+};
+
+__global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const LevelG pg = a.tree.g[a.lt];
+    for (uint64_t wi = warp; wi < a.n_work; wi += nwarps) {
+        const uint32_t prow = a.work[wi];
+        const uint32_t loc = prow - pg.row0;
+        const int pz = static_cast<int>(loc / pg.xd), px = static_cast<int>(loc % pg.xd);
+        const uint32_t pb = a.tree.rb[prow], pe = a.tree.rb[prow + 1];
+        // child row ranges (4 leaf + 4 interior), held by lanes 0..7 and broadcast
+        uint32_t cb = 0, ce = 0;
+        if (lane < 8) {
+            const int k = lane & 3;
+            const int cz = 2 * pz + (k >> 1), cx = 2 * px + (k & 1);
+            if (cz < a.czd && cx < a.cxd) {
+                if (lane < 4 && a.leaf_ok) {
+                    const LevelG g = a.leaf.g[a.c];
+                    const uint32_t row = g.row0 + static_cast<uint32_t>(cz) * g.xd + cx;
+                    cb = a.leaf.rb[row];
+                    ce = a.leaf.rb[row + 1];
+                } else if (lane >= 4 && a.tree_ok) {
+                    const LevelG g = a.tree.g[a.c];
+                    const uint32_t row = g.row0 + static_cast<uint32_t>(cz) * g.xd + cx;
+                    cb = a.tree.rb[row];
+                    ce = a.tree.rb[row + 1];
+                }
+            }
+        }
+        uint32_t rbk[8], rek[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            rbk[k] = __shfl_sync(kFull, cb, k);
+            rek[k] = __shfl_sync(kFull, ce, k);
+        }
+        for (uint32_t j = pb + lane; j < pe; j += 32) {
+            const int py = a.tree.y[j];
+            const int y0 = 2 * py;
+            double vs = 0.0, ws = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int cz = 2 * pz + (k >> 1), cx = 2 * px + (k & 1);
+                // leaf children (tree.hpp:124-132): w * value, w = clipped footprint
+                if (rek[k] > rbk[k]) {
+                    uint32_t i = lower_bound_u16(a.leaf.y, rbk[k], rek[k], y0);
+                    for (int t = 0; t < 2 && i < rek[k]; ++t) {
+                        const int yy = a.leaf.y[i];
+                        if (yy == y0 + t) {
+                            const double w = footprint_dev(a.c, cz, cx, yy, a.glm, a.nz, a.nx, a.ny);
+                            vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[i])));
+                            ws = __dadd_rn(ws, w);
+                            ++i;
+                        }
+                    }
+                }
+                // interior children (tree.hpp:133-139): their own fp64 sums
+                if (rek[k + 4] > rbk[k + 4]) {
+                    uint32_t i = lower_bound_u16(a.tree.y, rbk[k + 4], rek[k + 4], y0);
+                    for (int t = 0; t < 2 && i < rek[k + 4]; ++t) {
+                        const int yy = a.tree.y[i];
+                        if (yy == y0 + t) {
+                            vs = __dadd_rn(vs, a.vsum[i]);
+                            ws = __dadd_rn(ws, a.wsum[i]);
+                            ++i;
+                        }
+                    }
+                }
+            }
+            a.vsum[j] = vs;
+            a.wsum[j] = ws;
+        }
+    }
+}
+
+__global__ void k_tree_finalize(const double* __restrict__ vsum, const double* __restrict__ wsum, uint64_t n,
+                                float* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double w = wsum[i];
+        out[i] = w > 0.0 ? __double2float_rn(__ddiv_rn(vsum[i], w)) : 0.0f;  // tree.hpp:146-148
+    }
+}
+
+int compute_l_max_host(int nz, int nx, int ny) {
+    const int m = std::max(nz, std::max(nx, ny));
+    int l = 0;
+    while ((1 << l) < m) ++l;
+    return l;
+}
+
+}  // namespace
+
+void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr) {
+    cudaStream_t s = ctx->stream;
+    const DevAccess& L = apr->leaf;
+    DevAccess& T = apr->tree;
+    const int glm = L.l_max;
+    const int* d = apr->dims;
+    const int tmax = L.l_max - 1;
+    const int tmin = std::max(L.l_min - 1, 0);
+    if (tmax < tmin) {  // tree.hpp:31-42: single-cell domain, no interior nodes
+        T.l_min = T.l_max = 0;
+        T.zd = {grid_dim_dev(d[0], glm, 0)};
+        T.xd = {grid_dim_dev(d[1], glm, 0)};
+        T.yd = {grid_dim_dev(d[2], glm, 0)};
+        T.level_offset = {0};
+        T.n_rows = static_cast<uint64_t>(T.zd[0]) * T.xd[0];
+        T.n_particles = 0;
+        APR_CUDA(cudaMalloc(&T.y, 2));
+        APR_CUDA(cudaMalloc(&T.rb, sizeof(uint32_t) * (T.n_rows + 1)));
+        APR_CUDA(cudaMemsetAsync(T.rb, 0, sizeof(uint32_t) * (T.n_rows + 1), s));
+        build_work_lists(ctx, T);
+        return;
+    }
+    const int geom = std::max(tmax, compute_l_max_host(d[0], d[1], d[2]));  // assemble_access, linear_access.hpp:110
+    // per-level temporaries (level-local row begins + y)
+    std::vector<GpuBuf> lrb(tmax + 1), ly(tmax + 1);
+    std::vector<uint64_t> lcount(tmax + 1, 0);
+    GpuBuf counts, scan_tmp;
+    const AccessView lv = L.view();
+    for (int lt = tmax; lt >= tmin; --lt) {
+        const int zd = grid_dim_dev(d[0], glm, lt), xd = grid_dim_dev(d[1], glm, lt);
+        if (grid_dim_dev(d[0], geom, lt) != zd || grid_dim_dev(d[1], geom, lt) != xd)
+            fail(APRGPU_ERR_RANGE, "assemble_access: row list does not match level grids");
+        const int c = lt + 1;
+        const uint64_t rows = static_cast<uint64_t>(zd) * xd;
+        ChildSrc cs{};
+        cs.leaf = lv;
+        cs.leaf_ok = (c >= L.l_min && c <= L.l_max) ? 1 : 0;
+        cs.czd = grid_dim_dev(d[0], glm, c);
+        cs.cxd = grid_dim_dev(d[1], glm, c);
+        if (c <= tmax) {
+            cs.trb = lrb[c].as<uint32_t>();
+            cs.ty = ly[c].as<uint16_t>();
+            cs.ctxd = grid_dim_dev(d[1], glm, c);
+        }
+        counts.ensure(sizeof(uint32_t) * (rows + 1));
+        lrb[lt].ensure(sizeof(uint32_t) * (rows + 1));
+        APR_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(uint32_t) * (rows + 1), s));
+        const unsigned grid = std::min<unsigned>(blocks_for(rows, kTreeWarps), ctx->sm_count * 8);
+        k_tree_level<<<grid, kTreeWarps * 32, 0, s>>>(0, cs, c, zd, xd, counts.as<uint32_t>(), nullptr, nullptr);
+        APR_CUDA(cudaGetLastError());
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.as<uint32_t>(), lrb[lt].as<uint32_t>(),
+                                      static_cast<int64_t>(rows + 1), s);
+        scan_tmp.ensure(tb + 16);
+        tb = scan_tmp.bytes;
+        APR_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.p, tb, counts.as<uint32_t>(), lrb[lt].as<uint32_t>(),
+                                               static_cast<int64_t>(rows + 1), s));
+        uint32_t total = 0;
+        APR_CUDA(cudaMemcpyAsync(&total, lrb[lt].as<uint32_t>() + rows, 4, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+        lcount[lt] = total;
+        ly[lt].ensure(2ull * total + 2);
+        k_tree_level<<<grid, kTreeWarps * 32, 0, s>>>(1, cs, c, zd, xd, nullptr, lrb[lt].as<uint32_t>(),
+                                                      ly[lt].as<uint16_t>());
+        APR_CUDA(cudaGetLastError());
+        count_launch(ctx, 3);
+    }
+    // assemble levels tmin..tmax (assemble_access, linear_access.hpp:101-130)
+    T.l_min = tmin;
+    T.l_max = tmax;
+    T.zd.assign(tmax + 1, 0);
+    T.xd.assign(tmax + 1, 0);
+    T.yd.assign(tmax + 1, 0);
+    T.level_offset.assign(tmax + 1, 0);
+    uint64_t nrow = 0, np = 0;
+    for (int lt = tmin; lt <= tmax; ++lt) {
+        T.zd[lt] = grid_dim_dev(d[0], geom, lt);
+        T.xd[lt] = grid_dim_dev(d[1], geom, lt);
+        T.yd[lt] = grid_dim_dev(d[2], geom, lt);
+        T.level_offset[lt] = nrow;
+        nrow += static_cast<uint64_t>(T.zd[lt]) * T.xd[lt];
+        np += lcount[lt];
+    }
+    if (np >= (1ull << 32)) fail(APRGPU_ERR_CAPABILITY, "interior node count exceeds u32");
+    T.n_rows = nrow;
+    T.n_particles = np;
+    APR_CUDA(cudaMalloc(&T.y, 2 * np + 2));
+    APR_CUDA(cudaMalloc(&T.rb, sizeof(uint32_t) * (nrow + 1)));
+    APR_CUDA(cudaMemsetAsync(T.rb, 0, sizeof(uint32_t), s));
+    uint64_t poff = 0;
+    for (int lt = tmin; lt <= tmax; ++lt) {
+        const uint64_t rows = static_cast<uint64_t>(T.zd[lt]) * T.xd[lt];
+        if (lcount[lt])
+            APR_CUDA(cudaMemcpyAsync(T.y + poff, ly[lt].p, 2 * lcount[lt], cudaMemcpyDeviceToDevice, s));
+        k_assemble_rb<<<std::min<unsigned>(blocks_for(rows, 256), ctx->sm_count * 8), 256, 0, s>>>(
+            lrb[lt].as<uint32_t>(), rows, static_cast<uint32_t>(T.level_offset[lt]), static_cast<uint32_t>(poff), T.rb);
+        APR_CUDA(cudaGetLastError());
+        count_launch(ctx);
+        poff += lcount[lt];
+    }
+    APR_CUDA(cudaStreamSynchronize(s));
+    for (auto& b : lrb) b.release();
+    for (auto& b : ly) b.release();
+    build_work_lists(ctx, T);
+}
+
+void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr) {
+    cudaStream_t s = ctx->stream;
+    const DevAccess& L = apr->leaf;
+    const DevAccess& T = apr->tree;
+    GpuBuf flag;
+    flag.ensure(sizeof(int));
+    APR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+    const AccessView lv = L.view(), tv = T.view();
+    for (int c = std::max(L.l_min, T.l_min + 1); c <= std::min(L.l_max, T.l_max + 1); ++c) {
+        const uint64_t rows = static_cast<uint64_t>(L.zd[c]) * L.xd[c];
+        k_verify_links<<<std::min<unsigned>(blocks_for(rows * 32, 256), ctx->sm_count * 8), 256, 0, s>>>(
+            lv, tv, c, rows, flag.as<int>());
+        count_launch(ctx);
+    }
+    for (int c = T.l_min + 1; c <= T.l_max; ++c) {
+        const uint64_t rows = static_cast<uint64_t>(T.zd[c]) * T.xd[c];
+        k_verify_links<<<std::min<unsigned>(blocks_for(rows * 32, 256), ctx->sm_count * 8), 256, 0, s>>>(
+            tv, tv, c, rows, flag.as<int>());
+        count_launch(ctx);
+    }
+    APR_CUDA(cudaGetLastError());
+    int bad = 0;
+    APR_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    APR_CUDA(cudaStreamSynchronize(s));
+    if (bad) fail(APRGPU_ERR_INTEGRITY, "synchronized_parent_pass: missing parent for a child node");
+}
+
+void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s) {
+    aprgpu_ctx* ctx = apr->ctx;
+    const DevAccess& L = apr->leaf;
+    const DevAccess& T = apr->tree;
+    if (T.n_particles == 0) return;
+    apr->vsum.ensure(sizeof(double) * T.n_particles);
+    apr->wsum.ensure(sizeof(double) * T.n_particles);
+    FillArgs a{};
+    a.leaf = L.view();
+    a.tree = T.view();
+    a.leaf_v = leaf;
+    a.vsum = apr->vsum.as<double>();
+    a.wsum = apr->wsum.as<double>();
+    a.glm = L.l_max;
+    a.nz = apr->dims[0];
+    a.nx = apr->dims[1];
+    a.ny = apr->dims[2];
+    for (int lt = T.l_max; lt >= T.l_min; --lt) {
+        a.lt = lt;
+        a.c = lt + 1;
+        a.leaf_ok = (a.c >= L.l_min && a.c <= L.l_max) ? 1 : 0;
+        a.tree_ok = (a.c <= T.l_max) ? 1 : 0;
+        a.czd = grid_dim_dev(a.nz, a.glm, a.c);
+        a.cxd = grid_dim_dev(a.nx, a.glm, a.c);
+        a.work = T.work + T.work_off[lt];
+        a.n_work = T.work_off[lt + 1] - T.work_off[lt];
+        if (a.n_work == 0) continue;
+        const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), ctx->sm_count * 16);
+        k_fill_tree_level<<<grid, 256, 0, s>>>(a);
+        count_launch(ctx);
+    }
+    k_tree_finalize<<<std::min<unsigned>(blocks_for(T.n_particles, 256), ctx->sm_count * 8), 256, 0, s>>>(
+        apr->vsum.as<double>(), apr->wsum.as<double>(), T.n_particles, tree);
+    count_launch(ctx);
+    APR_CUDA(cudaGetLastError());
+}
+
+}  // namespace aprgpu
