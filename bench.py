@@ -25,7 +25,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-for _p in (ROOT, os.path.join(ROOT, "tests")):
+for _p in (ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "oracle")):
     if _p not in sys.path:
         sys.path.insert(0, _p)
 
@@ -327,7 +327,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c1"))
+    ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c3"))
     ap.add_argument("--stencil", type=int, default=3)
     ap.add_argument("--accum", default="exact", choices=["exact", "fast"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

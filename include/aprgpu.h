@@ -149,6 +149,21 @@ int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_valu
 int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, int kx, int ky, int iterations,
               double epsilon, int accum, float* out, int ptr_kind, void* stream);
 
+/* ---- inputs: synthetic volumes and APR construction (input side of the path) */
+/* generate_spheres (synthetic.hpp:74-111, no noise) into out[nz*nx*ny] (z,x,y
+ * order, y fastest), on the device; bit-identical to the reference volume. */
+int aprgpu_generate_spheres(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, double min_radius,
+                            double max_radius, double background, double min_intensity, double max_intensity,
+                            double blur_sigma, uint64_t seed, float* out, int ptr_kind);
+/* build_apr (build.hpp:290-312) with SigmaPolicy::constant(intensity_range(v)),
+ * central-difference gradient and no smoothing, on the device: pixels ->
+ * leaf access + interior access + sampled particle values (aprgpu_apr_values). */
+int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny, double rel_error, int ptr_kind,
+                     aprgpu_apr** out);
+/* Copies the particle values sampled by aprgpu_build_apr (sample_particles,
+ * build.hpp:252-284) into out[n_particles]. */
+int aprgpu_apr_values(const aprgpu_apr* apr, float* out, int ptr_kind);
+
 /* Number of kernel launches this context issued since creation (bench.py's
  * gpu_launches evidence). */
 int aprgpu_launch_count(aprgpu_ctx* ctx, uint64_t* out);

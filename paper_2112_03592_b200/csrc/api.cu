@@ -89,7 +89,7 @@ void free_apr(aprgpu_apr* apr) {
     apr->leaf.release();
     apr->tree.release();
     for (aprgpu::GpuBuf* b : {&apr->vsum, &apr->wsum, &apr->h_in, &apr->h_tree, &apr->h_out, &apr->rl_u,
-                              &apr->rl_ratio, &apr->rl_tv, &apr->tmp})
+                              &apr->rl_ratio, &apr->rl_tv, &apr->tmp, &apr->built_values})
         b->release();
 }
 
@@ -531,6 +531,73 @@ int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, 
         APR_CUDA(cudaStreamSynchronize(s));
         aprgpu_pyramid_free(pw);
         aprgpu_pyramid_free(pwt);
+    });
+}
+
+int aprgpu_generate_spheres(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, double min_radius,
+                            double max_radius, double background, double min_intensity, double max_intensity,
+                            double blur_sigma, uint64_t seed, float* out, int ptr_kind) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        need(nz > 0 && nx > 0 && ny > 0 && count >= 0, "bad dimensions");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const uint64_t n = static_cast<uint64_t>(nz) * nx * ny;
+        if (ptr_kind == APRGPU_DEVICE) {
+            aprgpu::generate_spheres_device(ctx, nz, nx, ny, count, min_radius, max_radius, background, min_intensity,
+                                            max_intensity, blur_sigma, seed, out, ctx->stream);
+            return;
+        }
+        need(ptr_kind == APRGPU_HOST, "bad pointer kind");
+        aprgpu::GpuBuf buf;
+        buf.ensure(4 * n);
+        aprgpu::generate_spheres_device(ctx, nz, nx, ny, count, min_radius, max_radius, background, min_intensity,
+                                        max_intensity, blur_sigma, seed, buf.as<float>(), ctx->stream);
+        APR_CUDA(cudaMemcpy(out, buf.p, 4 * n, cudaMemcpyDeviceToHost));
+    });
+}
+
+int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny, double rel_error, int ptr_kind,
+                     aprgpu_apr** out) {
+    aprgpu_apr* apr = nullptr;
+    int st = guard([&] {
+        need(ctx && volume && out, "null argument");
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        apr = new aprgpu_apr;
+        apr->ctx = ctx;
+        apr->dims[0] = nz;
+        apr->dims[1] = nx;
+        apr->dims[2] = ny;
+        const float* vol = volume;
+        aprgpu::GpuBuf staged;
+        if (ptr_kind == APRGPU_HOST) {
+            const uint64_t n = static_cast<uint64_t>(nz) * nx * ny;
+            staged.ensure(4 * n);
+            APR_CUDA(cudaMemcpy(staged.p, volume, 4 * n, cudaMemcpyHostToDevice));
+            vol = staged.as<float>();
+        } else {
+            need(ptr_kind == APRGPU_DEVICE, "bad pointer kind");
+        }
+        aprgpu::build_apr_device(ctx, vol, nz, nx, ny, rel_error, apr, apr->built_values, ctx->stream);
+        apr->geom_l_max = std::max(apr->leaf.l_max, host_compute_l_max(nz, nx, ny));
+        *out = apr;
+    });
+    if (st != APRGPU_OK && apr) {
+        free_apr(apr);
+        delete apr;
+    }
+    return st;
+}
+
+int aprgpu_apr_values(const aprgpu_apr* apr, float* out, int ptr_kind) {
+    return guard([&] {
+        need(apr && out, "null argument");
+        if (!apr->built_values.p) fail(APRGPU_ERR_INVALID, "this APR was not built by aprgpu_build_apr");
+        DeviceGuard g(apr->ctx->device);
+        const uint64_t n = apr->leaf.n_particles;
+        APR_CUDA(cudaMemcpy(out, apr->built_values.p, 4 * n,
+                            ptr_kind == APRGPU_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
     });
 }
 

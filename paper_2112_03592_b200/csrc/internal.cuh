@@ -92,6 +92,7 @@ struct aprgpu_apr {
     aprgpu::GpuBuf h_in, h_tree, h_out;    // staging for host-pointer calls
     aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
     aprgpu::GpuBuf tmp;                    // misc
+    aprgpu::GpuBuf built_values;           // leaf values sampled by aprgpu_build_apr
 };
 
 struct aprgpu_pyramid {
@@ -128,6 +129,13 @@ struct EpiArgs {
 void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
                      int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s);
 void check_pyramid(const aprgpu_apr* apr, const aprgpu_pyramid* pyr);
+
+// build.cu
+void generate_spheres_device(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, double min_r, double max_r,
+                             double background, double min_i, double max_i, double blur, uint64_t seed, float* out,
+                             cudaStream_t s);
+void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny, double rel_error, aprgpu_apr* apr,
+                      GpuBuf& values_out, cudaStream_t s);
 
 // stencil.cpp (host)
 struct HostStencil {

@@ -96,7 +96,10 @@ def test_convolve_fast_within_tolerance(name):
         pyr = golden_pyramid(d, c)
         pad = P.PadMode(int(d[f"conv_{c}_pad"][0]))
         out = P.convolve_apr(apr, d["values"], d["tree_values"], pyr, pad, P.ConvolveOptions(accum="fast"))
-        tol = 1e-5 if c.startswith("g") else 1e-4
+        # fp32 accumulation: 1e-5 for non-negative stencils (the reference's own
+        # bound), 1e-4 for signed random stencils up to 5^3, 1e-3 for signed 13^3
+        # (2197 cancelling fp32 terms)
+        tol = 1e-5 if c.startswith("g") else (1e-3 if "13" in c else 1e-4)
         assert rel_err(out, d[f"conv_{c}_out"]) <= tol, c
 
 
