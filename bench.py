@@ -128,8 +128,12 @@ def run_ours(args, rank, world):
     setup_s = time.time() - t0
     accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
 
-    stream = torch.cuda.current_stream()
+    # an explicit stream: torch's legacy default stream has handle 0, which the
+    # C-ABI reads as "the context's own stream"
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     s = stream.cuda_stream
+    assert s != 0
     v = torch.from_numpy(np.ascontiguousarray(values, np.float32)).cuda()
     tv = torch.empty(max(dapr.n_tree, 1), dtype=torch.float32, device="cuda")
     out = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")

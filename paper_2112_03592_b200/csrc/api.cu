@@ -54,7 +54,7 @@ int host_compute_l_max(int nz, int nx, int ny) {
     return l;
 }
 
-void upload_one(aprgpu_ctx* ctx, const aprgpu_access_desc* d, aprgpu::DevAccess& a) {
+void upload_one(aprgpu_ctx* ctx, const aprgpu_access_desc* d, aprgpu::DevAccess& a, bool tiles) {
     need(d != nullptr, "null access descriptor");
     need(d->l_min >= 0 && d->l_min <= d->l_max, "l_min > l_max");
     if (d->l_max >= aprgpu::kMaxLevels) fail(APRGPU_ERR_CAPABILITY, "too many levels");
@@ -83,6 +83,7 @@ void upload_one(aprgpu_ctx* ctx, const aprgpu_access_desc* d, aprgpu::DevAccess&
     if (a.n_rows == 0 && a.n_particles) fail(APRGPU_ERR_INTEGRITY, "particles present but no rows");
     aprgpu::build_row_begin(ctx, a, d->xz_end);
     aprgpu::build_work_lists(ctx, a);
+    if (tiles) aprgpu::build_tile_lists(ctx, a);
 }
 
 void free_apr(aprgpu_apr* apr) {
@@ -187,10 +188,10 @@ int aprgpu_upload_access(aprgpu_ctx* ctx, const aprgpu_access_desc* leaf, const 
         apr->ctx = ctx;
         for (int i = 0; i < 3; ++i) apr->dims[i] = source_dims[i];
         if (source_dims[2] > 65536) fail(APRGPU_ERR_CAPABILITY, "y dimension exceeds the 16-bit index limit");
-        upload_one(ctx, leaf, apr->leaf);
+        upload_one(ctx, leaf, apr->leaf, true);
         apr->geom_l_max = std::max(apr->leaf.l_max, host_compute_l_max(source_dims[0], source_dims[1], source_dims[2]));
         if (tree) {
-            upload_one(ctx, tree, apr->tree);
+            upload_one(ctx, tree, apr->tree, false);
             aprgpu::verify_tree_links(ctx, apr);
         } else {
             aprgpu::build_tree_structure(ctx, apr);

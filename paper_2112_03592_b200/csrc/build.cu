@@ -458,6 +458,7 @@ void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny,
     for (auto& b : Gm) b.release();
     counts.release();
     build_work_lists(ctx, A);
+    build_tile_lists(ctx, A);
     build_tree_structure(ctx, apr);
 
     // sample_particles

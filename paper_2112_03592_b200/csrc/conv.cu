@@ -21,6 +21,9 @@
 // (az,ax,ay) order: fp64 FMA of exact products (bit-identical to
 // LevelSlab::apply) in EXACT mode, fp32 FMA in FAST mode.  Optional RL
 // epilogues fuse deconv.hpp:98-99 (ratio) and :102 (multiply).
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 
 namespace aprgpu {
@@ -280,6 +283,14 @@ void dispatch(aprgpu_ctx* ctx, ConvArgs& a, cudaStream_t s) {
     return launch_conv<Acc, 0, 0, 0>(ctx, a, s);
 }
 
+bool use_tiles() {
+    static const bool on = [] {
+        const char* e = std::getenv("APRGPU_CONV_KERNEL");
+        return !(e && std::string(e) == "rows");
+    }();
+    return on;
+}
+
 }  // namespace
 
 void check_pyramid(const aprgpu_apr* apr, const aprgpu_pyramid* pyr) {
@@ -318,6 +329,9 @@ void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_val
         a.wf = pyr->w_dev + pyr->off[li];
         a.wd = pyr->wd_dev + pyr->off[li];
         a.tree_at_l = (T.n_particles > 0 && l >= T.l_min && l <= T.l_max) ? 1 : 0;
+        if (use_tiles() && conv_tile_level(apr, l, values, tree_values, &pyr->k3[3 * li], pyr->w_host.data() + pyr->off[li],
+                                           pad, accum, out, epi, s))
+            continue;
         if (accum == APRGPU_ACCUM_EXACT)
             dispatch<double>(apr->ctx, a, s);
         else

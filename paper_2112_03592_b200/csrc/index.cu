@@ -36,9 +36,11 @@ void DevAccess::release() {
     cudaFree(y);
     cudaFree(rb);
     cudaFree(work);
+    cudaFree(tiles);
     y = nullptr;
     rb = nullptr;
     work = nullptr;
+    tiles = nullptr;
 }
 
 void GpuBuf::ensure(size_t n) {

@@ -60,6 +60,10 @@ struct DevAccess {
     // per-level non-empty rows (global row ids), ascending == (z,x) order
     uint32_t* work = nullptr;              // device
     std::vector<uint64_t> work_off;        // l_max+2 offsets into work
+    // per-level occupied (8z x 8x x 16y) output tiles of the box-tile kernel
+    uint32_t* tiles = nullptr;             // device, linear tile ids per level
+    std::vector<uint64_t> tile_off;        // l_max+2 offsets into tiles
+    std::vector<int> tile_dims;            // 3 per level: tile grid (z, x, y)
     AccessView view() const;
     void release();
 };
@@ -112,6 +116,11 @@ void build_row_begin(aprgpu_ctx* ctx, DevAccess& a, const uint64_t* xz_end_host)
 void build_work_lists(aprgpu_ctx* ctx, DevAccess& a);
 void row_spans(aprgpu_ctx* ctx, const DevAccess& a, int level, int32_t* z, int32_t* x, uint16_t* ymin,
                uint16_t* ymax, uint64_t cap);
+
+// conv_tile.cu
+void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a);
+bool conv_tile_level(aprgpu_apr* apr, int l, const float* values, const float* tree_values, const int* k3,
+                     const float* w_host, int pad, int accum, float* out, const struct EpiArgs& epi, cudaStream_t s);
 
 // tree.cu
 void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr);

@@ -195,7 +195,9 @@ def test_device_pointer_path_with_torch():
     v = torch.from_numpy(d["values"]).cuda()
     tv = torch.empty(dev.n_tree, dtype=torch.float32, device="cuda")
     out = torch.empty(dev.n_particles, dtype=torch.float32, device="cuda")
-    s = torch.cuda.current_stream().cuda_stream
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    s = st.cuda_stream
     dev.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
     dev.convolve_ptr(v.data_ptr(), tv.data_ptr(), pyr, 1, L.ACCUM_EXACT, out.data_ptr(), s)
     torch.cuda.synchronize()
