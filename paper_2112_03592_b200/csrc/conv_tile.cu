@@ -14,12 +14,15 @@
 //            lower_bound, the particles of the level-l leaf row and of the
 //            level-l interior row whose y falls in the box, and for the 64
 //            inner rows the output particles of the tile;
-//   phase 2  half-warps scatter those particles into the box;
+//   phase 2  one warp per halo z-plane scatters those particles into the box
+//            (the plane's rows flattened across the lanes) and flags the cells;
 //   phase 3  for d = 1, 2, ... the few level l-d leaf rows covering the box
-//            are searched once and each coarse particle is constant-upsampled
-//            into the 2^d x 2^d x 2^d cells it covers -- repeated only while
-//            some in-domain box cell is still uncovered (a valid APR covers
-//            every cell exactly once);
+//            are searched once and each coarse particle is scattered ONCE into
+//            a small coarse box of level l-d -- repeated only while the
+//            coverage count says some in-domain box cell is still uncovered (a
+//            valid APR covers every cell exactly once);
+//   resolve  one cell-parallel pass fills every unflagged box cell from the
+//            finest coarse box that holds its ancestor (constant upsampling);
 //   phase 4  out-of-domain box cells: reflect_index copies or zeros.
 // Outputs: one thread per particle, (az,ax,ay)-ordered FMA chain exactly as
 // LevelSlab::apply (convolve.hpp:154-169): fp64 with exact products in EXACT
@@ -74,15 +77,27 @@ __device__ __forceinline__ int block_sum_add(int v, int* target) {
     return v;
 }
 
+template <int H>
+struct CoarseCap {  // sum over d >= 1 of the coarse-box sizes, rounded up
+    static constexpr int value = H == 1 ? 640 : 1024;
+};
+
 template <typename Acc, int H>
 __global__ void __launch_bounds__(kTileThreads) k_conv_tile(const __grid_constant__ TileArgs a) {
     using B = Box<H>;
     constexpr int K = 2 * H + 1;
-    __shared__ Acc S[B::NC];
+    constexpr int CC = CoarseCap<H>::value;
+    constexpr int kMaxD = 20;
+    __shared__ Acc S[B::NC];                       // level-l box
+    __shared__ Acc CV[CC];                         // coarse boxes, level by level
+    __shared__ __align__(16) uint8_t F[(B::NC + 15) & ~15];  // box cell written by a level-l source
+    __shared__ __align__(16) uint8_t CF[CC];       // coarse cell holds a leaf
     __shared__ int c_s[2 * B::NR], c_n[2 * B::NR];
     __shared__ int o_s[kTZ * kTX], o_n[kTZ * kTX], o_pre[kTZ * kTX + 1];
-    __shared__ int r_s[64], r_n[64], r_pre[65];
-    __shared__ int cov, holes;
+    __shared__ uint8_t o_row[kTZ * kTX * kTY];
+    __shared__ int r_s[64], r_n[64];
+    __shared__ int coff[kMaxD + 2];
+    __shared__ int cov;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int l = a.l;
@@ -99,6 +114,13 @@ __global__ void __launch_bounds__(kTileThreads) k_conv_tile(const __grid_constan
     const int needed = (zhi - zlo) * (xhi - xlo) * (yhi - ylo);
     const int nsrc = 1 + a.tree_at_l;
 
+    // ---- phase 0: clear coverage flags
+    {
+        uint32_t* f = reinterpret_cast<uint32_t*>(F);
+        for (int i = tid; i < static_cast<int>(sizeof(F) / 4); i += kTileThreads) f[i] = 0u;
+        uint32_t* cf = reinterpret_cast<uint32_t*>(CF);
+        for (int i = tid; i < CC / 4; i += kTileThreads) cf[i] = 0u;
+    }
     // ---- phase 1: candidate ranges of the halo rows, output ranges of the tile
     for (int t = tid; t < nsrc * B::NR; t += kTileThreads) {
         const int src = t >= B::NR;
@@ -135,103 +157,139 @@ __global__ void __launch_bounds__(kTileThreads) k_conv_tile(const __grid_constan
     }
     if (tid == 0) {
         cov = 0;
-        holes = 0;
+        coff[1] = 0;
     }
     __syncthreads();
 
-    // ---- phases 2+3 (repeated from a zeroed box if the APR leaves holes)
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        if (attempt == 1) {
-            if (!holes) break;
-            for (int c = tid; c < B::NC; c += kTileThreads) S[c] = Acc(0);
-            if (tid == 0) cov = 0;
-            __syncthreads();
-        }
-        int mine = 0;
-        {   // same-level leaves and level-l interior nodes: half-warp per row
-            const int hw = tid >> 4, hl = tid & 15;
-            for (int e = hw; e < nsrc * B::NR; e += kTileThreads / 16) {
-                const int n = c_n[e];
-                if (!n) continue;
-                const int src = e >= B::NR;
-                const int q = e - src * B::NR;
-                const uint16_t* ys = src ? a.tree.y : a.leaf.y;
-                const float* vs = src ? a.tval : a.val;
-                Acc* dst = S + q * B::BY - by0;
-                const int s = c_s[e];
-                for (int j = hl; j < n; j += 16) {
-                    const int yy = __ldg(ys + s + j);
-                    if (yy < yhi) {
-                        dst[yy] = static_cast<Acc>(__ldg(vs + s + j));
-                        ++mine;
-                    }
+    // ---- output map (inner row of every output) and level-l scatter
+    if (warp == 0) {
+        const int v0 = o_n[lane * 2], v1 = o_n[lane * 2 + 1];
+        const int incl = warp_incl_scan(v0 + v1, lane);
+        const int p0 = incl - v0 - v1, p1 = incl - v1;
+        o_pre[lane * 2] = p0;
+        o_pre[lane * 2 + 1] = p1;
+        if (lane == 31) o_pre[64] = incl;
+        for (int j = 0; j < v0; ++j) o_row[p0 + j] = static_cast<uint8_t>(lane * 2);
+        for (int j = 0; j < v1; ++j) o_row[p1 + j] = static_cast<uint8_t>(lane * 2 + 1);
+    }
+    int mine = 0;
+    // one warp per (source, z-plane of halo rows); the plane's BX rows are
+    // flattened so all lanes scatter particles
+    for (int p = warp; p < nsrc * B::BZ; p += kTileThreads / 32) {
+        const int src = p >= B::BZ;
+        const int bz = p - src * B::BZ;
+        const int ebase = src * B::NR + bz * B::BX;
+        const int n_l = lane < B::BX ? c_n[ebase + lane] : 0;
+        const int s_l = lane < B::BX ? c_s[ebase + lane] : 0;
+        const int incl = warp_incl_scan(n_l, lane);
+        const int excl = incl - n_l;
+        const int total = __shfl_sync(kFull, incl, B::BX - 1);
+        const uint16_t* ys = src ? a.tree.y : a.leaf.y;
+        const float* vs = src ? a.tval : a.val;
+        for (int e0 = 0; e0 < total; e0 += 32) {
+            const int e = e0 + lane;
+            // owning row: last bx with excl[bx] <= e (binary search over lanes)
+            int lo = 0, hi = B::BX - 1;
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+                const int mid = (lo + hi + 1) >> 1;
+                const int em = __shfl_sync(kFull, excl, mid);
+                if (em <= e) lo = mid; else hi = mid - 1;
+            }
+            const int ex = __shfl_sync(kFull, excl, lo);
+            const int sx = __shfl_sync(kFull, s_l, lo);
+            if (e < total) {
+                const int idx = sx + (e - ex);
+                const int yy = __ldg(ys + idx);
+                if (yy < yhi) {
+                    const int c = (bz * B::BX + lo) * B::BY + (yy - by0);
+                    S[c] = static_cast<Acc>(__ldg(vs + idx));
+                    F[c] = 1;
+                    ++mine;
                 }
             }
+        }
+    }
+    block_sum_add(mine, &cov);
+
+    // ---- coarse levels: scatter each level-(l-d) leaf once into its coarse box
+    int dmax = 0;
+    for (int d = 1; d <= kMaxD; ++d) {
+        __syncthreads();
+        if (cov >= needed || l - d < a.leaf.l_min) break;
+        const int czlo = zlo >> d, cxlo = xlo >> d, cylo = ylo >> d;
+        const int nzc = ((zhi - 1) >> d) - czlo + 1, nxc = ((xhi - 1) >> d) - cxlo + 1;
+        const int nyc = ((yhi - 1) >> d) - cylo + 1;
+        const int base = coff[d];
+        if (base + nzc * nxc * nyc > CC) break;  // cannot happen for H <= 2 (see CoarseCap)
+        const int ncr = nzc * nxc;
+        const LevelG gc = a.leaf.g[l - d];
+        if (tid < ncr) {
+            const int cz = czlo + tid / nxc, cx = cxlo + tid % nxc;
+            int s = 0, n = 0;
+            if (cz < gc.zd && cx < gc.xd) {
+                const uint32_t row = gc.row0 + static_cast<uint32_t>(cz) * gc.xd + cx;
+                const uint32_t b = __ldg(a.leaf.rb + row), e = __ldg(a.leaf.rb + row + 1);
+                if (e > b) {
+                    const uint32_t s0 = lower_bound_u16(a.leaf.y, b, e, cylo);
+                    s = static_cast<int>(s0);
+                    n = min(static_cast<int>(e - s0), nyc);
+                }
+            }
+            r_s[tid] = s;
+            r_n[tid] = n;
+        }
+        if (tid == 0) coff[d + 1] = base + nzc * nxc * nyc;
+        dmax = d;
+        __syncthreads();
+        mine = 0;
+        // (coarse row, candidate) pairs; nyc <= 11 candidates per row
+        for (int t = tid; t < ncr * nyc; t += kTileThreads) {
+            const int r = t / nyc, j = t - r * nyc;
+            if (j >= r_n[r]) continue;
+            const int idx = r_s[r] + j;
+            const int yy = __ldg(a.leaf.y + idx);
+            if (yy - cylo >= nyc) continue;
+            const int rz = r / nxc, rx = r - rz * nxc;
+            const int ci = base + (rz * nxc + rx) * nyc + (yy - cylo);
+            CV[ci] = static_cast<Acc>(__ldg(a.val + idx));
+            CF[ci] = 1;
+            const int cz = czlo + rz, cx = cxlo + rx;
+            const int zA = max(cz << d, zlo), zB = min((cz + 1) << d, zhi);
+            const int xA = max(cx << d, xlo), xB = min((cx + 1) << d, xhi);
+            const int yA = max(yy << d, ylo), yB = min((yy + 1) << d, yhi);
+            mine += (zB - zA) * (xB - xA) * (yB - yA);
         }
         block_sum_add(mine, &cov);
-        for (int d = 1;; ++d) {
-            __syncthreads();
-            if ((attempt == 0 && cov >= needed) || l - d < a.leaf.l_min) break;
-            const LevelG gc = a.leaf.g[l - d];
-            const int czlo = zlo >> d, czhi = (zhi - 1) >> d, cxlo = xlo >> d, cxhi = (xhi - 1) >> d;
-            const int ncx = cxhi - cxlo + 1;
-            const int ncr = (czhi - czlo + 1) * ncx;  // <= 49 for H <= 2
-            const int yl = ylo >> d, yh = ((yhi - 1) >> d) + 1;
-            if (tid < ncr) {
-                const int cz = czlo + tid / ncx, cx = cxlo + tid % ncx;
-                int s = 0, n = 0;
-                if (cz < gc.zd && cx < gc.xd) {
-                    const uint32_t row = gc.row0 + static_cast<uint32_t>(cz) * gc.xd + cx;
-                    const uint32_t b = __ldg(a.leaf.rb + row), e = __ldg(a.leaf.rb + row + 1);
-                    if (e > b) {
-                        const uint32_t s0 = lower_bound_u16(a.leaf.y, b, e, yl);
-                        s = static_cast<int>(s0);
-                        n = min(static_cast<int>(e - s0), yh - yl);
-                    }
+    }
+    __syncthreads();
+
+    // ---- resolve every in-domain cell not written at level l through the
+    // coarse boxes, finest first (uncovered cells of a malformed APR -> 0)
+    if (dmax > 0 || cov < needed) {
+        for (int c = tid; c < B::NC; c += kTileThreads) {
+            if (F[c]) continue;
+            const int bz = c / (B::BX * B::BY);
+            const int rem = c - bz * (B::BX * B::BY);
+            const int bx = rem / B::BY, by = rem - bx * B::BY;
+            const int zz = bz0 + bz, xx = bx0 + bx, yy = by0 + by;
+            if (zz < zlo || zz >= zhi || xx < xlo || xx >= xhi || yy < ylo || yy >= yhi) continue;
+            Acc v = Acc(0);
+            for (int d = 1; d <= dmax; ++d) {
+                const int czlo = zlo >> d, cxlo = xlo >> d, cylo = ylo >> d;
+                const int nxc = ((xhi - 1) >> d) - cxlo + 1, nyc = ((yhi - 1) >> d) - cylo + 1;
+                const int ci = coff[d] + (((zz >> d) - czlo) * nxc + ((xx >> d) - cxlo)) * nyc + ((yy >> d) - cylo);
+                if (CF[ci]) {
+                    v = CV[ci];
+                    break;
                 }
-                r_s[tid] = s;
-                r_n[tid] = n;
             }
-            __syncthreads();
-            if (warp == 0) {  // prefix over <= 64 coarse rows
-                const int v0 = lane * 2 < ncr ? r_n[lane * 2] : 0;
-                const int v1 = lane * 2 + 1 < ncr ? r_n[lane * 2 + 1] : 0;
-                const int incl = warp_incl_scan(v0 + v1, lane);
-                r_pre[lane * 2] = incl - v0 - v1;
-                r_pre[lane * 2 + 1] = incl - v1;
-                if (lane == 31) r_pre[64] = incl;
-            }
-            __syncthreads();
-            const int E = r_pre[64];
-            mine = 0;
-            for (int e = tid; e < E; e += kTileThreads) {
-                int lo = 0, hi = ncr - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (r_pre[mid] <= e) lo = mid; else hi = mid - 1;
-                }
-                const int idx = r_s[lo] + (e - r_pre[lo]);
-                const int yy = __ldg(a.leaf.y + idx);
-                if (yy >= yh) continue;
-                const Acc v = static_cast<Acc>(__ldg(a.val + idx));
-                const int cz = czlo + lo / ncx, cx = cxlo + lo % ncx;
-                const int zA = max(cz << d, zlo), zB = min((cz + 1) << d, zhi);
-                const int xA = max(cx << d, xlo), xB = min((cx + 1) << d, xhi);
-                const int yA = max(yy << d, ylo), yB = min((yy + 1) << d, yhi);
-                for (int zz = zA; zz < zB; ++zz)
-                    for (int xx = xA; xx < xB; ++xx) {
-                        Acc* dst = S + ((zz - bz0) * B::BX + (xx - bx0)) * B::BY - by0;
-                        for (int y = yA; y < yB; ++y) dst[y] = v;
-                    }
-                mine += max(zB - zA, 0) * max(xB - xA, 0) * max(yB - yA, 0);
-            }
-            block_sum_add(mine, &cov);
+            S[c] = v;
         }
-        if (attempt == 0 && tid == 0 && cov < needed) holes = 1;
         __syncthreads();
     }
 
-    // ---- phase 4: out-of-domain box cells (reflect_index / zero padding)
+    // ---- out-of-domain box cells (reflect_index / zero padding)
     if (bz0 < 0 || bx0 < 0 || by0 < 0 || bz0 + B::BZ > g.zd || bx0 + B::BX > g.xd || by0 + B::BY > g.yd) {
         for (int c = tid; c < B::NC; c += kTileThreads) {
             const int bz = c / (B::BX * B::BY);
@@ -250,25 +308,13 @@ __global__ void __launch_bounds__(kTileThreads) k_conv_tile(const __grid_constan
         __syncthreads();
     }
 
-    // ---- outputs: prefix over the 64 inner rows, one thread per particle
-    if (warp == 0) {
-        const int v0 = o_n[lane * 2], v1 = o_n[lane * 2 + 1];
-        const int incl = warp_incl_scan(v0 + v1, lane);
-        o_pre[lane * 2] = incl - v0 - v1;
-        o_pre[lane * 2 + 1] = incl - v1;
-        if (lane == 31) o_pre[64] = incl;
-    }
-    __syncthreads();
+    // ---- outputs: one thread per particle, taps in the reference's order
     const int NO = o_pre[64];
     for (int o = tid; o < NO; o += kTileThreads) {
-        int lo = 0, hi = kTZ * kTX - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (o_pre[mid] <= o) lo = mid; else hi = mid - 1;
-        }
-        const int i = o_s[lo] + (o - o_pre[lo]);
+        const int k = o_row[o];
+        const int i = o_s[k] + (o - o_pre[k]);
         const int yy = __ldg(a.leaf.y + i);
-        const int bz = H + lo / kTX, bx = H + lo % kTX;
+        const int bz = H + (k >> 3), bx = H + (k & 7);
         // cell (z + H - az, x + H - ax, y + H - ay) for tap (az, ax, ay)
         const Acc* base = S + ((bz + H) * B::BX + (bx + H)) * B::BY + (yy - by0 + H);
         Acc acc = Acc(0);
