@@ -297,6 +297,9 @@ __global__ void __launch_bounds__(kTileThreads) k_conv_tile(const __grid_constan
             const int bx = rem / B::BY, by = rem - bx * B::BY;
             const int zz = bz0 + bz, xx = bx0 + bx, yy = by0 + by;
             if (zz >= 0 && zz < g.zd && xx >= 0 && xx < g.xd && yy >= 0 && yy < g.yd) continue;
+            // cells more than H beyond the domain are read by no output (and
+            // their reflection may fall outside the box)
+            if (zz >= g.zd + H || xx >= g.xd + H || yy >= g.yd + H) continue;
             if (a.pad == APRGPU_PAD_ZERO) {
                 S[c] = Acc(0);
             } else {

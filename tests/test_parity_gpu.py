@@ -172,10 +172,13 @@ def test_errors_map_to_reference_exceptions():
     bad = G.product_apr(d)
     t = bad.tree_access
     if t.y_idx.size:
-        lvl = t.l_max
+        # the finest interior level that holds nodes
+        lvl = next(l for l in range(t.l_max, t.l_min - 1, -1)
+                   if (int(t.xz_end[-1]) if l == t.l_max else int(t.xz_end[int(t.level_offset[l + 1]) - 1]))
+                   > (int(t.xz_end[int(t.level_offset[l]) - 1]) if int(t.level_offset[l]) else 0))
         r0 = int(t.level_offset[lvl])
         b = int(t.xz_end[r0 - 1]) if r0 else 0
-        # drop the first node of the finest interior level by shifting one row end
+        # drop the first node of that level by shifting the row ends
         ye = t.y_idx.copy()
         xz = t.xz_end.copy()
         first_row = next(r for r in range(r0, xz.size) if int(xz[r]) > b)
