@@ -317,7 +317,10 @@ void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_val
     a.pad = pad;
     a.out = out;
     a.epi = epi;
+    bool done[kMaxLevels] = {};
+    if (use_tiles()) conv_tile_levels(apr, pyr, values, tree_values, pad, accum, out, epi, s, done);
     for (int l = L.l_max; l >= L.l_min; --l) {
+        if (done[l]) continue;
         a.n_work = L.work_off[l + 1] - L.work_off[l];
         if (a.n_work == 0) continue;
         a.work = L.work + L.work_off[l];
@@ -329,9 +332,6 @@ void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_val
         a.wf = pyr->w_dev + pyr->off[li];
         a.wd = pyr->wd_dev + pyr->off[li];
         a.tree_at_l = (T.n_particles > 0 && l >= T.l_min && l <= T.l_max) ? 1 : 0;
-        if (use_tiles() && conv_tile_level(apr, l, values, tree_values, &pyr->k3[3 * li], pyr->w_host.data() + pyr->off[li],
-                                           pad, accum, out, epi, s))
-            continue;
         if (accum == APRGPU_ACCUM_EXACT)
             dispatch<double>(apr->ctx, a, s);
         else

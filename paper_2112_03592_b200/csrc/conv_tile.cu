@@ -1,33 +1,54 @@
 // Box-tile convolution for isotropic 3^3 / 5^3 levels (the hot path).
 //
-// Work item: one (level l, 8z x 8x x 16y) output tile that holds at least one
-// particle (tile lists are built once per APR at upload, from the non-empty
-// rows).  One CTA per tile reconstructs the level-l image over the tile plus
-// its H halo -- a (8+2H) x (8+2H) x (16+2H) box -- into shared memory, once,
-// and every output particle of the tile reads its k^3 neighbourhood from it.
-// Measured on C3's finest level this box holds ~4.6 reconstructed cells per
-// output particle, against ~20 for per-row windows (the v1 kernel in conv.cu):
-// the halo rows are shared by the 64 output rows of the tile.
+// Output tiles: (level l, 8z x 8x x 16y) boxes of level-l cells holding at
+// least one particle (tile lists are built once per APR at upload, from the
+// non-empty rows).  Work item: a SEGMENT = up to kSegTiles consecutive
+// occupied tiles of one (z, x) tile column.  One 128-thread CTA per segment:
 //
-// Box fill (fill_level_row semantics, reconstruct.hpp:41-69):
-//   phase 1  one thread per (halo row, source) finds, with an L1-resident
-//            lower_bound, the particles of the level-l leaf row and of the
-//            level-l interior row whose y falls in the box, and for the 64
-//            inner rows the output particles of the tile;
-//   phase 2  one warp per halo z-plane scatters those particles into the box
-//            (the plane's rows flattened across the lanes) and flags the cells;
-//   phase 3  for d = 1, 2, ... the few level l-d leaf rows covering the box
-//            are searched once and each coarse particle is scattered ONCE into
-//            a small coarse box of level l-d -- repeated only while the
-//            coverage count says some in-domain box cell is still uncovered (a
-//            valid APR covers every cell exactly once);
-//   resolve  one cell-parallel pass fills every unflagged box cell from the
-//            finest coarse box that holds its ancestor (constant upsampling);
-//   phase 4  out-of-domain box cells: reflect_index copies or zeros.
-// Outputs: one thread per particle, (az,ax,ay)-ordered FMA chain exactly as
-// LevelSlab::apply (convolve.hpp:154-169): fp64 with exact products in EXACT
-// mode (bit-identical), fp32 in FAST mode.  Weights travel in the kernel
-// parameter block (constant bank operands).
+//   stage   every source row that can reach the segment's boxes -- the level-l
+//           leaf rows and interior rows of the (8+2H)^2 halo plane, and the
+//           level l-d leaf rows covering it for d = 1..D -- is searched ONCE
+//           (two lower_bounds) for the segment's y-range, and the particles
+//           found (y and value) are copied into shared memory with coalesced
+//           warp-per-row loads.  This replaces per-tile dependent global
+//           searches/walks (the latency chain that bounds a tile) by one
+//           search per row per segment plus shared-memory walks.
+//   per tile of the segment (in y order):
+//     fill  the level-l image of the tile's (8+2H)x(8+2H)x(16+2H) box is
+//           rebuilt in shared memory (fill_level_row semantics,
+//           reconstruct.hpp:41-69): each source row is walked from its
+//           cursor by one thread; level-l leaves / interior nodes write their
+//           cell, a coarse leaf at depth d writes its 2^d-aligned group of
+//           cells (constant upsampling) as vector stores (the box's y origin
+//           is y0 - 4, so pairs and quads are aligned); leaves >= 3 levels
+//           coarser are filled by the whole CTA.  In a valid APR every
+//           in-domain cell is covered by exactly one source, so all rows
+//           scatter in one unordered pass.
+//     pad   out-of-domain cells within H of the domain: reflect_index / 0.
+//     apply the tile is cut into 2x2x2 cell blocks (an APR refines cells into
+//           sibling octets, so finest-level particles come in complete
+//           blocks); blocks holding particles are compacted and each is
+//           evaluated by one thread from a (2+2H)^3 neighbourhood streamed
+//           plane by plane through registers (8 outputs, 3 vector loads per
+//           neighbourhood row).  Every output's taps accumulate in the
+//           reference's exact (az, ax, ay) order (LevelSlab::apply,
+//           convolve.hpp:154-169): fp64 FMA of exact products in EXACT mode
+//           (bit-identical), fp32 FMA in FAST mode.
+//
+// A probe kernel (k_tile_probe) runs once per APR and stores one byte per
+// tile: D (deepest coarse depth whose leaves reach into the 5^3 box, so no
+// coverage counting is needed), OVERLAP (malformed APR: some cell covered
+// twice -> the segment is filled in the reference's order, level l, l-1, ...,
+// then interior nodes, last writer wins) and HOLES (some cell uncovered -> the
+// box is zeroed first); plus a per-tile source-particle count used to cut the
+// tile columns into segments that fit the staging buffer.  A segment whose
+// rows still do not fit is filled straight from global memory.
+//
+// All levels that use the same isotropic extent run in ONE launch (coarse
+// levels first), so the few, short coarse segments overlap the finest level.
+#include <algorithm>
+#include <cstdlib>
+
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -36,308 +57,682 @@
 namespace aprgpu {
 
 constexpr int kTZ = 8, kTX = 8, kTY = 16, kTileThreads = 128;
+constexpr int kProbeH = 2;
+constexpr int kSegTiles = 16;      // tiles per segment (4-bit count)
+constexpr int kStageCap = 4096;    // source particles per segment (segment cut estimate)
+constexpr int kBatch = 8;          // particles per walk batch (independent loads in flight)
+constexpr int kMaxSrcRows = 512;   // >= 2*(8+2*2)^2 + coarse rows of a 5^3 box
+constexpr int kPadY = 4;           // box y origin = y0 - kPadY (>= H, multiple of 4)
+enum : uint8_t { kMetaDepth = 0x1f, kMetaOverlap = 0x20, kMetaHoles = 0x40 };
 
 namespace {
 
-struct TileArgs {
+struct TileLaunch {
     AccessView leaf, tree;
     const float* val;
     const float* tval;
-    const uint32_t* tiles;
-    uint32_t n_tiles;
-    int tzd, txd, tyd;
-    int l, pad, tree_at_l;
+    const uint32_t* tiles;   // tile ids of all levels (absolute indexing)
+    const uint8_t* meta;     // one byte per tile
+    uint16_t* count;         // probe only: source particles per tile
+    const uint32_t* segs;    // work items: (first tile << 4) | (tiles - 1)
+    uint32_t tile_base;      // probe only: first tile of the launch
+    int n_levels;                   // level segments in this launch
+    int lvl[kMaxLevels];            // level of each segment
+    uint32_t seg_end[kMaxLevels];   // exclusive end (in blocks) of each level segment
+    int tdim[kMaxLevels][3];        // tile grid dims of each segment's level
+    uint64_t woff[kMaxLevels];      // weight offset of each segment's level
+    const float* wf;
+    const double* wd;
+    int tree_lmin, tree_lmax;       // interior levels present (tree_lmax < tree_lmin: none)
+    int pad;
     float* out;
     EpiArgs epi;
-    double wd[125];
-    float wf[125];
 };
 
+struct Geo {
+    int l;
+    int z0, x0, y0;                    // tile origin (level-l cells)
+    int bz0, bx0, by0;                 // box origin
+    int zlo, zhi, xlo, xhi, ylo, yhi;  // in-domain part of the box
+};
+
+// Box layout: (8+2H) x (8+2H) rows of kTY + 2*kPadY cells, y origin y0 - 4,
+// so a coarse leaf's 2^d cells start at an index aligned to min(2^d, 4).
 template <int H>
 struct Box {
-    static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * H;
+    static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * kPadY;
     static constexpr int NR = BZ * BX, NC = BZ * BX * BY;
 };
 
-template <typename Acc>
-__device__ __forceinline__ Acc wsel(const TileArgs& a, int i);
-template <>
-__device__ __forceinline__ double wsel<double>(const TileArgs& a, int i) { return a.wd[i]; }
-template <>
-__device__ __forceinline__ float wsel<float>(const TileArgs& a, int i) { return a.wf[i]; }
+template <int H>
+__device__ __forceinline__ Geo make_geo(int l, uint32_t id, int txd, int tyd, const LevelG& g) {
+    Geo G;
+    G.l = l;
+    const int ty = static_cast<int>(id % tyd);
+    const uint32_t t2 = id / tyd;
+    const int tx = static_cast<int>(t2 % txd), tz = static_cast<int>(t2 / txd);
+    G.z0 = tz * kTZ;
+    G.x0 = tx * kTX;
+    G.y0 = ty * kTY;
+    G.bz0 = G.z0 - H;
+    G.bx0 = G.x0 - H;
+    G.by0 = G.y0 - kPadY;
+    G.zlo = max(G.bz0, 0);
+    G.zhi = min(G.z0 + kTZ + H, g.zd);
+    G.xlo = max(G.bx0, 0);
+    G.xhi = min(G.x0 + kTX + H, g.xd);
+    G.ylo = max(G.y0 - H, 0);
+    G.yhi = min(G.y0 + kTY + H, g.yd);
+    return G;
+}
 
-__device__ __forceinline__ double fma_t(double w, double u, double acc) { return __fma_rn(w, u, acc); }
-__device__ __forceinline__ float fma_t(float w, float u, float acc) { return __fmaf_rn(w, u, acc); }
+__device__ __forceinline__ int seg_of(const uint32_t* seg_end, int n, uint32_t b) {
+    int s = 0;
+    while (s + 1 < n && b >= seg_end[s]) ++s;
+    return s;
+}
+
+// Number of level l-d rows covering the in-domain box (d >= 1).
+__device__ __forceinline__ int coarse_rows(const Geo& G, int d, int& czlo, int& cxlo, int& nxc) {
+    czlo = G.zlo >> d;
+    cxlo = G.xlo >> d;
+    const int nzc = ((G.zhi - 1) >> d) - czlo + 1;
+    nxc = ((G.xhi - 1) >> d) - cxlo + 1;
+    return nzc * nxc;
+}
+
+// Source rows of a box, in the reference's fill order: [0, NR) level-l leaf
+// rows, then for d = 1..D the level l-d leaf rows covering it, then [.., +NR)
+// the level-l interior rows (when the level has interior nodes).  Depends on
+// the box's z/x extent only, so one table serves every tile of a segment.
+struct SrcTable {
+    int D, tree, n;
+    int base[kMetaDepth + 3];
+};
+
+template <int H>
+__device__ __forceinline__ void make_src_table(const Geo& G, int D, int tree, SrcTable& T) {
+    T.D = D;
+    T.tree = tree;
+    int n = Box<H>::NR;
+    T.base[0] = 0;
+    for (int d = 1; d <= D; ++d) {
+        T.base[d] = n;
+        int czlo, cxlo, nxc;
+        n += coarse_rows(G, d, czlo, cxlo, nxc);
+    }
+    T.base[D + 1] = n;
+    if (tree) n += Box<H>::NR;
+    T.n = n;
+}
+
+// One source row, resolved: particles [b, e) of the row; d = coarse depth
+// (0: level-l leaf or interior row); (zA, zB) x (xA, xB) = the clipped level-l
+// rows its cells cover; r00 = box offset of cell (zA, xA, y = 0); obase =
+// output-map offset of y = 0 when the row is an inner level-l leaf row.
+struct RowJob {
+    uint32_t b, e;
+    int d, is_tree, inner;
+    int zA, zB, xA, xB;
+    int r00, obase;
+};
+
+template <int H, bool LOAD = true>
+__device__ __forceinline__ bool resolve_row(const TileLaunch& a, const Geo& G, const SrcTable& T, int t, RowJob& J) {
+    using B = Box<H>;
+    int d = 0;
+    int r = t;
+    J.is_tree = 0;
+    if (t >= T.base[T.D + 1]) {
+        J.is_tree = 1;
+        r = t - T.base[T.D + 1];
+    } else {
+        while (d < T.D && t >= T.base[d + 1]) ++d;
+        r = t - T.base[d];
+    }
+    J.d = d;
+    uint32_t row;
+    const AccessView& av = J.is_tree ? a.tree : a.leaf;
+    if (d == 0) {
+        const int bz = r / B::BX, bx = r - (r / B::BX) * B::BX;
+        const int zz = G.bz0 + bz, xx = G.bx0 + bx;
+        if (zz < G.zlo || zz >= G.zhi || xx < G.xlo || xx >= G.xhi) return false;
+        const LevelG g = av.g[G.l];
+        row = g.row0 + static_cast<uint32_t>(zz) * g.xd + xx;
+        J.zA = zz;
+        J.zB = zz + 1;
+        J.xA = xx;
+        J.xB = xx + 1;
+        J.inner = !J.is_tree && bz >= H && bz < H + kTZ && bx >= H && bx < H + kTX;
+        J.obase = ((bz - H) * kTX + (bx - H)) * kTY - G.y0;
+    } else {
+        int czlo, cxlo, nxc;
+        coarse_rows(G, d, czlo, cxlo, nxc);
+        const int cz = czlo + r / nxc, cx = cxlo + r % nxc;
+        const LevelG gc = a.leaf.g[G.l - d];
+        if (cz >= gc.zd || cx >= gc.xd) return false;
+        row = gc.row0 + static_cast<uint32_t>(cz) * gc.xd + cx;
+        J.zA = max(cz << d, G.zlo);
+        J.zB = min((cz + 1) << d, G.zhi);
+        J.xA = max(cx << d, G.xlo);
+        J.xB = min((cx + 1) << d, G.xhi);
+        J.inner = 0;
+        J.obase = 0;
+    }
+    J.r00 = ((J.zA - G.bz0) * B::BX + (J.xA - G.bx0)) * B::BY - G.by0;
+    if (!LOAD) return true;
+    J.b = __ldg(av.rb + row);
+    J.e = __ldg(av.rb + row + 1);
+    return J.e > J.b;
+}
+
+// ---------------------------------------------------------------- probe ----
+// Per tile: deepest coarse depth reaching into the (5^3) box, whether the
+// sources overlap or leave holes there, and how many source particles reach
+// it.  Scans every depth down to l_min, so D is exact even for malformed APRs.
+__global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_constant__ TileLaunch a) {
+    using B = Box<kProbeH>;
+    __shared__ uint8_t cnt[B::NC];
+    __shared__ int hit[kMetaDepth + 2];
+    __shared__ int flags, total;
+    __shared__ SrcTable T;
+    const int tid = threadIdx.x;
+    const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
+    const int l = a.lvl[s];
+    const LevelG g = a.leaf.g[l];
+    const uint32_t tile = a.tile_base + blockIdx.x;
+    const Geo G = make_geo<kProbeH>(l, a.tiles[tile], a.tdim[s][1], a.tdim[s][2], g);
+    for (int i = tid; i < B::NC; i += kTileThreads) cnt[i] = 0;
+    if (tid < kMetaDepth + 2) hit[tid] = 0;
+    const int tree = (l >= a.tree_lmin && l <= a.tree_lmax) ? 1 : 0;
+    const int Dall = min(l - a.leaf.l_min, static_cast<int>(kMetaDepth));
+    if (tid == 0) {
+        flags = 0;
+        total = 0;
+        make_src_table<kProbeH>(G, Dall, tree, T);
+    }
+    __syncthreads();
+    int mine = 0;
+    for (int t = tid; t < T.n; t += kTileThreads) {
+        RowJob J;
+        if (!resolve_row<kProbeH>(a, G, T, t, J)) continue;
+        const uint16_t* ys = J.is_tree ? a.tree.y : a.leaf.y;
+        const int d = J.d;
+        bool any = false;
+        for (uint32_t i = lower_bound_u16(ys, J.b, J.e, G.ylo >> d); i < J.e; ++i) {
+            const int yy = __ldg(ys + i);
+            if ((yy << d) >= G.yhi) break;
+            ++mine;
+            const int yA = max(yy << d, G.ylo), yB = min((yy + 1) << d, G.yhi);
+            for (int z = J.zA; z < J.zB; ++z)
+                for (int x = J.xA; x < J.xB; ++x)
+                    for (int y = yA; y < yB; ++y) {
+                        const int c = ((z - G.bz0) * B::BX + (x - G.bx0)) * B::BY + (y - G.by0);
+                        // byte counters packed in words (a cell sees at most one source per depth + 1)
+                        atomicAdd(reinterpret_cast<uint32_t*>(cnt + (c & ~3)), 1u << (8 * (c & 3)));
+                        any = true;
+                    }
+        }
+        if (any) hit[d] = 1;
+    }
+    if (mine) atomicAdd(&total, mine);
+    __syncthreads();
+    int f = 0;
+    for (int c = tid; c < B::NC; c += kTileThreads) {
+        const int bz = c / (B::BX * B::BY);
+        const int rem = c - bz * (B::BX * B::BY);
+        const int bx = rem / B::BY, by = rem - bx * B::BY;
+        const int zz = G.bz0 + bz, xx = G.bx0 + bx, yy = G.by0 + by;
+        if (zz < G.zlo || zz >= G.zhi || xx < G.xlo || xx >= G.xhi || yy < G.ylo || yy >= G.yhi) continue;
+        const int v = cnt[c];
+        if (v == 0) f |= kMetaHoles;
+        if (v > 1) f |= kMetaOverlap;
+    }
+    if (f) atomicOr(&flags, f);
+    __syncthreads();
+    if (tid == 0) {
+        int D = 0;
+        for (int d = 1; d <= Dall; ++d)
+            if (hit[d]) D = d;
+        const_cast<uint8_t*>(a.meta)[tile] = static_cast<uint8_t>(D | flags);
+        a.count[tile] = static_cast<uint16_t>(min(total, 65535));
+    }
+}
+
+// ------------------------------------------------------------ convolution --
+template <typename Acc>
+__device__ __forceinline__ Acc fma_t(Acc w, Acc u, Acc acc);
+template <>
+__device__ __forceinline__ double fma_t<double>(double w, double u, double acc) { return __fma_rn(w, u, acc); }
+template <>
+__device__ __forceinline__ float fma_t<float>(float w, float u, float acc) { return __fmaf_rn(w, u, acc); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // fma.rn.f32x2 (sm_100)
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<unsigned long long*>(&c)));
+    return *reinterpret_cast<float2*>(&r);
+}
 __device__ __forceinline__ float to_f(double v) { return __double2float_rn(v); }
 __device__ __forceinline__ float to_f(float v) { return v; }
 
-__device__ __forceinline__ int block_sum_add(int v, int* target) {
-    v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(target, v);
-    return v;
-}
+constexpr int kMaxRegions = 64;
 
-template <int H>
-struct CoarseCap {  // sum over d >= 1 of the coarse-box sizes, rounded up
-    static constexpr int value = H == 1 ? 640 : 1024;
+// A leaf >= 3 levels coarser than the tile's level: the box offset of its
+// first clipped row (z, x at y = by0), nz x nx clipped rows, and nq quads of 4
+// box cells from quad q0, filled cooperatively.
+template <typename Acc>
+struct Region {
+    int rbase, nz, nx, q0, nq;
+    Acc v;
+};
+
+template <typename Acc> struct Vec;
+template <> struct Vec<float> {
+    using T2 = float2;
+    __device__ static void st2(float* p, float v) { *reinterpret_cast<float2*>(p) = make_float2(v, v); }
+    __device__ static void st4(float* p, float v) { *reinterpret_cast<float4*>(p) = make_float4(v, v, v, v); }
+};
+template <> struct Vec<double> {
+    using T2 = double2;
+    __device__ static void st2(double* p, double v) { *reinterpret_cast<double2*>(p) = make_double2(v, v); }
+    __device__ static void st4(double* p, double v) {
+        reinterpret_cast<double2*>(p)[0] = make_double2(v, v);
+        reinterpret_cast<double2*>(p)[1] = make_double2(v, v);
+    }
 };
 
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads) k_conv_tile(const __grid_constant__ TileArgs a) {
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 6 : 7))
+    k_conv_seg(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
-    constexpr int K = 2 * H + 1;
-    constexpr int CC = CoarseCap<H>::value;
-    constexpr int kMaxD = 20;
-    __shared__ Acc S[B::NC];                       // level-l box
-    __shared__ Acc CV[CC];                         // coarse boxes, level by level
-    __shared__ __align__(16) uint8_t F[(B::NC + 15) & ~15];  // box cell written by a level-l source
-    __shared__ __align__(16) uint8_t CF[CC];       // coarse cell holds a leaf
-    __shared__ int c_s[2 * B::NR], c_n[2 * B::NR];
-    __shared__ int o_s[kTZ * kTX], o_n[kTZ * kTX], o_pre[kTZ * kTX + 1];
-    __shared__ uint8_t o_row[kTZ * kTX * kTY];
-    __shared__ int r_s[64], r_n[64];
-    __shared__ int coff[kMaxD + 2];
-    __shared__ int cov;
+    using VT = Vec<Acc>;
+    using V2 = typename VT::T2;
+    constexpr int K = 2 * H + 1, N = 2 + 2 * H, KW = K * K * K;
+    __shared__ __align__(16) Acc S[B::NC];
+    __shared__ __align__(16) int omap[kTZ * kTX * kTY];
+    __shared__ Acc W[KW];
+    __shared__ uint8_t blist[kTileThreads];
+    __shared__ int nblk, nreg, seg_flags;
+    __shared__ Region<Acc> reg[kMaxRegions];
+    __shared__ int rpre[kMaxRegions + 1];
+    __shared__ SrcTable T;
+    __shared__ int rcur[kMaxSrcRows];       // per source row: next particle to visit
+    __shared__ int rend[kMaxSrcRows];       // per source row: end of the row
+    __shared__ uint32_t rinfo[kMaxSrcRows]; // per source row: packed geometry
+    __shared__ int16_t rob[kMaxSrcRows];    // per source row: output-map offset
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int l = a.l;
+    const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
+    const int l = a.lvl[s];
     const LevelG g = a.leaf.g[l];
-    const uint32_t id = a.tiles[blockIdx.x];
-    const int ty = static_cast<int>(id % a.tyd);
-    const uint32_t t2 = id / a.tyd;
-    const int tx = static_cast<int>(t2 % a.txd), tz = static_cast<int>(t2 / a.txd);
-    const int z0 = tz * kTZ, x0 = tx * kTX, y0 = ty * kTY;
-    const int bz0 = z0 - H, bx0 = x0 - H, by0 = y0 - H;  // box origin (level-l cells)
-    const int zlo = max(bz0, 0), zhi = min(z0 + kTZ + H, g.zd);
-    const int xlo = max(bx0, 0), xhi = min(x0 + kTX + H, g.xd);
-    const int ylo = max(by0, 0), yhi = min(y0 + kTY + H, g.yd);
-    const int needed = (zhi - zlo) * (xhi - xlo) * (yhi - ylo);
-    const int nsrc = 1 + a.tree_at_l;
+    const uint32_t seg = a.segs[blockIdx.x];
+    const uint32_t t0 = seg >> 4;
+    const int nt = static_cast<int>(seg & 15) + 1;
+    const int txd = a.tdim[s][1], tyd = a.tdim[s][2];
+    const int tree = (l >= a.tree_lmin && l <= a.tree_lmax) ? 1 : 0;
 
-    // ---- phase 0: clear coverage flags
-    {
-        uint32_t* f = reinterpret_cast<uint32_t*>(F);
-        for (int i = tid; i < static_cast<int>(sizeof(F) / 4); i += kTileThreads) f[i] = 0u;
-        uint32_t* cf = reinterpret_cast<uint32_t*>(CF);
-        for (int i = tid; i < CC / 4; i += kTileThreads) cf[i] = 0u;
-    }
-    // ---- phase 1: candidate ranges of the halo rows, output ranges of the tile
-    for (int t = tid; t < nsrc * B::NR; t += kTileThreads) {
-        const int src = t >= B::NR;
-        const int q = t - src * B::NR;
-        const int bz = q / B::BX, bx = q - bz * B::BX;
-        const int zz = bz0 + bz, xx = bx0 + bx;
-        const bool inner = !src && bz >= H && bz < H + kTZ && bx >= H && bx < H + kTX;
-        int s = 0, n = 0, os = 0, on = 0;
-        if (zz >= 0 && zz < g.zd && xx >= 0 && xx < g.xd) {
-            const uint16_t* ys = src ? a.tree.y : a.leaf.y;
-            const uint32_t* rb = src ? a.tree.rb : a.leaf.rb;
-            const LevelG gg = src ? a.tree.g[l] : g;
-            const uint32_t row = gg.row0 + static_cast<uint32_t>(zz) * gg.xd + xx;
-            const uint32_t b = __ldg(rb + row), e = __ldg(rb + row + 1);
-            if (e > b) {
-                const uint32_t s0 = lower_bound_u16(ys, b, e, ylo);
-                s = static_cast<int>(s0);
-                n = min(static_cast<int>(e - s0), yhi - ylo);
-                if (inner) {
-                    const uint32_t o0 = lower_bound_u16(ys, s0, s0 + n, y0);
-                    const uint32_t o1 = lower_bound_u16(ys, o0, s0 + n, y0 + kTY);
-                    os = static_cast<int>(o0);
-                    on = static_cast<int>(o1 - o0);
-                }
-            }
-        }
-        c_s[t] = s;
-        c_n[t] = n;
-        if (inner) {
-            const int k = (bz - H) * kTX + (bx - H);
-            o_s[k] = os;
-            o_n[k] = on;
-        }
-    }
+    // segment geometry: the first tile's box extended to the last tile's y
+    Geo SG = make_geo<H>(l, a.tiles[t0], txd, tyd, g);
+    SG.yhi = make_geo<H>(l, a.tiles[t0 + nt - 1], txd, tyd, g).yhi;
+    for (int i = tid; i < KW; i += kTileThreads)
+        W[i] = sizeof(Acc) == 8 ? static_cast<Acc>(a.wd[a.woff[s] + i]) : static_cast<Acc>(a.wf[a.woff[s] + i]);
     if (tid == 0) {
-        cov = 0;
-        coff[1] = 0;
+        int D = 0, f = 0;
+        for (int k = 0; k < nt; ++k) {
+            const int m = a.meta[t0 + k];
+            D = max(D, m & kMetaDepth);
+            f |= m & (kMetaOverlap | kMetaHoles);
+        }
+        seg_flags = f;
+        make_src_table<H>(SG, D, tree, T);
+        nreg = 0;
     }
     __syncthreads();
 
-    // ---- output map (inner row of every output) and level-l scatter
-    if (warp == 0) {
-        const int v0 = o_n[lane * 2], v1 = o_n[lane * 2 + 1];
-        const int incl = warp_incl_scan(v0 + v1, lane);
-        const int p0 = incl - v0 - v1, p1 = incl - v1;
-        o_pre[lane * 2] = p0;
-        o_pre[lane * 2 + 1] = p1;
-        if (lane == 31) o_pre[64] = incl;
-        for (int j = 0; j < v0; ++j) o_row[p0 + j] = static_cast<uint8_t>(lane * 2);
-        for (int j = 0; j < v1; ++j) o_row[p1 + j] = static_cast<uint8_t>(lane * 2 + 1);
+    // ---- segment start: one search per source row (the cursors then only move
+    // forward) and the row's box geometry, packed:
+    //   rinfo = d | is_tree << 5 | inner << 6 | (nz-1) << 7 | (nx-1) << 11 | rbase << 15
+    // with rbase = box offset of (zA, xA, y = by0), rob = output-map offset of (row, y = y0)
+    for (int t = tid; t < T.n; t += kTileThreads) {
+        RowJob J;
+        int i = 0, e = 0;
+        uint32_t info = 0;
+        int ob = 0;
+        if (resolve_row<H>(a, SG, T, t, J)) {
+            const uint16_t* ys = J.is_tree ? a.tree.y : a.leaf.y;
+            i = static_cast<int>(lower_bound_u16(ys, J.b, J.e, SG.ylo >> J.d));
+            e = static_cast<int>(J.e);
+            const uint32_t rbase = static_cast<uint32_t>(J.r00 + SG.by0);
+            info = static_cast<uint32_t>(J.d) | (J.is_tree << 5) | (J.inner << 6) |
+                   (static_cast<uint32_t>(J.zB - J.zA - 1) << 7) | (static_cast<uint32_t>(J.xB - J.xA - 1) << 11) |
+                   (rbase << 15);
+            ob = J.obase + SG.y0;
+        }
+        rcur[t] = i;
+        rend[t] = e;
+        rinfo[t] = info;
+        rob[t] = ob;
     }
-    int mine = 0;
-    // one warp per (source, z-plane of halo rows); the plane's BX rows are
-    // flattened so all lanes scatter particles
-    for (int p = warp; p < nsrc * B::BZ; p += kTileThreads / 32) {
-        const int src = p >= B::BZ;
-        const int bz = p - src * B::BZ;
-        const int ebase = src * B::NR + bz * B::BX;
-        const int n_l = lane < B::BX ? c_n[ebase + lane] : 0;
-        const int s_l = lane < B::BX ? c_s[ebase + lane] : 0;
-        const int incl = warp_incl_scan(n_l, lane);
-        const int excl = incl - n_l;
-        const int total = __shfl_sync(kFull, incl, B::BX - 1);
-        const uint16_t* ys = src ? a.tree.y : a.leaf.y;
-        const float* vs = src ? a.tval : a.val;
-        for (int e0 = 0; e0 < total; e0 += 32) {
-            const int e = e0 + lane;
-            // owning row: last bx with excl[bx] <= e (binary search over lanes)
-            int lo = 0, hi = B::BX - 1;
+    __syncthreads();
+
+    const uint32_t col = a.tiles[t0] / static_cast<uint32_t>(tyd);
+    for (int k = 0; k < nt; ++k) {
+        const uint32_t tix = t0 + k;
+        Geo G = SG;  // same column: only the y extent changes
+        G.y0 = static_cast<int>(a.tiles[tix] - col * static_cast<uint32_t>(tyd)) * kTY;
+        G.by0 = G.y0 - kPadY;
+        G.ylo = max(G.y0 - H, 0);
+        G.yhi = min(G.y0 + kTY + H, g.yd);
+        const int meta = a.meta[tix];
+        // ---- init: output map, (holes only) zeroed box
+        {
+            int4* om = reinterpret_cast<int4*>(omap);
+            for (int i = tid; i < kTZ * kTX * kTY / 4; i += kTileThreads) om[i] = make_int4(-1, -1, -1, -1);
+        }
+        if (tid == 0) nblk = 0;
+        if (meta & kMetaHoles)
+            for (int i = tid; i < B::NC; i += kTileThreads) S[i] = Acc(0);
+        __syncthreads();
+
+        // ---- fill: each source row is walked from its cursor by one thread, 8
+        // particles per batch (independent loads in flight).  Level-l particles
+        // and leaves one or two levels coarser are written in place; leaves >= 3
+        // levels coarser are queued as regions and filled by the whole CTA.
+        const int ynext = G.y0 + kTY - H;  // a consecutive next tile's first y
+        auto scatter = [&](int t) {
+            int i = rcur[t];
+            const int e = rend[t];
+            if (i >= e) return;
+            const uint32_t info = rinfo[t];
+            const int d = info & 31;
+            const bool is_tree = (info >> 5) & 1, inner = (info >> 6) & 1;
+            const int nzr = ((info >> 7) & 15) + 1, nxr = ((info >> 11) & 15) + 1;
+            const int rbase = static_cast<int>(info >> 15);
+            const int r00 = rbase - G.by0;
+            const uint16_t* ys = is_tree ? a.tree.y : a.leaf.y;
+            const float* vs = is_tree ? a.tval : a.val;
+            while (i < e && ((static_cast<int>(__ldg(ys + i)) + 1) << d) <= G.ylo) ++i;  // gap between tiles
+            int keep = 0;  // processed particles the next tile needs again (a suffix)
+            if (d == 0) {
+                const int obase = rob[t] - G.y0;
+                for (;;) {
+                    int yb[kBatch];
+                    float vb[kBatch];
 #pragma unroll
-            for (int it = 0; it < 4; ++it) {
-                const int mid = (lo + hi + 1) >> 1;
-                const int em = __shfl_sync(kFull, excl, mid);
-                if (em <= e) lo = mid; else hi = mid - 1;
-            }
-            const int ex = __shfl_sync(kFull, excl, lo);
-            const int sx = __shfl_sync(kFull, s_l, lo);
-            if (e < total) {
-                const int idx = sx + (e - ex);
-                const int yy = __ldg(ys + idx);
-                if (yy < yhi) {
-                    const int c = (bz * B::BX + lo) * B::BY + (yy - by0);
-                    S[c] = static_cast<Acc>(__ldg(vs + idx));
-                    F[c] = 1;
-                    ++mine;
+                    for (int q = 0; q < kBatch; ++q) {
+                        const bool ok = i + q < e;
+                        yb[q] = ok ? static_cast<int>(__ldg(ys + i + q)) : 0x7fffffff;
+                        vb[q] = ok ? __ldg(vs + i + q) : 0.0f;
+                    }
+                    int used = 0;
+#pragma unroll
+                    for (int q = 0; q < kBatch; ++q) {
+                        const int yy = yb[q];
+                        if (yy < G.yhi) {
+                            ++used;
+                            keep += yy >= ynext;
+                            S[r00 + yy] = static_cast<Acc>(vb[q]);
+                            if (inner && static_cast<unsigned>(yy - G.y0) < static_cast<unsigned>(kTY))
+                                omap[obase + yy] = i + q;
+                        }
+                    }
+                    i += used;
+                    if (used < kBatch) break;
                 }
-            }
-        }
-    }
-    block_sum_add(mine, &cov);
-
-    // ---- coarse levels: scatter each level-(l-d) leaf once into its coarse box
-    int dmax = 0;
-    for (int d = 1; d <= kMaxD; ++d) {
-        __syncthreads();
-        if (cov >= needed || l - d < a.leaf.l_min) break;
-        const int czlo = zlo >> d, cxlo = xlo >> d, cylo = ylo >> d;
-        const int nzc = ((zhi - 1) >> d) - czlo + 1, nxc = ((xhi - 1) >> d) - cxlo + 1;
-        const int nyc = ((yhi - 1) >> d) - cylo + 1;
-        const int base = coff[d];
-        if (base + nzc * nxc * nyc > CC) break;  // cannot happen for H <= 2 (see CoarseCap)
-        const int ncr = nzc * nxc;
-        const LevelG gc = a.leaf.g[l - d];
-        if (tid < ncr) {
-            const int cz = czlo + tid / nxc, cx = cxlo + tid % nxc;
-            int s = 0, n = 0;
-            if (cz < gc.zd && cx < gc.xd) {
-                const uint32_t row = gc.row0 + static_cast<uint32_t>(cz) * gc.xd + cx;
-                const uint32_t b = __ldg(a.leaf.rb + row), e = __ldg(a.leaf.rb + row + 1);
-                if (e > b) {
-                    const uint32_t s0 = lower_bound_u16(a.leaf.y, b, e, cylo);
-                    s = static_cast<int>(s0);
-                    n = min(static_cast<int>(e - s0), nyc);
-                }
-            }
-            r_s[tid] = s;
-            r_n[tid] = n;
-        }
-        if (tid == 0) coff[d + 1] = base + nzc * nxc * nyc;
-        dmax = d;
-        __syncthreads();
-        mine = 0;
-        // (coarse row, candidate) pairs; nyc <= 11 candidates per row
-        for (int t = tid; t < ncr * nyc; t += kTileThreads) {
-            const int r = t / nyc, j = t - r * nyc;
-            if (j >= r_n[r]) continue;
-            const int idx = r_s[r] + j;
-            const int yy = __ldg(a.leaf.y + idx);
-            if (yy - cylo >= nyc) continue;
-            const int rz = r / nxc, rx = r - rz * nxc;
-            const int ci = base + (rz * nxc + rx) * nyc + (yy - cylo);
-            CV[ci] = static_cast<Acc>(__ldg(a.val + idx));
-            CF[ci] = 1;
-            const int cz = czlo + rz, cx = cxlo + rx;
-            const int zA = max(cz << d, zlo), zB = min((cz + 1) << d, zhi);
-            const int xA = max(cx << d, xlo), xB = min((cx + 1) << d, xhi);
-            const int yA = max(yy << d, ylo), yB = min((yy + 1) << d, yhi);
-            mine += (zB - zA) * (xB - xA) * (yB - yA);
-        }
-        block_sum_add(mine, &cov);
-    }
-    __syncthreads();
-
-    // ---- resolve every in-domain cell not written at level l through the
-    // coarse boxes, finest first (uncovered cells of a malformed APR -> 0)
-    if (dmax > 0 || cov < needed) {
-        for (int c = tid; c < B::NC; c += kTileThreads) {
-            if (F[c]) continue;
-            const int bz = c / (B::BX * B::BY);
-            const int rem = c - bz * (B::BX * B::BY);
-            const int bx = rem / B::BY, by = rem - bx * B::BY;
-            const int zz = bz0 + bz, xx = bx0 + bx, yy = by0 + by;
-            if (zz < zlo || zz >= zhi || xx < xlo || xx >= xhi || yy < ylo || yy >= yhi) continue;
-            Acc v = Acc(0);
-            for (int d = 1; d <= dmax; ++d) {
-                const int czlo = zlo >> d, cxlo = xlo >> d, cylo = ylo >> d;
-                const int nxc = ((xhi - 1) >> d) - cxlo + 1, nyc = ((yhi - 1) >> d) - cylo + 1;
-                const int ci = coff[d] + (((zz >> d) - czlo) * nxc + ((xx >> d) - cxlo)) * nyc + ((yy >> d) - cylo);
-                if (CF[ci]) {
-                    v = CV[ci];
-                    break;
-                }
-            }
-            S[c] = v;
-        }
-        __syncthreads();
-    }
-
-    // ---- out-of-domain box cells (reflect_index / zero padding)
-    if (bz0 < 0 || bx0 < 0 || by0 < 0 || bz0 + B::BZ > g.zd || bx0 + B::BX > g.xd || by0 + B::BY > g.yd) {
-        for (int c = tid; c < B::NC; c += kTileThreads) {
-            const int bz = c / (B::BX * B::BY);
-            const int rem = c - bz * (B::BX * B::BY);
-            const int bx = rem / B::BY, by = rem - bx * B::BY;
-            const int zz = bz0 + bz, xx = bx0 + bx, yy = by0 + by;
-            if (zz >= 0 && zz < g.zd && xx >= 0 && xx < g.xd && yy >= 0 && yy < g.yd) continue;
-            // cells more than H beyond the domain are read by no output (and
-            // their reflection may fall outside the box)
-            if (zz >= g.zd + H || xx >= g.xd + H || yy >= g.yd + H) continue;
-            if (a.pad == APRGPU_PAD_ZERO) {
-                S[c] = Acc(0);
             } else {
-                const int rz = reflect_dev(zz, g.zd) - bz0, rx = reflect_dev(xx, g.xd) - bx0,
-                          ry = reflect_dev(yy, g.yd) - by0;
-                S[c] = S[(rz * B::BX + rx) * B::BY + ry];
+                for (;;) {
+                    int yb[kBatch];
+                    float vb[kBatch];
+#pragma unroll
+                    for (int q = 0; q < kBatch; ++q) {
+                        const bool ok = i + q < e;
+                        yb[q] = ok ? static_cast<int>(__ldg(ys + i + q)) : (G.yhi >> d) + 1;  // sentinel past the box
+                        vb[q] = ok ? __ldg(vs + i + q) : 0.0f;
+                    }
+                    int used = 0;
+#pragma unroll
+                    for (int q = 0; q < kBatch; ++q) {
+                        const int yy = yb[q];
+                        if ((yy << d) < G.yhi) {
+                            ++used;
+                            keep += ((yy + 1) << d) > ynext;
+                            const Acc v = static_cast<Acc>(vb[q]);
+                            if (d == 1) {
+                                Acc* p0 = S + r00 + (yy << 1);
+                                VT::st2(p0, v);
+                                if (nxr == 2) VT::st2(p0 + B::BY, v);
+                                if (nzr == 2) {
+                                    VT::st2(p0 + B::BX * B::BY, v);
+                                    if (nxr == 2) VT::st2(p0 + B::BX * B::BY + B::BY, v);
+                                }
+                            } else if (d == 2) {
+                                Acc* p0 = S + r00 + (yy << 2);
+#pragma unroll
+                                for (int z = 0; z < 4; ++z)
+#pragma unroll
+                                    for (int x = 0; x < 4; ++x)
+                                        if (z < nzr && x < nxr) VT::st4(p0 + (z * B::BX + x) * B::BY, v);
+                            } else {
+                                const int c0 = max((yy << d) - G.by0, 0), c1 = min(((yy + 1) << d) - G.by0, B::BY);
+                                const int slot = atomicAdd(&nreg, 1);
+                                if (slot < kMaxRegions) {
+                                    reg[slot] = Region<Acc>{rbase, nzr, nxr, c0 >> 2, (c1 - c0) >> 2, v};
+                                } else {
+                                    for (int z = 0; z < nzr; ++z)
+                                        for (int x = 0; x < nxr; ++x)
+                                            for (int c = c0; c < c1; c += 4)
+                                                VT::st4(S + rbase + (z * B::BX + x) * B::BY + c, v);
+                                }
+                            }
+                        }
+                    }
+                    i += used;
+                    if (used < kBatch) break;
+                }
+            }
+            rcur[t] = i - keep;
+        };
+        // cooperative fill of the queued regions: flattened over their quads
+        auto fill_regions = [&]() {
+            const int n = min(nreg, kMaxRegions);
+            if (n == 0) return;
+            if (warp == 0) {
+                // exclusive prefix of the regions' quad counts (<= 2 regions per lane)
+                int c0 = 0, c1 = 0;
+                if (2 * lane < n) c0 = reg[2 * lane].nz * reg[2 * lane].nx * reg[2 * lane].nq;
+                if (2 * lane + 1 < n) c1 = reg[2 * lane + 1].nz * reg[2 * lane + 1].nx * reg[2 * lane + 1].nq;
+                const int incl = warp_incl_scan(c0 + c1, lane);
+                rpre[2 * lane] = incl - c0 - c1;
+                rpre[2 * lane + 1] = incl - c1;
+                if (lane == 31) rpre[kMaxRegions] = incl;
+            }
+            __syncthreads();
+            const int total = rpre[kMaxRegions];
+            for (int c = tid; c < total; c += kTileThreads) {
+                // region of quad c: binary search over the prefix (<= 64 regions)
+                int lo = 0, hi = n - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (rpre[mid] <= c) lo = mid; else hi = mid - 1;
+                }
+                const Region<Acc> R = reg[lo];
+                const int j = c - rpre[lo];
+                const int row = j / R.nq, qd = j - row * R.nq;
+                const int zz = row / R.nx, xx = row - zz * R.nx;
+                VT::st4(S + R.rbase + (zz * B::BX + xx) * B::BY + 4 * (R.q0 + qd), R.v);
+            }
+            __syncthreads();
+            if (tid == 0) nreg = 0;
+        };
+        if (!(seg_flags & kMetaOverlap)) {
+            for (int t = tid; t < T.n; t += kTileThreads) scatter(t);
+            __syncthreads();
+            fill_regions();
+        } else {
+            // reference order: level l, l-1, ..., l-D, then interior nodes (last writer wins)
+            for (int p = 0; p <= T.D + 1; ++p) {
+                const int q0 = T.base[p];
+                const int q1 = p <= T.D ? T.base[p + 1] : T.n;
+                for (int t = q0 + tid; t < q1; t += kTileThreads) scatter(t);
+                __syncthreads();
+                fill_regions();
+                __syncthreads();
             }
         }
         __syncthreads();
-    }
 
-    // ---- outputs: one thread per particle, taps in the reference's order
-    const int NO = o_pre[64];
-    for (int o = tid; o < NO; o += kTileThreads) {
-        const int k = o_row[o];
-        const int i = o_s[k] + (o - o_pre[k]);
-        const int yy = __ldg(a.leaf.y + i);
-        const int bz = H + (k >> 3), bx = H + (k & 7);
-        // cell (z + H - az, x + H - ax, y + H - ay) for tap (az, ax, ay)
-        const Acc* base = S + ((bz + H) * B::BX + (bx + H)) * B::BY + (yy - by0 + H);
-        Acc acc = Acc(0);
-#pragma unroll
-        for (int az = 0; az < K; ++az)
-#pragma unroll
-            for (int ax = 0; ax < K; ++ax)
-#pragma unroll
-                for (int ay = 0; ay < K; ++ay)
-                    acc = fma_t(wsel<Acc>(a, (az * K + ax) * K + ay), base[-(az * B::BX + ax) * B::BY - ay], acc);
-        const float o_ = to_f(acc);
-        if (a.epi.mode == EPI_STORE) {
-            a.out[i] = o_;
-        } else if (a.epi.mode == EPI_RL_RATIO) {
-            const double bd = static_cast<double>(o_);
-            const double den = bd < a.epi.eps ? a.epi.eps : bd;  // std::max<double>(blurred, eps)
-            a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
-        } else {
-            a.epi.est[i] = __fmul_rn(a.epi.est[i], o_);
+        // ---- pad: out-of-domain box cells within H of the domain
+        if (G.z0 - H < 0 || G.x0 - H < 0 || G.y0 - H < 0 || G.z0 + kTZ + H > g.zd || G.x0 + kTX + H > g.xd ||
+            G.y0 + kTY + H > g.yd) {
+            for (int c = tid; c < B::NC; c += kTileThreads) {
+                const int bz = c / (B::BX * B::BY);
+                const int rem = c - bz * (B::BX * B::BY);
+                const int bx = rem / B::BY, by = rem - bx * B::BY;
+                const int zz = G.bz0 + bz, xx = G.bx0 + bx, yy = G.by0 + by;
+                if (yy < G.y0 - H || yy >= G.y0 + kTY + H) continue;  // pad columns: read by no output
+                if (zz >= 0 && zz < g.zd && xx >= 0 && xx < g.xd && yy >= 0 && yy < g.yd) continue;
+                if (zz >= g.zd + H || xx >= g.xd + H || yy >= g.yd + H) continue;  // read by no output
+                if (a.pad == APRGPU_PAD_ZERO) {
+                    S[c] = Acc(0);
+                } else {
+                    const int rz = reflect_dev(zz, g.zd) - G.bz0, rx = reflect_dev(xx, g.xd) - G.bx0,
+                              ry = reflect_dev(yy, g.yd) - G.by0;
+                    S[c] = S[(rz * B::BX + rx) * B::BY + ry];
+                }
+            }
+            __syncthreads();
         }
+
+        // ---- compact the 2x2x2 blocks that hold output particles
+        {
+            const int qz = tid >> 5, qx = (tid >> 3) & 3, qy = tid & 7;
+            const int* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
+            const int2 m0 = *reinterpret_cast<const int2*>(o);
+            const int2 m1 = *reinterpret_cast<const int2*>(o + kTY);
+            const int2 m2 = *reinterpret_cast<const int2*>(o + kTX * kTY);
+            const int2 m3 = *reinterpret_cast<const int2*>(o + kTX * kTY + kTY);
+            const int mx = max(max(max(m0.x, m0.y), max(m1.x, m1.y)), max(max(m2.x, m2.y), max(m3.x, m3.y)));
+            if (mx >= 0) blist[atomicAdd(&nblk, 1)] = static_cast<uint8_t>(tid);
+        }
+        __syncthreads();
+
+        // ---- apply: one thread per active block, 8 outputs
+        // neighbourhood y window of block qy: box index 2qy + kPadY - H .. +N,
+        // loaded as aligned pairs from the even index at or below it
+        constexpr int Y0 = kPadY - H;
+        constexpr int YA = Y0 & ~1, SH = Y0 - YA, NP = (SH + N + 1) / 2;
+        const int nb = nblk;
+        for (int q = tid; q < nb; q += kTileThreads) {
+            const int bidx = blist[q];
+            const int qz = bidx >> 5, qx = (bidx >> 3) & 3, qy = bidx & 7;
+            const Acc* base = S + ((2 * qz) * B::BX + 2 * qx) * B::BY + 2 * qy + YA;
+            Acc acc[8];
+            if constexpr (sizeof(Acc) == 4) {
+                // FAST: the two y-outputs of a block share every tap's weight ->
+                // packed fp32x2 FMA (same per-element rounding as two FFMAs)
+                float2 acc2[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int nz = N - 1; nz >= 0; --nz) {
+                    float v[N][N];
+#pragma unroll
+                    for (int nx = 0; nx < N; ++nx) {
+                        float r[2 * NP];
+#pragma unroll
+                        for (int p = 0; p < NP; ++p) {
+                            const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * B::BX + nx) * B::BY + 2 * p);
+                            r[2 * p] = t2.x;
+                            r[2 * p + 1] = t2.y;
+                        }
+#pragma unroll
+                        for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
+                    }
+#pragma unroll
+                    for (int oz = 0; oz < 2; ++oz) {
+                        const int az = oz + 2 * H - nz;
+                        if (az < 0 || az > 2 * H) continue;
+#pragma unroll
+                        for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+                            for (int ax = 0; ax < K; ++ax)
+#pragma unroll
+                                for (int ay = 0; ay < K; ++ay) {
+                                    const float w = W[(az * K + ax) * K + ay];
+                                    const int vx = ox + 2 * H - ax, vy = 2 * H - ay;
+                                    acc2[oz * 2 + ox] = ffma2(make_float2(w, w), make_float2(v[vx][vy], v[vx][vy + 1]),
+                                                              acc2[oz * 2 + ox]);
+                                }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    acc[2 * i] = acc2[i].x;
+                    acc[2 * i + 1] = acc2[i].y;
+                }
+            } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = Acc(0);
+#pragma unroll
+            for (int nz = N - 1; nz >= 0; --nz) {
+                Acc v[N][N];
+#pragma unroll
+                for (int nx = 0; nx < N; ++nx) {
+                    Acc r[2 * NP];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        const V2 t2 = *reinterpret_cast<const V2*>(base + (nz * B::BX + nx) * B::BY + 2 * p);
+                        r[2 * p] = t2.x;
+                        r[2 * p + 1] = t2.y;
+                    }
+#pragma unroll
+                    for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
+                }
+                // output (oz, ox, oy) reads neighbourhood cell (oz + 2H - az, ox + 2H - ax, oy + 2H - ay);
+                // planes stream from the top, so each output sees az ascending
+#pragma unroll
+                for (int oz = 0; oz < 2; ++oz) {
+                    const int az = oz + 2 * H - nz;
+                    if (az < 0 || az > 2 * H) continue;
+#pragma unroll
+                    for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+                        for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+                            for (int ax = 0; ax < K; ++ax)
+#pragma unroll
+                                for (int ay = 0; ay < K; ++ay)
+                                    acc[(oz * 2 + ox) * 2 + oy] = fma_t<Acc>(
+                                        W[(az * K + ax) * K + ay], v[ox + 2 * H - ax][oy + 2 * H - ay],
+                                        acc[(oz * 2 + ox) * 2 + oy]);
+                }
+            }
+            }
+            const int* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+                for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+                    for (int oy = 0; oy < 2; ++oy) {
+                        const int i = o[(oz * kTX + ox) * kTY + oy];
+                        if (i < 0) continue;
+                        const float r = to_f(acc[(oz * 2 + ox) * 2 + oy]);
+                        if (a.epi.mode == EPI_STORE) {
+                            a.out[i] = r;
+                        } else if (a.epi.mode == EPI_RL_RATIO) {
+                            // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
+                            const double bd = static_cast<double>(r);
+                            const double den = bd < a.epi.eps ? a.epi.eps : bd;
+                            a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
+                        } else {
+                            a.epi.est[i] = __fmul_rn(a.epi.est[i], r);  // deconv.hpp:102
+                        }
+                    }
+        }
+        __syncthreads();  // S / omap / blist are rebuilt by the next tile
     }
 }
 
@@ -357,10 +752,90 @@ __global__ void k_mark_tiles(const uint32_t* __restrict__ work, uint64_t n_work,
     }
 }
 
+TileLaunch base_launch(const aprgpu_apr* apr) {
+    const DevAccess& L = apr->leaf;
+    const DevAccess& Tr = apr->tree;
+    TileLaunch a{};
+    a.leaf = L.view();
+    a.tree = Tr.view();
+    a.tree_lmin = Tr.n_particles ? Tr.l_min : 1;
+    a.tree_lmax = Tr.n_particles ? Tr.l_max : 0;
+    return a;
+}
+
+void set_level(TileLaunch& a, const DevAccess& L, int l, uint32_t end) {
+    const int s = a.n_levels++;
+    a.lvl[s] = l;
+    a.tdim[s][0] = L.tile_dims[3 * l];
+    a.tdim[s][1] = L.tile_dims[3 * l + 1];
+    a.tdim[s][2] = L.tile_dims[3 * l + 2];
+    a.seg_end[s] = end;
+}
+
+// First use of an APR by the tile path: probe every tile, then cut each
+// level's tile columns into segments whose staged rows should fit.
+void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
+    DevAccess& L = apr->leaf;
+    if (L.tile_meta || !L.tiles) return;
+    std::lock_guard<std::mutex> lk(apr->ctx->mu);
+    if (L.tile_meta) return;
+    const uint64_t n = L.tile_off[L.l_max + 1];
+    uint8_t* meta = nullptr;
+    APR_CUDA(cudaMalloc(&meta, n + 16));
+    GpuBuf counts;
+    counts.ensure(2 * n + 16);
+    TileLaunch a = base_launch(apr);
+    uint32_t total = 0;
+    for (int l = L.l_min; l <= L.l_max; ++l) {
+        const uint32_t c = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
+        if (!c) continue;
+        total += c;
+        set_level(a, L, l, total);
+    }
+    std::vector<uint32_t> segs;
+    L.seg_off.assign(L.l_max + 2, 0);
+    if (total) {
+        a.tiles = L.tiles;
+        a.tile_base = static_cast<uint32_t>(L.tile_off[L.l_min]);
+        a.meta = meta;
+        a.count = counts.as<uint16_t>();
+        k_tile_probe<<<total, kTileThreads, 0, s>>>(a);
+        count_launch(apr->ctx);
+        APR_CUDA(cudaGetLastError());
+        std::vector<uint32_t> ids(n);
+        std::vector<uint16_t> cnt(n);
+        APR_CUDA(cudaMemcpyAsync(ids.data(), L.tiles, 4 * n, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaMemcpyAsync(cnt.data(), counts.p, 2 * n, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+        for (int l = L.l_min; l <= L.l_max; ++l) {
+            L.seg_off[l] = segs.size();
+            const uint64_t b = L.tile_off[l], e = L.tile_off[l + 1];
+            const uint32_t tyd = static_cast<uint32_t>(L.tile_dims[3 * l + 2]);
+            uint64_t i = b;
+            while (i < e) {
+                const uint32_t col = ids[i] / tyd;
+                uint64_t j = i + 1;
+                uint32_t est = cnt[i];
+                while (j < e && j - i < static_cast<uint64_t>(kSegTiles) && ids[j] / tyd == col &&
+                       est + cnt[j] <= static_cast<uint32_t>(kStageCap))
+                    est += cnt[j++];
+                if (i >= (1ull << 28)) fail(APRGPU_ERR_CAPABILITY, "too many tiles for the segment encoding");
+                segs.push_back(static_cast<uint32_t>(i << 4) | static_cast<uint32_t>(j - i - 1));
+                i = j;
+            }
+        }
+        L.seg_off[L.l_max + 1] = segs.size();
+        for (int l = 0; l < L.l_min; ++l) L.seg_off[l] = 0;
+    }
+    APR_CUDA(cudaMalloc(&L.segs, 4 * segs.size() + 4));
+    if (!segs.empty())
+        APR_CUDA(cudaMemcpy(L.segs, segs.data(), 4 * segs.size(), cudaMemcpyHostToDevice));
+    L.tile_meta = meta;
+}
+
 template <typename Acc, int H>
-void launch_tile(aprgpu_ctx* ctx, const TileArgs& a, cudaStream_t s) {
-    if (!a.n_tiles) return;
-    k_conv_tile<Acc, H><<<a.n_tiles, kTileThreads, 0, s>>>(a);
+void launch_segs(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
+    k_conv_seg<Acc, H><<<n, kTileThreads, 0, s>>>(a);
     count_launch(ctx);
     APR_CUDA(cudaGetLastError());
 }
@@ -370,7 +845,6 @@ void launch_tile(aprgpu_ctx* ctx, const TileArgs& a, cudaStream_t s) {
 void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a) {
     a.tile_off.assign(a.l_max + 2, 0);
     a.tile_dims.assign(3 * (a.l_max + 1), 0);
-    std::vector<uint32_t> counts(a.l_max + 1, 0);
     uint64_t total_flags = 0;
     for (int l = a.l_min; l <= a.l_max; ++l) {
         const uint64_t tzd = (a.zd[l] + kTZ - 1) / kTZ, txd = (a.xd[l] + kTX - 1) / kTX, tyd = (a.yd[l] + kTY - 1) / kTY;
@@ -382,7 +856,6 @@ void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a) {
     if (total_flags >= (1ull << 32)) fail(APRGPU_ERR_CAPABILITY, "tile grid exceeds u32 ids");
     GpuBuf flags, out, nsel, temp;
     flags.ensure(total_flags + 16);
-    std::vector<uint32_t> host_tiles;
     std::vector<std::vector<uint32_t>> per_level(a.l_max + 1);
     uint64_t off = 0;
     for (int l = a.l_min; l <= a.l_max; ++l) {
@@ -424,39 +897,65 @@ void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a) {
                                 cudaMemcpyHostToDevice));
 }
 
-bool conv_tile_level(aprgpu_apr* apr, int l, const float* values, const float* tree_values, const int* k3,
-                     const float* w_host, int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s) {
+// Runs every level whose stencil is an isotropic 3^3 or 5^3 through the
+// segment kernel (one launch per extent and run of consecutive levels, coarse
+// levels first); sets done[l] for them.
+void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* values, const float* tree_values,
+                      int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s, bool* done) {
     const DevAccess& L = apr->leaf;
-    const DevAccess& T = apr->tree;
-    if (!L.tiles) return false;
-    if (!(k3[0] == k3[1] && k3[1] == k3[2] && (k3[0] == 3 || k3[0] == 5))) return false;
-    TileArgs a{};
-    a.leaf = L.view();
-    a.tree = T.view();
-    a.val = values;
-    a.tval = tree_values;
-    a.tiles = L.tiles + L.tile_off[l];
-    a.n_tiles = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
-    a.tzd = L.tile_dims[3 * l];
-    a.txd = L.tile_dims[3 * l + 1];
-    a.tyd = L.tile_dims[3 * l + 2];
-    a.l = l;
-    a.pad = pad;
-    a.tree_at_l = (T.n_particles > 0 && l >= T.l_min && l <= T.l_max) ? 1 : 0;
-    a.out = out;
-    a.epi = epi;
-    const int n = k3[0] * k3[1] * k3[2];
-    for (int i = 0; i < n; ++i) {
-        a.wf[i] = w_host[i];
-        a.wd[i] = static_cast<double>(w_host[i]);
-    }
+    if (!L.tiles) return;
+    ensure_tile_meta(apr, s);
+    // APRGPU_TILE_SPLIT=1: one launch per level (profiling aid)
+    static const bool split = [] {
+        const char* e = std::getenv("APRGPU_TILE_SPLIT");
+        return e && e[0] == '1';
+    }();
     const bool exact = accum == APRGPU_ACCUM_EXACT;
-    if (k3[0] == 3) {
-        if (exact) launch_tile<double, 1>(apr->ctx, a, s); else launch_tile<float, 1>(apr->ctx, a, s);
-    } else {
-        if (exact) launch_tile<double, 2>(apr->ctx, a, s); else launch_tile<float, 2>(apr->ctx, a, s);
+    for (int H = 1; H <= 2; ++H) {
+        const int K = 2 * H + 1;
+        auto ok = [&](int lv) {
+            const int* k = &pyr->k3[3 * (lv - pyr->l_min)];
+            return k[0] == K && k[1] == K && k[2] == K;
+        };
+        int l = L.l_min;
+        while (l <= L.l_max) {
+            if (!ok(l)) {
+                ++l;
+                continue;
+            }
+            TileLaunch b = base_launch(apr);
+            b.val = values;
+            b.tval = tree_values;
+            b.wf = pyr->w_dev;
+            b.wd = pyr->wd_dev;
+            b.pad = pad;
+            b.out = out;
+            b.epi = epi;
+            b.tiles = L.tiles;
+            b.meta = L.tile_meta;
+            const int first = l;
+            uint32_t total = 0;
+            for (; l <= L.l_max && ok(l); ++l) {
+                done[l] = true;
+                const uint32_t c = static_cast<uint32_t>(L.seg_off[l + 1] - L.seg_off[l]);
+                if (!c) continue;
+                total += c;
+                b.woff[b.n_levels] = pyr->off[l - pyr->l_min];
+                set_level(b, L, l, total);
+                if (split) {
+                    ++l;
+                    break;
+                }
+            }
+            if (!total) continue;
+            b.segs = L.segs + L.seg_off[first];
+            if (H == 1) {
+                if (exact) launch_segs<double, 1>(apr->ctx, b, total, s); else launch_segs<float, 1>(apr->ctx, b, total, s);
+            } else {
+                if (exact) launch_segs<double, 2>(apr->ctx, b, total, s); else launch_segs<float, 2>(apr->ctx, b, total, s);
+            }
+        }
     }
-    return true;
 }
 
 }  // namespace aprgpu

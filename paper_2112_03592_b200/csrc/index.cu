@@ -37,6 +37,10 @@ void DevAccess::release() {
     cudaFree(rb);
     cudaFree(work);
     cudaFree(tiles);
+    cudaFree(tile_meta);
+    cudaFree(segs);
+    tile_meta = nullptr;
+    segs = nullptr;
     y = nullptr;
     rb = nullptr;
     work = nullptr;

@@ -64,6 +64,9 @@ struct DevAccess {
     uint32_t* tiles = nullptr;             // device, linear tile ids per level
     std::vector<uint64_t> tile_off;        // l_max+2 offsets into tiles
     std::vector<int> tile_dims;            // 3 per level: tile grid (z, x, y)
+    uint8_t* tile_meta = nullptr;          // device, one byte per tile (coarse depth, fill flags); lazy
+    uint32_t* segs = nullptr;              // device, tile-column segments (first tile << 4 | count - 1); lazy
+    std::vector<uint64_t> seg_off;         // l_max+2 offsets into segs
     AccessView view() const;
     void release();
 };
@@ -119,8 +122,8 @@ void row_spans(aprgpu_ctx* ctx, const DevAccess& a, int level, int32_t* z, int32
 
 // conv_tile.cu
 void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a);
-bool conv_tile_level(aprgpu_apr* apr, int l, const float* values, const float* tree_values, const int* k3,
-                     const float* w_host, int pad, int accum, float* out, const struct EpiArgs& epi, cudaStream_t s);
+void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* values, const float* tree_values,
+                      int pad, int accum, float* out, const struct EpiArgs& epi, cudaStream_t s, bool* done);
 
 // tree.cu
 void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr);
