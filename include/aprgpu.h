@@ -149,6 +149,15 @@ int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_valu
 int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, int kx, int ky, int iterations,
               double epsilon, int accum, float* out, int ptr_kind, void* stream);
 
+/* rl_apr resumed from a running estimate (estimate_in[n_particles]; NULL =
+ * start from the clamped observation, i.e. aprgpu_rl).  The reference's state
+ * between iterations is exactly (u, epsilon, estimate), so running k iterations
+ * and resuming for m more is bit-identical to k + m iterations: this is how the
+ * C++ drop-in serves rl_apr's observer (deconv.hpp:103-104). */
+int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estimate_in, const float* psf, int kz,
+                     int kx, int ky, int iterations, double epsilon, int accum, float* out, int ptr_kind,
+                     void* stream);
+
 /* ---- inputs: synthetic volumes and APR construction (input side of the path) */
 /* generate_spheres (synthetic.hpp:74-111, no noise) into out[nz*nx*ny] (z,x,y
  * order, y fastest), on the device; bit-identical to the reference volume. */

@@ -1,0 +1,253 @@
+// include/aprkit_gpu.hpp -- C++ host runtime of the B200 drop-in for aprkit's
+// hot path (APR-native convolution, arXiv 2112.03592).
+//
+// This header is the host side above the C-ABI (include/aprgpu.h): it keeps
+// the reference's C++ types (aprkit::APR, LinearAccess, ParticleValues,
+// StencilPyramid, PadMode, ConvolveOptions, RLConfig) and turns them into
+// C-ABI calls, mapping status codes back onto aprkit's exception taxonomy
+// (errors.hpp:9-41).  The drop-in headers under include/aprkit_gpu/aprkit/
+// use it to replace convolve_apr / nonempty_row_index (convolve.hpp),
+// fill_tree / init_tree_structure (tree.hpp) and rl_apr (deconv.hpp); a
+// program compiled with -Iinclude/aprkit_gpu ahead of the reference's include
+// directory gets the GPU path with no source change.
+//
+// Runtime model: one aprgpu context per process on device $APRGPU_DEVICE
+// (default 0).  APRs are uploaded on first use and cached by a content
+// fingerprint (structure arrays + dims), so repeated fill_tree/convolve_apr
+// calls on the same APR reuse the device structure, tile lists and work lists.
+// Accumulation: EXACT (fp64 in the reference's order, bit-identical) unless
+// $APRGPU_ACCUM=fast.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "aprgpu.h"
+#include "aprkit/apr.hpp"
+#include "aprkit/errors.hpp"
+#include "aprkit/linear_access.hpp"
+#include "aprkit/reconstruct.hpp"
+#include "aprkit/stencil.hpp"
+
+namespace aprkit {
+namespace gpu {
+
+// C-ABI status -> the reference's exception types (errors.hpp:9-41).
+[[noreturn]] inline void raise_status(int st) {
+    const std::string m = aprgpu_last_error();
+    switch (st) {
+        case APRGPU_ERR_RANGE: throw RangeError(m);
+        case APRGPU_ERR_CAPABILITY: throw CapabilityError(m);
+        case APRGPU_ERR_INTEGRITY: throw IntegrityError(m);
+        case APRGPU_ERR_OOM: throw std::bad_alloc();
+        default: throw std::runtime_error("aprgpu: " + m);
+    }
+}
+
+inline void check(int st) {
+    if (st != APRGPU_OK) raise_status(st);
+}
+
+inline aprgpu_access_desc describe(const LinearAccess& a) {
+    aprgpu_access_desc d{};
+    d.l_min = a.l_min;
+    d.l_max = a.l_max;
+    d.z_dim = a.z_dim.data();
+    d.x_dim = a.x_dim.data();
+    d.y_dim = a.y_dim.data();
+    d.y_idx = a.y_idx.empty() ? nullptr : a.y_idx.data();
+    d.n_particles = a.y_idx.size();
+    d.xz_end = a.xz_end.empty() ? nullptr : a.xz_end.data();
+    d.n_rows = a.xz_end.size();
+    d.level_offset = a.level_offset.data();
+    return d;
+}
+
+// An access structure the device can take: level vectors sized l_max + 1.
+inline bool well_formed(const LinearAccess& a) {
+    const std::size_t n = static_cast<std::size_t>(a.l_max) + 1;
+    return a.l_min >= 0 && a.l_min <= a.l_max && a.z_dim.size() >= n && a.x_dim.size() >= n &&
+           a.y_dim.size() >= n && a.level_offset.size() >= n;
+}
+
+// 64-bit content fingerprint (FNV-1a over 8-byte words).
+class Fingerprint {
+public:
+    void bytes(const void* p, std::size_t n) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        std::size_t i = 0;
+        for (; i + 8 <= n; i += 8) {
+            std::uint64_t w;
+            std::memcpy(&w, c + i, 8);
+            mix(w);
+        }
+        std::uint64_t tail = 0;
+        std::memcpy(&tail, c + i, n - i);
+        mix(tail ^ (static_cast<std::uint64_t>(n) << 56));
+    }
+    template <class T>
+    void vec(const std::vector<T>& v) {
+        mix(v.size());
+        if (!v.empty()) bytes(v.data(), v.size() * sizeof(T));
+    }
+    void access(const LinearAccess& a) {
+        mix(static_cast<std::uint64_t>(a.l_min) << 32 | static_cast<std::uint32_t>(a.l_max));
+        vec(a.z_dim);
+        vec(a.x_dim);
+        vec(a.y_dim);
+        vec(a.y_idx);
+        vec(a.xz_end);
+        vec(a.level_offset);
+    }
+    std::uint64_t value() const { return h_; }
+
+private:
+    void mix(std::uint64_t w) {
+        h_ ^= w;
+        h_ *= 0x100000001b3ull;
+        h_ ^= h_ >> 29;
+    }
+    std::uint64_t h_ = 0xcbf29ce484222325ull;
+};
+
+// Process-wide device runtime: context + LRU cache of uploaded APRs.
+class Runtime {
+public:
+    static Runtime& get() {
+        static Runtime rt;
+        return rt;
+    }
+
+    aprgpu_ctx* ctx() { return ctx_; }
+
+    int accum() const { return accum_; }
+
+    // Device handle of an APR (uploaded on first use).  With an empty
+    // tree_access the interior structure is built on the device
+    // (init_tree_structure semantics).
+    aprgpu_apr* upload(const APR& apr) {
+        Fingerprint f;
+        f.access(apr.access);
+        const bool tree = well_formed(apr.tree_access);
+        if (tree) f.access(apr.tree_access);
+        f.bytes(apr.source_dims.data(), sizeof(int) * 3);
+        return lookup(f.value(), [&](aprgpu_apr** out) {
+            if (!well_formed(apr.access)) throw RangeError("APR access structure has no levels");
+            const aprgpu_access_desc leaf = describe(apr.access);
+            aprgpu_access_desc td{};
+            if (tree) td = describe(apr.tree_access);
+            const int32_t dims[3] = {apr.source_dims[0], apr.source_dims[1], apr.source_dims[2]};
+            return aprgpu_upload_access(ctx_, &leaf, tree ? &td : nullptr, dims, out);
+        });
+    }
+
+    // Device handle of a bare access structure (leaf only; dims = its finest grid).
+    aprgpu_apr* upload(const LinearAccess& a, const std::array<int, 3>& dims) {
+        Fingerprint f;
+        f.access(a);
+        f.bytes(dims.data(), sizeof(int) * 3);
+        f.bytes("access-only", 11);
+        return lookup(f.value(), [&](aprgpu_apr** out) {
+            if (!well_formed(a)) throw RangeError("access structure has no levels");
+            const aprgpu_access_desc leaf = describe(a);
+            const int32_t d3[3] = {dims[0], dims[1], dims[2]};
+            return aprgpu_upload_access(ctx_, &leaf, nullptr, d3, out);
+        });
+    }
+
+    ~Runtime() {
+        for (auto& e : cache_) aprgpu_apr_free(e.second);
+        if (ctx_) aprgpu_ctx_free(ctx_);
+    }
+
+private:
+    Runtime() {
+        const char* dev = std::getenv("APRGPU_DEVICE");
+        check(aprgpu_init(dev ? std::atoi(dev) : 0, &ctx_));
+        const char* acc = std::getenv("APRGPU_ACCUM");
+        accum_ = (acc && std::string(acc) == "fast") ? APRGPU_ACCUM_FAST : APRGPU_ACCUM_EXACT;
+    }
+
+    template <class Upload>
+    aprgpu_apr* lookup(std::uint64_t key, Upload&& up) {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto it = cache_.begin(); it != cache_.end(); ++it)
+            if (it->first == key) {
+                cache_.splice(cache_.begin(), cache_, it);
+                return cache_.front().second;
+            }
+        aprgpu_apr* h = nullptr;
+        check(up(&h));
+        cache_.emplace_front(key, h);
+        while (cache_.size() > kCacheSize) {
+            aprgpu_apr_free(cache_.back().second);
+            cache_.pop_back();
+        }
+        return h;
+    }
+
+    static constexpr std::size_t kCacheSize = 8;
+    aprgpu_ctx* ctx_ = nullptr;
+    int accum_ = APRGPU_ACCUM_EXACT;
+    std::mutex mu_;
+    std::list<std::pair<std::uint64_t, aprgpu_apr*>> cache_;
+};
+
+// A StencilPyramid held on the device for one call.
+class DevicePyramid {
+public:
+    explicit DevicePyramid(const StencilPyramid& p) {
+        std::vector<float> w;
+        std::vector<int32_t> k3;
+        for (const Stencil& s : p.stencils) {
+            w.insert(w.end(), s.weights.begin(), s.weights.end());
+            k3.insert(k3.end(), {s.kz, s.kx, s.ky});
+        }
+        if (p.stencils.empty()) throw RangeError("StencilPyramid has no levels");
+        check(aprgpu_pyramid_create_explicit(Runtime::get().ctx(), w.data(), k3.data(), p.l_min, p.l_max, &h_));
+    }
+    ~DevicePyramid() { aprgpu_pyramid_free(h_); }
+    DevicePyramid(const DevicePyramid&) = delete;
+    DevicePyramid& operator=(const DevicePyramid&) = delete;
+    aprgpu_pyramid* get() const { return h_; }
+
+private:
+    aprgpu_pyramid* h_ = nullptr;
+};
+
+inline std::uint64_t count(aprgpu_apr* h, int which) {
+    aprgpu_access_info info{};
+    check(aprgpu_access_get_info(h, which, &info));
+    return info.n_particles;
+}
+
+inline LinearAccess download(aprgpu_apr* h, int which) {
+    aprgpu_access_info info{};
+    check(aprgpu_access_get_info(h, which, &info));
+    LinearAccess a;
+    a.l_min = info.l_min;
+    a.l_max = info.l_max;
+    const std::size_t n = static_cast<std::size_t>(info.l_max) + 1;
+    a.z_dim.resize(n);
+    a.x_dim.resize(n);
+    a.y_dim.resize(n);
+    a.level_offset.resize(n);
+    a.y_idx.resize(info.n_particles);
+    a.xz_end.resize(info.n_rows);
+    check(aprgpu_download_access(h, which, a.y_idx.data(), a.xz_end.data(), a.level_offset.data(), a.z_dim.data(),
+                                 a.x_dim.data(), a.y_dim.data()));
+    return a;
+}
+
+}  // namespace gpu
+}  // namespace aprkit

@@ -450,6 +450,13 @@ int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_valu
 
 int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, int kx, int ky, int iterations,
               double epsilon, int accum, float* out, int ptr_kind, void* stream) {
+    return aprgpu_rl_resume(apr, observed, nullptr, psf, kz, kx, ky, iterations, epsilon, accum, out, ptr_kind,
+                            stream);
+}
+
+int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estimate_in, const float* psf, int kz,
+                     int kx, int ky, int iterations, double epsilon, int accum, float* out, int ptr_kind,
+                     void* stream) {
     return guard([&] {
         need(apr && observed && psf && out, "null argument");
         need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
@@ -499,6 +506,9 @@ int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, 
                                                                                                        np);
         aprgpu::count_launch(ctx);
         APR_CUDA(cudaGetLastError());
+        if (estimate_in && estimate_in != est)  // resume: the running estimate replaces the clamped observation
+            APR_CUDA(cudaMemcpyAsync(est, estimate_in, 4 * np,
+                                     ptr_kind == APRGPU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
         // mean of the clamped observations in the reference's sequential order (deconv.hpp:90-92)
         host_obs.resize(np);
         APR_CUDA(cudaMemcpyAsync(host_obs.data(), u, 4 * np, cudaMemcpyDeviceToHost, s));
