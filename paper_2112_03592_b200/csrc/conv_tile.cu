@@ -1,51 +1,45 @@
 // Box-tile convolution for isotropic 3^3 / 5^3 levels (the hot path).
 //
-// Output tiles: (level l, 8z x 8x x 16y) boxes of level-l cells holding at
-// least one particle (tile lists are built once per APR at upload, from the
-// non-empty rows).  Work item: a SEGMENT = up to kSegTiles consecutive
-// occupied tiles of one (z, x) tile column.  One 128-thread CTA per segment:
+// Work item: one (level l, 8z x 8x x kTY y) output tile holding at least one
+// particle (tile lists are built once per APR at upload, from the non-empty
+// rows).  All levels that use the same isotropic extent run in ONE launch
+// (coarse levels first, so their few tiles overlap the finest level's bulk).
+// One 128-thread CTA per tile:
 //
-//   stage   every source row that can reach the segment's boxes -- the level-l
-//           leaf rows and interior rows of the (8+2H)^2 halo plane, and the
-//           level l-d leaf rows covering it for d = 1..D -- is searched ONCE
-//           (two lower_bounds) for the segment's y-range, and the particles
-//           found (y and value) are copied into shared memory with coalesced
-//           warp-per-row loads.  This replaces per-tile dependent global
-//           searches/walks (the latency chain that bounds a tile) by one
-//           search per row per segment plus shared-memory walks.
-//   per tile of the segment (in y order):
-//     fill  the level-l image of the tile's (8+2H)x(8+2H)x(16+2H) box is
-//           rebuilt in shared memory (fill_level_row semantics,
-//           reconstruct.hpp:41-69): each source row is walked from its
-//           cursor by one thread; level-l leaves / interior nodes write their
-//           cell, a coarse leaf at depth d writes its 2^d-aligned group of
-//           cells (constant upsampling) as vector stores (the box's y origin
-//           is y0 - 4, so pairs and quads are aligned); leaves >= 3 levels
-//           coarser are filled by the whole CTA.  In a valid APR every
-//           in-domain cell is covered by exactly one source, so all rows
-//           scatter in one unordered pass.
-//     pad   out-of-domain cells within H of the domain: reflect_index / 0.
-//     apply the tile is cut into 2x2x2 cell blocks (an APR refines cells into
+//   rows    every source row that can reach the tile's (8+2H)x(8+2H)x(kTY+2H)
+//           box -- the level-l leaf rows and interior rows of the halo plane,
+//           and the level l-d leaf rows covering it for d = 1..D -- is
+//           resolved by one thread: its particle range inside the box's
+//           y-extent (two lower_bounds) and its box geometry, packed.
+//   flatten a block-wide scan of the ranges numbers every source particle of
+//           the tile; each particle gets its row id in shared memory.
+//   fill    one thread per source PARTICLE (warp-uniform work: no per-row
+//           loops): level-l leaves / interior nodes write their cell and the
+//           output map, a coarse leaf at depth d writes its 2^d-aligned group
+//           of cells (constant upsampling, fill_level_row semantics,
+//           reconstruct.hpp:41-69) as vector stores (the box's y origin is
+//           y0 - 4, so pairs and quads are aligned); leaves >= 3 levels
+//           coarser are queued and filled by the whole CTA.  In a valid APR
+//           every in-domain cell is covered by exactly one source, so all
+//           particles scatter in one unordered pass.
+//   pad     out-of-domain cells within H of the domain: reflect_index / 0.
+//   apply   the tile is cut into 2x2x2 cell blocks (an APR refines cells into
 //           sibling octets, so finest-level particles come in complete
 //           blocks); blocks holding particles are compacted and each is
 //           evaluated by one thread from a (2+2H)^3 neighbourhood streamed
-//           plane by plane through registers (8 outputs, 3 vector loads per
-//           neighbourhood row).  Every output's taps accumulate in the
-//           reference's exact (az, ax, ay) order (LevelSlab::apply,
+//           plane by plane through registers.  Every output's taps accumulate
+//           in the reference's exact (az, ax, ay) order (LevelSlab::apply,
 //           convolve.hpp:154-169): fp64 FMA of exact products in EXACT mode
-//           (bit-identical), fp32 FMA in FAST mode.
+//           (bit-identical), fp32 FMA (packed fp32x2 over the block's y pair)
+//           in FAST mode.
 //
 // A probe kernel (k_tile_probe) runs once per APR and stores one byte per
 // tile: D (deepest coarse depth whose leaves reach into the 5^3 box, so no
 // coverage counting is needed), OVERLAP (malformed APR: some cell covered
-// twice -> the segment is filled in the reference's order, level l, l-1, ...,
+// twice -> the tile is filled in the reference's order, level l, l-1, ...,
 // then interior nodes, last writer wins) and HOLES (some cell uncovered -> the
-// box is zeroed first); plus a per-tile source-particle count used to cut the
-// tile columns into segments that fit the staging buffer.  A segment whose
-// rows still do not fit is filled straight from global memory.
-//
-// All levels that use the same isotropic extent run in ONE launch (coarse
-// levels first), so the few, short coarse segments overlap the finest level.
+// box is zeroed first).  The probe uses the 5^3 box, a superset of the 3^3
+// box, so one byte serves both stencil sizes.
 #include <algorithm>
 #include <cstdlib>
 
@@ -54,14 +48,17 @@
 
 #include "common.cuh"
 
+#ifndef APRGPU_TILE_Y
+#define APRGPU_TILE_Y 32
+#endif
+
 namespace aprgpu {
 
-constexpr int kTZ = 8, kTX = 8, kTY = 16, kTileThreads = 128;
+constexpr int kTZ = 8, kTX = 8, kTY = APRGPU_TILE_Y, kTileThreads = 128;
+constexpr int kBlocks = (kTZ / 2) * (kTX / 2) * (kTY / 2);  // 2x2x2 output blocks per tile
 constexpr int kProbeH = 2;
-constexpr int kSegTiles = 16;      // tiles per segment (4-bit count)
-constexpr int kStageCap = 4096;    // source particles per segment (segment cut estimate)
-constexpr int kBatch = 8;          // particles per walk batch (independent loads in flight)
 constexpr int kMaxSrcRows = 512;   // >= 2*(8+2*2)^2 + coarse rows of a 5^3 box
+constexpr int kMaxFlat = 4096;     // source particles per flattened chunk
 constexpr int kPadY = 4;           // box y origin = y0 - kPadY (>= H, multiple of 4)
 enum : uint8_t { kMetaDepth = 0x1f, kMetaOverlap = 0x20, kMetaHoles = 0x40 };
 
@@ -73,9 +70,7 @@ struct TileLaunch {
     const float* tval;
     const uint32_t* tiles;   // tile ids of all levels (absolute indexing)
     const uint8_t* meta;     // one byte per tile
-    uint16_t* count;         // probe only: source particles per tile
-    const uint32_t* segs;    // work items: (first tile << 4) | (tiles - 1)
-    uint32_t tile_base;      // probe only: first tile of the launch
+    uint32_t tile_base;      // first tile of the launch (blocks map to consecutive tiles)
     int n_levels;                   // level segments in this launch
     int lvl[kMaxLevels];            // level of each segment
     uint32_t seg_end[kMaxLevels];   // exclusive end (in blocks) of each level segment
@@ -204,7 +199,7 @@ __device__ __forceinline__ bool resolve_row(const TileLaunch& a, const Geo& G, c
         J.xA = xx;
         J.xB = xx + 1;
         J.inner = !J.is_tree && bz >= H && bz < H + kTZ && bx >= H && bx < H + kTX;
-        J.obase = ((bz - H) * kTX + (bx - H)) * kTY - G.y0;
+        J.obase = (bz - H) * kTX + (bx - H);  // inner row id (when inner)
     } else {
         int czlo, cxlo, nxc;
         coarse_rows(G, d, czlo, cxlo, nxc);
@@ -227,14 +222,14 @@ __device__ __forceinline__ bool resolve_row(const TileLaunch& a, const Geo& G, c
 }
 
 // ---------------------------------------------------------------- probe ----
-// Per tile: deepest coarse depth reaching into the (5^3) box, whether the
-// sources overlap or leave holes there, and how many source particles reach
-// it.  Scans every depth down to l_min, so D is exact even for malformed APRs.
+// Per tile: deepest coarse depth reaching into the (5^3) box and whether the
+// sources overlap or leave holes there.  Scans every depth down to l_min, so D
+// is exact even for malformed APRs.
 __global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_constant__ TileLaunch a) {
     using B = Box<kProbeH>;
     __shared__ uint8_t cnt[B::NC];
     __shared__ int hit[kMetaDepth + 2];
-    __shared__ int flags, total;
+    __shared__ int flags;
     __shared__ SrcTable T;
     const int tid = threadIdx.x;
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
@@ -248,11 +243,9 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_consta
     const int Dall = min(l - a.leaf.l_min, static_cast<int>(kMetaDepth));
     if (tid == 0) {
         flags = 0;
-        total = 0;
         make_src_table<kProbeH>(G, Dall, tree, T);
     }
     __syncthreads();
-    int mine = 0;
     for (int t = tid; t < T.n; t += kTileThreads) {
         RowJob J;
         if (!resolve_row<kProbeH>(a, G, T, t, J)) continue;
@@ -262,7 +255,6 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_consta
         for (uint32_t i = lower_bound_u16(ys, J.b, J.e, G.ylo >> d); i < J.e; ++i) {
             const int yy = __ldg(ys + i);
             if ((yy << d) >= G.yhi) break;
-            ++mine;
             const int yA = max(yy << d, G.ylo), yB = min((yy + 1) << d, G.yhi);
             for (int z = J.zA; z < J.zB; ++z)
                 for (int x = J.xA; x < J.xB; ++x)
@@ -275,7 +267,6 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_consta
         }
         if (any) hit[d] = 1;
     }
-    if (mine) atomicAdd(&total, mine);
     __syncthreads();
     int f = 0;
     for (int c = tid; c < B::NC; c += kTileThreads) {
@@ -295,7 +286,6 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_consta
         for (int d = 1; d <= Dall; ++d)
             if (hit[d]) D = d;
         const_cast<uint8_t*>(a.meta)[tile] = static_cast<uint8_t>(D | flags);
-        a.count[tile] = static_cast<uint16_t>(min(total, 65535));
     }
 }
 
@@ -344,335 +334,289 @@ template <> struct Vec<double> {
 };
 
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 6 : 7))
-    k_conv_seg(const __grid_constant__ TileLaunch a) {
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 3) : (H == 2 ? 4 : 5))
+    k_conv_tile(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
     using VT = Vec<Acc>;
     using V2 = typename VT::T2;
     constexpr int K = 2 * H + 1, N = 2 + 2 * H, KW = K * K * K;
-    __shared__ __align__(16) Acc S[B::NC];
-    __shared__ __align__(16) int omap[kTZ * kTX * kTY];
+    extern __shared__ __align__(16) unsigned char box_smem[];
+    Acc* S = reinterpret_cast<Acc*>(box_smem);  // B::NC cells
+    // output map: per inner cell the particle's offset from its row's first
+    // particle in the box (0xff: no output particle); per inner row that index
+    __shared__ __align__(16) uint8_t omap[kTZ * kTX * kTY];
+    __shared__ uint32_t orow[kTZ * kTX];
     __shared__ Acc W[KW];
-    __shared__ uint8_t blist[kTileThreads];
-    __shared__ int nblk, nreg, seg_flags;
+    __shared__ uint16_t blist[kBlocks];
+    __shared__ int nblk, nreg;
     __shared__ Region<Acc> reg[kMaxRegions];
     __shared__ int rpre[kMaxRegions + 1];
     __shared__ SrcTable T;
-    __shared__ int rcur[kMaxSrcRows];       // per source row: next particle to visit
-    __shared__ int rend[kMaxSrcRows];       // per source row: end of the row
-    __shared__ uint32_t rinfo[kMaxSrcRows]; // per source row: packed geometry
-    __shared__ int16_t rob[kMaxSrcRows];    // per source row: output-map offset
+    __shared__ uint32_t rinfo[kMaxSrcRows];  // packed row geometry
+    __shared__ uint32_t rsrc[kMaxSrcRows];   // global index of the row's first particle in the box
+    __shared__ int roff[kMaxSrcRows + 1];    // flattened offsets; roff[kMaxSrcRows] = total
+    __shared__ int wsum[kTileThreads / 32];
+    __shared__ uint16_t rid[kMaxFlat];       // row of each flattened particle (current chunk)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
     const int l = a.lvl[s];
     const LevelG g = a.leaf.g[l];
-    const uint32_t seg = a.segs[blockIdx.x];
-    const uint32_t t0 = seg >> 4;
-    const int nt = static_cast<int>(seg & 15) + 1;
-    const int txd = a.tdim[s][1], tyd = a.tdim[s][2];
+    const uint32_t tix = a.tile_base + blockIdx.x;
+    const Geo G = make_geo<H>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], g);
+    const int meta = a.meta[tix];
     const int tree = (l >= a.tree_lmin && l <= a.tree_lmax) ? 1 : 0;
 
-    // segment geometry: the first tile's box extended to the last tile's y
-    Geo SG = make_geo<H>(l, a.tiles[t0], txd, tyd, g);
-    SG.yhi = make_geo<H>(l, a.tiles[t0 + nt - 1], txd, tyd, g).yhi;
+    // ---- init: weights, output map, (holes only) zeroed box, source table
     for (int i = tid; i < KW; i += kTileThreads)
         W[i] = sizeof(Acc) == 8 ? static_cast<Acc>(a.wd[a.woff[s] + i]) : static_cast<Acc>(a.wf[a.woff[s] + i]);
+    {
+        uint4* om = reinterpret_cast<uint4*>(omap);
+        for (int i = tid; i < kTZ * kTX * kTY / 16; i += kTileThreads) om[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+    if (meta & kMetaHoles)
+        for (int i = tid; i < B::NC; i += kTileThreads) S[i] = Acc(0);
     if (tid == 0) {
-        int D = 0, f = 0;
-        for (int k = 0; k < nt; ++k) {
-            const int m = a.meta[t0 + k];
-            D = max(D, m & kMetaDepth);
-            f |= m & (kMetaOverlap | kMetaHoles);
-        }
-        seg_flags = f;
-        make_src_table<H>(SG, D, tree, T);
+        nblk = 0;
         nreg = 0;
+        make_src_table<H>(G, meta & kMetaDepth, tree, T);
     }
     __syncthreads();
 
-    // ---- segment start: one search per source row (the cursors then only move
-    // forward) and the row's box geometry, packed:
+    // ---- rows: range inside the box and packed geometry, one thread per row
     //   rinfo = d | is_tree << 5 | inner << 6 | (nz-1) << 7 | (nx-1) << 11 | rbase << 15
-    // with rbase = box offset of (zA, xA, y = by0), rob = output-map offset of (row, y = y0)
-    for (int t = tid; t < T.n; t += kTileThreads) {
-        RowJob J;
-        int i = 0, e = 0;
-        uint32_t info = 0;
-        int ob = 0;
-        if (resolve_row<H>(a, SG, T, t, J)) {
-            const uint16_t* ys = J.is_tree ? a.tree.y : a.leaf.y;
-            i = static_cast<int>(lower_bound_u16(ys, J.b, J.e, SG.ylo >> J.d));
-            e = static_cast<int>(J.e);
-            const uint32_t rbase = static_cast<uint32_t>(J.r00 + SG.by0);
-            info = static_cast<uint32_t>(J.d) | (J.is_tree << 5) | (J.inner << 6) |
-                   (static_cast<uint32_t>(J.zB - J.zA - 1) << 7) | (static_cast<uint32_t>(J.xB - J.xA - 1) << 11) |
-                   (rbase << 15);
-            ob = J.obase + SG.y0;
+    //   rbase = box offset of the row's first clipped (z, x) at y = by0
+    {
+        int cnt[kMaxSrcRows / kTileThreads];
+#pragma unroll
+        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
+            const int t = kMaxSrcRows / kTileThreads * tid + k;
+            RowJob J;
+            int n = 0;
+            uint32_t s0 = 0, info = 0;
+            if (t < T.n && resolve_row<H>(a, G, T, t, J)) {
+                const uint16_t* ys = J.is_tree ? a.tree.y : a.leaf.y;
+                const int d = J.d;
+                s0 = lower_bound_u16(ys, J.b, J.e, G.ylo >> d);
+                const uint32_t s1 = lower_bound_u16(ys, s0, J.e, (G.yhi + (1 << d) - 1) >> d);
+                n = static_cast<int>(s1 - s0);
+                const uint32_t rbase = static_cast<uint32_t>(J.r00 + G.by0);
+                info = static_cast<uint32_t>(d) | (J.is_tree << 5) | (J.inner << 6) |
+                       (static_cast<uint32_t>(J.zB - J.zA - 1) << 7) | (static_cast<uint32_t>(J.xB - J.xA - 1) << 11) |
+                       (rbase << 15);
+                if (J.inner) orow[J.obase] = s0;
+            }
+            rsrc[t] = s0;
+            rinfo[t] = info;
+            cnt[k] = n;
         }
-        rcur[t] = i;
-        rend[t] = e;
-        rinfo[t] = info;
-        rob[t] = ob;
+        // exclusive scan over rows (thread tid owns rows 4*tid .. 4*tid+3)
+        int sum = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) sum += cnt[k];
+        const int incl = warp_incl_scan(sum, lane);
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int base = incl - sum;
+        for (int w = 0; w < warp; ++w) base += wsum[w];
+#pragma unroll
+        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
+            roff[kMaxSrcRows / kTileThreads * tid + k] = base;
+            base += cnt[k];
+        }
+        if (tid == kTileThreads - 1) roff[kMaxSrcRows] = base;
     }
     __syncthreads();
 
-    const uint32_t col = a.tiles[t0] / static_cast<uint32_t>(tyd);
-    for (int k = 0; k < nt; ++k) {
-        const uint32_t tix = t0 + k;
-        Geo G = SG;  // same column: only the y extent changes
-        G.y0 = static_cast<int>(a.tiles[tix] - col * static_cast<uint32_t>(tyd)) * kTY;
-        G.by0 = G.y0 - kPadY;
-        G.ylo = max(G.y0 - H, 0);
-        G.yhi = min(G.y0 + kTY + H, g.yd);
-        const int meta = a.meta[tix];
-        // ---- init: output map, (holes only) zeroed box
-        {
-            int4* om = reinterpret_cast<int4*>(omap);
-            for (int i = tid; i < kTZ * kTX * kTY / 4; i += kTileThreads) om[i] = make_int4(-1, -1, -1, -1);
+    // ---- fill: one thread per source particle
+    auto put = [&](int p) {
+        const int t = rid[p & (kMaxFlat - 1)];
+        const uint32_t info = rinfo[t];
+        const int d = info & 31;
+        const bool is_tree = (info >> 5) & 1;
+        const int rbase = static_cast<int>(info >> 15);
+        const uint32_t gi = rsrc[t] + static_cast<uint32_t>(p - roff[t]);
+        const int yy = __ldg((is_tree ? a.tree.y : a.leaf.y) + gi);
+        const Acc v = static_cast<Acc>(__ldg((is_tree ? a.tval : a.val) + gi));
+        if (d == 0) {
+            S[rbase - G.by0 + yy] = v;
+            if (((info >> 6) & 1) && static_cast<unsigned>(yy - G.y0) < static_cast<unsigned>(kTY)) {
+                const int row = rbase / B::BY;  // box row = bz * BX + bx
+                const int orid = (row / B::BX - H) * kTX + (row % B::BX - H);
+                omap[orid * kTY + yy - G.y0] = static_cast<uint8_t>(gi - orow[orid]);
+            }
+            return;
         }
-        if (tid == 0) nblk = 0;
-        if (meta & kMetaHoles)
-            for (int i = tid; i < B::NC; i += kTileThreads) S[i] = Acc(0);
-        __syncthreads();
-
-        // ---- fill: each source row is walked from its cursor by one thread, 8
-        // particles per batch (independent loads in flight).  Level-l particles
-        // and leaves one or two levels coarser are written in place; leaves >= 3
-        // levels coarser are queued as regions and filled by the whole CTA.
-        const int ynext = G.y0 + kTY - H;  // a consecutive next tile's first y
-        auto scatter = [&](int t) {
-            int i = rcur[t];
-            const int e = rend[t];
-            if (i >= e) return;
-            const uint32_t info = rinfo[t];
-            const int d = info & 31;
-            const bool is_tree = (info >> 5) & 1, inner = (info >> 6) & 1;
-            const int nzr = ((info >> 7) & 15) + 1, nxr = ((info >> 11) & 15) + 1;
-            const int rbase = static_cast<int>(info >> 15);
-            const int r00 = rbase - G.by0;
-            const uint16_t* ys = is_tree ? a.tree.y : a.leaf.y;
-            const float* vs = is_tree ? a.tval : a.val;
-            while (i < e && ((static_cast<int>(__ldg(ys + i)) + 1) << d) <= G.ylo) ++i;  // gap between tiles
-            int keep = 0;  // processed particles the next tile needs again (a suffix)
-            if (d == 0) {
-                const int obase = rob[t] - G.y0;
-                for (;;) {
-                    int yb[kBatch];
-                    float vb[kBatch];
-#pragma unroll
-                    for (int q = 0; q < kBatch; ++q) {
-                        const bool ok = i + q < e;
-                        yb[q] = ok ? static_cast<int>(__ldg(ys + i + q)) : 0x7fffffff;
-                        vb[q] = ok ? __ldg(vs + i + q) : 0.0f;
-                    }
-                    int used = 0;
-#pragma unroll
-                    for (int q = 0; q < kBatch; ++q) {
-                        const int yy = yb[q];
-                        if (yy < G.yhi) {
-                            ++used;
-                            keep += yy >= ynext;
-                            S[r00 + yy] = static_cast<Acc>(vb[q]);
-                            if (inner && static_cast<unsigned>(yy - G.y0) < static_cast<unsigned>(kTY))
-                                omap[obase + yy] = i + q;
-                        }
-                    }
-                    i += used;
-                    if (used < kBatch) break;
-                }
-            } else {
-                for (;;) {
-                    int yb[kBatch];
-                    float vb[kBatch];
-#pragma unroll
-                    for (int q = 0; q < kBatch; ++q) {
-                        const bool ok = i + q < e;
-                        yb[q] = ok ? static_cast<int>(__ldg(ys + i + q)) : (G.yhi >> d) + 1;  // sentinel past the box
-                        vb[q] = ok ? __ldg(vs + i + q) : 0.0f;
-                    }
-                    int used = 0;
-#pragma unroll
-                    for (int q = 0; q < kBatch; ++q) {
-                        const int yy = yb[q];
-                        if ((yy << d) < G.yhi) {
-                            ++used;
-                            keep += ((yy + 1) << d) > ynext;
-                            const Acc v = static_cast<Acc>(vb[q]);
-                            if (d == 1) {
-                                Acc* p0 = S + r00 + (yy << 1);
-                                VT::st2(p0, v);
-                                if (nxr == 2) VT::st2(p0 + B::BY, v);
-                                if (nzr == 2) {
-                                    VT::st2(p0 + B::BX * B::BY, v);
-                                    if (nxr == 2) VT::st2(p0 + B::BX * B::BY + B::BY, v);
-                                }
-                            } else if (d == 2) {
-                                Acc* p0 = S + r00 + (yy << 2);
-#pragma unroll
-                                for (int z = 0; z < 4; ++z)
-#pragma unroll
-                                    for (int x = 0; x < 4; ++x)
-                                        if (z < nzr && x < nxr) VT::st4(p0 + (z * B::BX + x) * B::BY, v);
-                            } else {
-                                const int c0 = max((yy << d) - G.by0, 0), c1 = min(((yy + 1) << d) - G.by0, B::BY);
-                                const int slot = atomicAdd(&nreg, 1);
-                                if (slot < kMaxRegions) {
-                                    reg[slot] = Region<Acc>{rbase, nzr, nxr, c0 >> 2, (c1 - c0) >> 2, v};
-                                } else {
-                                    for (int z = 0; z < nzr; ++z)
-                                        for (int x = 0; x < nxr; ++x)
-                                            for (int c = c0; c < c1; c += 4)
-                                                VT::st4(S + rbase + (z * B::BX + x) * B::BY + c, v);
-                                }
-                            }
-                        }
-                    }
-                    i += used;
-                    if (used < kBatch) break;
-                }
+        const int nzr = ((info >> 7) & 15) + 1, nxr = ((info >> 11) & 15) + 1;
+        Acc* p0 = S + rbase - G.by0 + (yy << d);
+        if (d == 1) {
+            VT::st2(p0, v);
+            if (nxr == 2) VT::st2(p0 + B::BY, v);
+            if (nzr == 2) {
+                VT::st2(p0 + B::BX * B::BY, v);
+                if (nxr == 2) VT::st2(p0 + B::BX * B::BY + B::BY, v);
             }
-            rcur[t] = i - keep;
-        };
-        // cooperative fill of the queued regions: flattened over their quads
-        auto fill_regions = [&]() {
-            const int n = min(nreg, kMaxRegions);
-            if (n == 0) return;
-            if (warp == 0) {
-                // exclusive prefix of the regions' quad counts (<= 2 regions per lane)
-                int c0 = 0, c1 = 0;
-                if (2 * lane < n) c0 = reg[2 * lane].nz * reg[2 * lane].nx * reg[2 * lane].nq;
-                if (2 * lane + 1 < n) c1 = reg[2 * lane + 1].nz * reg[2 * lane + 1].nx * reg[2 * lane + 1].nq;
-                const int incl = warp_incl_scan(c0 + c1, lane);
-                rpre[2 * lane] = incl - c0 - c1;
-                rpre[2 * lane + 1] = incl - c1;
-                if (lane == 31) rpre[kMaxRegions] = incl;
-            }
-            __syncthreads();
-            const int total = rpre[kMaxRegions];
-            for (int c = tid; c < total; c += kTileThreads) {
-                // region of quad c: binary search over the prefix (<= 64 regions)
-                int lo = 0, hi = n - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (rpre[mid] <= c) lo = mid; else hi = mid - 1;
-                }
-                const Region<Acc> R = reg[lo];
-                const int j = c - rpre[lo];
-                const int row = j / R.nq, qd = j - row * R.nq;
-                const int zz = row / R.nx, xx = row - zz * R.nx;
-                VT::st4(S + R.rbase + (zz * B::BX + xx) * B::BY + 4 * (R.q0 + qd), R.v);
-            }
-            __syncthreads();
-            if (tid == 0) nreg = 0;
-        };
-        if (!(seg_flags & kMetaOverlap)) {
-            for (int t = tid; t < T.n; t += kTileThreads) scatter(t);
-            __syncthreads();
-            fill_regions();
+        } else if (d == 2) {
+#pragma unroll
+            for (int z = 0; z < 4; ++z)
+#pragma unroll
+                for (int x = 0; x < 4; ++x)
+                    if (z < nzr && x < nxr) VT::st4(p0 + (z * B::BX + x) * B::BY, v);
         } else {
-            // reference order: level l, l-1, ..., l-D, then interior nodes (last writer wins)
-            for (int p = 0; p <= T.D + 1; ++p) {
-                const int q0 = T.base[p];
-                const int q1 = p <= T.D ? T.base[p + 1] : T.n;
-                for (int t = q0 + tid; t < q1; t += kTileThreads) scatter(t);
-                __syncthreads();
-                fill_regions();
-                __syncthreads();
+            const int c0 = max((yy << d) - G.by0, 0), c1 = min(((yy + 1) << d) - G.by0, B::BY);
+            const int slot = atomicAdd(&nreg, 1);
+            if (slot < kMaxRegions) {
+                reg[slot] = Region<Acc>{rbase, nzr, nxr, c0 >> 2, (c1 - c0) >> 2, v};
+            } else {
+                for (int z = 0; z < nzr; ++z)
+                    for (int x = 0; x < nxr; ++x)
+                        for (int c = c0; c < c1; c += 4) VT::st4(S + rbase + (z * B::BX + x) * B::BY + c, v);
             }
         }
+    };
+    // cooperative fill of the queued regions (leaves >= 3 levels coarser)
+    auto fill_regions = [&]() {
         __syncthreads();
-
-        // ---- pad: out-of-domain box cells within H of the domain
-        if (G.z0 - H < 0 || G.x0 - H < 0 || G.y0 - H < 0 || G.z0 + kTZ + H > g.zd || G.x0 + kTX + H > g.xd ||
-            G.y0 + kTY + H > g.yd) {
-            for (int c = tid; c < B::NC; c += kTileThreads) {
-                const int bz = c / (B::BX * B::BY);
-                const int rem = c - bz * (B::BX * B::BY);
-                const int bx = rem / B::BY, by = rem - bx * B::BY;
-                const int zz = G.bz0 + bz, xx = G.bx0 + bx, yy = G.by0 + by;
-                if (yy < G.y0 - H || yy >= G.y0 + kTY + H) continue;  // pad columns: read by no output
-                if (zz >= 0 && zz < g.zd && xx >= 0 && xx < g.xd && yy >= 0 && yy < g.yd) continue;
-                if (zz >= g.zd + H || xx >= g.xd + H || yy >= g.yd + H) continue;  // read by no output
-                if (a.pad == APRGPU_PAD_ZERO) {
-                    S[c] = Acc(0);
-                } else {
-                    const int rz = reflect_dev(zz, g.zd) - G.bz0, rx = reflect_dev(xx, g.xd) - G.bx0,
-                              ry = reflect_dev(yy, g.yd) - G.by0;
-                    S[c] = S[(rz * B::BX + rx) * B::BY + ry];
-                }
+        const int n = min(nreg, kMaxRegions);
+        if (n == 0) return;
+        if (warp == 0) {
+            int c0 = 0, c1 = 0;
+            if (2 * lane < n) c0 = reg[2 * lane].nz * reg[2 * lane].nx * reg[2 * lane].nq;
+            if (2 * lane + 1 < n) c1 = reg[2 * lane + 1].nz * reg[2 * lane + 1].nx * reg[2 * lane + 1].nq;
+            const int incl = warp_incl_scan(c0 + c1, lane);
+            rpre[2 * lane] = incl - c0 - c1;
+            rpre[2 * lane + 1] = incl - c1;
+            if (lane == 31) rpre[kMaxRegions] = incl;
+        }
+        __syncthreads();
+        const int total = rpre[kMaxRegions];
+        for (int c = tid; c < total; c += kTileThreads) {
+            int lo = 0, hi = n - 1;  // region of quad c
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (rpre[mid] <= c) lo = mid; else hi = mid - 1;
+            }
+            const Region<Acc> R = reg[lo];
+            const int j = c - rpre[lo];
+            const int row = j / R.nq, qd = j - row * R.nq;
+            const int zz = row / R.nx, xx = row - zz * R.nx;
+            VT::st4(S + R.rbase + (zz * B::BX + xx) * B::BY + 4 * (R.q0 + qd), R.v);
+        }
+        __syncthreads();
+        if (tid == 0) nreg = 0;
+    };
+    // particles [q0, q1) of the flattened numbering, in chunks of kMaxFlat
+    auto scatter_range = [&](int r0, int r1) {
+        const int q0 = roff[r0], q1 = roff[r1];
+        for (int c0 = q0; c0 < q1; c0 += kMaxFlat) {
+            const int c1 = min(c0 + kMaxFlat, q1);
+            for (int t = r0 + tid; t < r1; t += kTileThreads) {
+                const int lo = max(roff[t], c0), hi = min(roff[t + 1], c1);
+                for (int q = lo; q < hi; ++q) rid[q & (kMaxFlat - 1)] = static_cast<uint16_t>(t);
             }
             __syncthreads();
+            for (int q = c0 + tid; q < c1; q += kTileThreads) put(q);
+            __syncthreads();
         }
+    };
+    if (!(meta & kMetaOverlap)) {
+        scatter_range(0, T.n);
+        fill_regions();
+    } else {
+        // reference order: level l, l-1, ..., l-D, then interior nodes (last writer wins)
+        for (int ph = 0; ph <= T.D + 1; ++ph) {
+            scatter_range(T.base[ph], ph <= T.D ? T.base[ph + 1] : T.n);
+            fill_regions();
+        }
+    }
+    __syncthreads();
 
-        // ---- compact the 2x2x2 blocks that hold output particles
-        {
-            const int qz = tid >> 5, qx = (tid >> 3) & 3, qy = tid & 7;
-            const int* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
-            const int2 m0 = *reinterpret_cast<const int2*>(o);
-            const int2 m1 = *reinterpret_cast<const int2*>(o + kTY);
-            const int2 m2 = *reinterpret_cast<const int2*>(o + kTX * kTY);
-            const int2 m3 = *reinterpret_cast<const int2*>(o + kTX * kTY + kTY);
-            const int mx = max(max(max(m0.x, m0.y), max(m1.x, m1.y)), max(max(m2.x, m2.y), max(m3.x, m3.y)));
-            if (mx >= 0) blist[atomicAdd(&nblk, 1)] = static_cast<uint8_t>(tid);
+    // ---- pad: out-of-domain box cells within H of the domain
+    if (G.z0 - H < 0 || G.x0 - H < 0 || G.y0 - H < 0 || G.z0 + kTZ + H > g.zd || G.x0 + kTX + H > g.xd ||
+        G.y0 + kTY + H > g.yd) {
+        for (int r = tid; r < B::NR; r += kTileThreads) {
+            const int bz = r / B::BX, bx = r - bz * B::BX;
+            const int zz = G.bz0 + bz, xx = G.bx0 + bx;
+            if (zz >= g.zd + H || xx >= g.xd + H) continue;  // read by no output
+            const bool row_out = zz < 0 || zz >= g.zd || xx < 0 || xx >= g.xd;
+            const int rz = reflect_dev(zz, g.zd) - G.bz0, rx = reflect_dev(xx, g.xd) - G.bx0;
+            Acc* dst = S + r * B::BY - G.by0;
+            const Acc* src = S + (rz * B::BX + rx) * B::BY - G.by0;
+            for (int yy = G.y0 - H; yy < min(G.y0 + kTY + H, g.yd + H); ++yy) {
+                const bool out = row_out || yy < 0 || yy >= g.yd;
+                if (!out) continue;
+                dst[yy] = a.pad == APRGPU_PAD_ZERO ? Acc(0) : src[reflect_dev(yy, g.yd)];
+            }
         }
         __syncthreads();
+    }
 
-        // ---- apply: one thread per active block, 8 outputs
-        // neighbourhood y window of block qy: box index 2qy + kPadY - H .. +N,
-        // loaded as aligned pairs from the even index at or below it
-        constexpr int Y0 = kPadY - H;
-        constexpr int YA = Y0 & ~1, SH = Y0 - YA, NP = (SH + N + 1) / 2;
-        const int nb = nblk;
-        for (int q = tid; q < nb; q += kTileThreads) {
-            const int bidx = blist[q];
-            const int qz = bidx >> 5, qx = (bidx >> 3) & 3, qy = bidx & 7;
-            const Acc* base = S + ((2 * qz) * B::BX + 2 * qx) * B::BY + 2 * qy + YA;
-            Acc acc[8];
-            if constexpr (sizeof(Acc) == 4) {
-                // FAST: the two y-outputs of a block share every tap's weight ->
-                // packed fp32x2 FMA (same per-element rounding as two FFMAs)
-                float2 acc2[4];
+    // ---- compact the 2x2x2 blocks that hold output particles
+    for (int b = tid; b < kBlocks; b += kTileThreads) {
+        const int qz = b / (kBlocks / 4), qx = (b / (kTY / 2)) & 3, qy = b & (kTY / 2 - 1);
+        const uint8_t* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
+        const unsigned m = *reinterpret_cast<const uint16_t*>(o) & *reinterpret_cast<const uint16_t*>(o + kTY) &
+                           *reinterpret_cast<const uint16_t*>(o + kTX * kTY) &
+                           *reinterpret_cast<const uint16_t*>(o + kTX * kTY + kTY);
+        if (m != 0xffffu) blist[atomicAdd(&nblk, 1)] = static_cast<uint16_t>(b);
+    }
+    __syncthreads();
+
+    // ---- apply: one thread per active block, 8 outputs
+    // neighbourhood y window of block qy: box index 2qy + kPadY - H .. +N,
+    // loaded as aligned pairs from the even index at or below it
+    constexpr int Y0 = kPadY - H;
+    constexpr int YA = Y0 & ~1, SH = Y0 - YA, NP = (SH + N + 1) / 2;
+    const int nb = nblk;
+    for (int q = tid; q < nb; q += kTileThreads) {
+        const int bidx = blist[q];
+        const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
+        const Acc* base = S + ((2 * qz) * B::BX + 2 * qx) * B::BY + 2 * qy + YA;
+        Acc acc[8];
+        if constexpr (sizeof(Acc) == 4) {
+            // FAST: the block's two y-outputs share every tap's weight -> packed
+            // fp32x2 FMA (same per-element rounding as two FFMAs)
+            float2 acc2[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.0f, 0.0f);
+            for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.0f, 0.0f);
 #pragma unroll
-                for (int nz = N - 1; nz >= 0; --nz) {
-                    float v[N][N];
+            for (int nz = N - 1; nz >= 0; --nz) {
+                float v[N][N];
 #pragma unroll
-                    for (int nx = 0; nx < N; ++nx) {
-                        float r[2 * NP];
+                for (int nx = 0; nx < N; ++nx) {
+                    float r[2 * NP];
 #pragma unroll
-                        for (int p = 0; p < NP; ++p) {
-                            const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * B::BX + nx) * B::BY + 2 * p);
-                            r[2 * p] = t2.x;
-                            r[2 * p + 1] = t2.y;
-                        }
-#pragma unroll
-                        for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
+                    for (int pp = 0; pp < NP; ++pp) {
+                        const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * B::BX + nx) * B::BY + 2 * pp);
+                        r[2 * pp] = t2.x;
+                        r[2 * pp + 1] = t2.y;
                     }
 #pragma unroll
-                    for (int oz = 0; oz < 2; ++oz) {
-                        const int az = oz + 2 * H - nz;
-                        if (az < 0 || az > 2 * H) continue;
-#pragma unroll
-                        for (int ox = 0; ox < 2; ++ox)
-#pragma unroll
-                            for (int ax = 0; ax < K; ++ax)
-#pragma unroll
-                                for (int ay = 0; ay < K; ++ay) {
-                                    const float w = W[(az * K + ax) * K + ay];
-                                    const int vx = ox + 2 * H - ax, vy = 2 * H - ay;
-                                    acc2[oz * 2 + ox] = ffma2(make_float2(w, w), make_float2(v[vx][vy], v[vx][vy + 1]),
-                                                              acc2[oz * 2 + ox]);
-                                }
-                    }
+                    for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
                 }
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    acc[2 * i] = acc2[i].x;
-                    acc[2 * i + 1] = acc2[i].y;
+                for (int oz = 0; oz < 2; ++oz) {
+                    const int az = oz + 2 * H - nz;
+                    if (az < 0 || az > 2 * H) continue;
+#pragma unroll
+                    for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+                        for (int ax = 0; ax < K; ++ax)
+#pragma unroll
+                            for (int ay = 0; ay < K; ++ay) {
+                                const float w = W[(az * K + ax) * K + ay];
+                                const int vx = ox + 2 * H - ax, vy = 2 * H - ay;
+                                acc2[oz * 2 + ox] =
+                                    ffma2(make_float2(w, w), make_float2(v[vx][vy], v[vx][vy + 1]), acc2[oz * 2 + ox]);
+                            }
                 }
-            } else {
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[2 * i] = acc2[i].x;
+                acc[2 * i + 1] = acc2[i].y;
+            }
+        } else {
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = Acc(0);
 #pragma unroll
@@ -682,10 +626,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                 for (int nx = 0; nx < N; ++nx) {
                     Acc r[2 * NP];
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        const V2 t2 = *reinterpret_cast<const V2*>(base + (nz * B::BX + nx) * B::BY + 2 * p);
-                        r[2 * p] = t2.x;
-                        r[2 * p + 1] = t2.y;
+                    for (int pp = 0; pp < NP; ++pp) {
+                        const V2 t2 = *reinterpret_cast<const V2*>(base + (nz * B::BX + nx) * B::BY + 2 * pp);
+                        r[2 * pp] = t2.x;
+                        r[2 * pp + 1] = t2.y;
                     }
 #pragma unroll
                     for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
@@ -704,35 +648,34 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                             for (int ax = 0; ax < K; ++ax)
 #pragma unroll
                                 for (int ay = 0; ay < K; ++ay)
-                                    acc[(oz * 2 + ox) * 2 + oy] = fma_t<Acc>(
-                                        W[(az * K + ax) * K + ay], v[ox + 2 * H - ax][oy + 2 * H - ay],
-                                        acc[(oz * 2 + ox) * 2 + oy]);
+                                    acc[(oz * 2 + ox) * 2 + oy] =
+                                        fma_t<Acc>(W[(az * K + ax) * K + ay], v[ox + 2 * H - ax][oy + 2 * H - ay],
+                                                   acc[(oz * 2 + ox) * 2 + oy]);
                 }
             }
-            }
-            const int* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
-#pragma unroll
-            for (int oz = 0; oz < 2; ++oz)
-#pragma unroll
-                for (int ox = 0; ox < 2; ++ox)
-#pragma unroll
-                    for (int oy = 0; oy < 2; ++oy) {
-                        const int i = o[(oz * kTX + ox) * kTY + oy];
-                        if (i < 0) continue;
-                        const float r = to_f(acc[(oz * 2 + ox) * 2 + oy]);
-                        if (a.epi.mode == EPI_STORE) {
-                            a.out[i] = r;
-                        } else if (a.epi.mode == EPI_RL_RATIO) {
-                            // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
-                            const double bd = static_cast<double>(r);
-                            const double den = bd < a.epi.eps ? a.epi.eps : bd;
-                            a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
-                        } else {
-                            a.epi.est[i] = __fmul_rn(a.epi.est[i], r);  // deconv.hpp:102
-                        }
-                    }
         }
-        __syncthreads();  // S / omap / blist are rebuilt by the next tile
+        const uint8_t* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
+#pragma unroll
+        for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+            for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+                for (int oy = 0; oy < 2; ++oy) {
+                    const int off = o[(oz * kTX + ox) * kTY + oy];
+                    if (off == 0xff) continue;
+                    const uint32_t i = orow[(2 * qz + oz) * kTX + 2 * qx + ox] + off;
+                    const float r = to_f(acc[(oz * 2 + ox) * 2 + oy]);
+                    if (a.epi.mode == EPI_STORE) {
+                        a.out[i] = r;
+                    } else if (a.epi.mode == EPI_RL_RATIO) {
+                        // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
+                        const double bd = static_cast<double>(r);
+                        const double den = bd < a.epi.eps ? a.epi.eps : bd;
+                        a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
+                    } else {
+                        a.epi.est[i] = __fmul_rn(a.epi.est[i], r);  // deconv.hpp:102
+                    }
+                }
     }
 }
 
@@ -772,8 +715,7 @@ void set_level(TileLaunch& a, const DevAccess& L, int l, uint32_t end) {
     a.seg_end[s] = end;
 }
 
-// First use of an APR by the tile path: probe every tile, then cut each
-// level's tile columns into segments whose staged rows should fit.
+// First use of an APR by the tile path: probe every tile once.
 void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
     DevAccess& L = apr->leaf;
     if (L.tile_meta || !L.tiles) return;
@@ -782,8 +724,6 @@ void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
     const uint64_t n = L.tile_off[L.l_max + 1];
     uint8_t* meta = nullptr;
     APR_CUDA(cudaMalloc(&meta, n + 16));
-    GpuBuf counts;
-    counts.ensure(2 * n + 16);
     TileLaunch a = base_launch(apr);
     uint32_t total = 0;
     for (int l = L.l_min; l <= L.l_max; ++l) {
@@ -792,50 +732,27 @@ void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
         total += c;
         set_level(a, L, l, total);
     }
-    std::vector<uint32_t> segs;
-    L.seg_off.assign(L.l_max + 2, 0);
     if (total) {
         a.tiles = L.tiles;
         a.tile_base = static_cast<uint32_t>(L.tile_off[L.l_min]);
         a.meta = meta;
-        a.count = counts.as<uint16_t>();
         k_tile_probe<<<total, kTileThreads, 0, s>>>(a);
         count_launch(apr->ctx);
         APR_CUDA(cudaGetLastError());
-        std::vector<uint32_t> ids(n);
-        std::vector<uint16_t> cnt(n);
-        APR_CUDA(cudaMemcpyAsync(ids.data(), L.tiles, 4 * n, cudaMemcpyDeviceToHost, s));
-        APR_CUDA(cudaMemcpyAsync(cnt.data(), counts.p, 2 * n, cudaMemcpyDeviceToHost, s));
         APR_CUDA(cudaStreamSynchronize(s));
-        for (int l = L.l_min; l <= L.l_max; ++l) {
-            L.seg_off[l] = segs.size();
-            const uint64_t b = L.tile_off[l], e = L.tile_off[l + 1];
-            const uint32_t tyd = static_cast<uint32_t>(L.tile_dims[3 * l + 2]);
-            uint64_t i = b;
-            while (i < e) {
-                const uint32_t col = ids[i] / tyd;
-                uint64_t j = i + 1;
-                uint32_t est = cnt[i];
-                while (j < e && j - i < static_cast<uint64_t>(kSegTiles) && ids[j] / tyd == col &&
-                       est + cnt[j] <= static_cast<uint32_t>(kStageCap))
-                    est += cnt[j++];
-                if (i >= (1ull << 28)) fail(APRGPU_ERR_CAPABILITY, "too many tiles for the segment encoding");
-                segs.push_back(static_cast<uint32_t>(i << 4) | static_cast<uint32_t>(j - i - 1));
-                i = j;
-            }
-        }
-        L.seg_off[L.l_max + 1] = segs.size();
-        for (int l = 0; l < L.l_min; ++l) L.seg_off[l] = 0;
     }
-    APR_CUDA(cudaMalloc(&L.segs, 4 * segs.size() + 4));
-    if (!segs.empty())
-        APR_CUDA(cudaMemcpy(L.segs, segs.data(), 4 * segs.size(), cudaMemcpyHostToDevice));
     L.tile_meta = meta;
 }
 
 template <typename Acc, int H>
-void launch_segs(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
-    k_conv_seg<Acc, H><<<n, kTileThreads, 0, s>>>(a);
+void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
+    constexpr int bytes = Box<H>::NC * static_cast<int>(sizeof(Acc));
+    static const bool attr = [] {
+        APR_CUDA(cudaFuncSetAttribute(k_conv_tile<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        return true;
+    }();
+    (void)attr;
+    k_conv_tile<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
     count_launch(ctx);
     APR_CUDA(cudaGetLastError());
 }
@@ -897,9 +814,9 @@ void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a) {
                                 cudaMemcpyHostToDevice));
 }
 
-// Runs every level whose stencil is an isotropic 3^3 or 5^3 through the
-// segment kernel (one launch per extent and run of consecutive levels, coarse
-// levels first); sets done[l] for them.
+// Runs every level whose stencil is an isotropic 3^3 or 5^3 through the tile
+// kernel (one launch per extent and run of consecutive levels, coarse levels
+// first); sets done[l] for them.
 void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* values, const float* tree_values,
                       int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s, bool* done) {
     const DevAccess& L = apr->leaf;
@@ -937,7 +854,7 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
             uint32_t total = 0;
             for (; l <= L.l_max && ok(l); ++l) {
                 done[l] = true;
-                const uint32_t c = static_cast<uint32_t>(L.seg_off[l + 1] - L.seg_off[l]);
+                const uint32_t c = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
                 if (!c) continue;
                 total += c;
                 b.woff[b.n_levels] = pyr->off[l - pyr->l_min];
@@ -948,11 +865,11 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
                 }
             }
             if (!total) continue;
-            b.segs = L.segs + L.seg_off[first];
+            b.tile_base = static_cast<uint32_t>(L.tile_off[first]);
             if (H == 1) {
-                if (exact) launch_segs<double, 1>(apr->ctx, b, total, s); else launch_segs<float, 1>(apr->ctx, b, total, s);
+                if (exact) launch_tiles<double, 1>(apr->ctx, b, total, s); else launch_tiles<float, 1>(apr->ctx, b, total, s);
             } else {
-                if (exact) launch_segs<double, 2>(apr->ctx, b, total, s); else launch_segs<float, 2>(apr->ctx, b, total, s);
+                if (exact) launch_tiles<double, 2>(apr->ctx, b, total, s); else launch_tiles<float, 2>(apr->ctx, b, total, s);
             }
         }
     }

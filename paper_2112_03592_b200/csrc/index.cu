@@ -38,9 +38,7 @@ void DevAccess::release() {
     cudaFree(work);
     cudaFree(tiles);
     cudaFree(tile_meta);
-    cudaFree(segs);
     tile_meta = nullptr;
-    segs = nullptr;
     y = nullptr;
     rb = nullptr;
     work = nullptr;

@@ -65,8 +65,6 @@ struct DevAccess {
     std::vector<uint64_t> tile_off;        // l_max+2 offsets into tiles
     std::vector<int> tile_dims;            // 3 per level: tile grid (z, x, y)
     uint8_t* tile_meta = nullptr;          // device, one byte per tile (coarse depth, fill flags); lazy
-    uint32_t* segs = nullptr;              // device, tile-column segments (first tile << 4 | count - 1); lazy
-    std::vector<uint64_t> seg_off;         // l_max+2 offsets into segs
     AccessView view() const;
     void release();
 };
