@@ -31,6 +31,46 @@ __device__ __forceinline__ uint32_t lower_bound_u16(const uint16_t* __restrict__
     return b;
 }
 
+// Both lower bounds (of k0 <= k1) in the sorted y[b, e) with 8-ary rounds:
+// each round issues up to 7 independent loads per key and shrinks the
+// interval 8x, so a row of n particles costs ~log8(n) + 1 dependent load
+// latencies instead of log2(n) (the tile kernels are latency-bound here).
+__device__ __forceinline__ void lower_bound2_kary(const uint16_t* __restrict__ y, uint32_t b, uint32_t e, int k0,
+                                                  int k1, uint32_t& s0, uint32_t& s1) {
+    uint32_t l0 = b, r0 = e, l1 = b, r1 = e;
+    while (r0 - l0 > 8 || r1 - l1 > 8) {
+        const uint32_t st0 = (r0 - l0 + 7) >> 3, st1 = (r1 - l1 + 7) >> 3;
+        const bool a0 = r0 - l0 > 8, a1 = r1 - l1 > 8;
+        int j0 = 0, j1 = 0;
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+            const uint32_t p0 = l0 + k * st0, p1 = l1 + k * st1;
+            const int v0 = (a0 && p0 < r0) ? static_cast<int>(__ldg(y + p0)) : 0x10000;
+            const int v1 = (a1 && p1 < r1) ? static_cast<int>(__ldg(y + p1)) : 0x10000;
+            j0 += v0 < k0;
+            j1 += v1 < k1;
+        }
+        if (a0) {
+            const uint32_t nl = j0 ? l0 + j0 * st0 + 1 : l0;
+            r0 = min(l0 + (j0 + 1) * st0, r0);
+            l0 = nl;
+        }
+        if (a1) {
+            const uint32_t nl = j1 ? l1 + j1 * st1 + 1 : l1;
+            r1 = min(l1 + (j1 + 1) * st1, r1);
+            l1 = nl;
+        }
+    }
+    uint32_t c0 = 0, c1 = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        c0 += (l0 + k < r0 && static_cast<int>(__ldg(y + l0 + k)) < k0);
+        c1 += (l1 + k < r1 && static_cast<int>(__ldg(y + l1 + k)) < k1);
+    }
+    s0 = l0 + c0;
+    s1 = l1 + c1;
+}
+
 __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);

@@ -387,18 +387,19 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     //   rinfo = d | is_tree << 5 | inner << 6 | (nz-1) << 7 | (nx-1) << 11 | rbase << 15
     //   rbase = box offset of the row's first clipped (z, x) at y = by0
     {
-        int cnt[kMaxSrcRows / kTileThreads];
+        // rows are interleaved over the threads (the level-l rows come first
+        // and would otherwise all land in one warp); counts go through roff
 #pragma unroll
         for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
-            const int t = kMaxSrcRows / kTileThreads * tid + k;
+            const int t = tid + k * kTileThreads;
             RowJob J;
             int n = 0;
             uint32_t s0 = 0, info = 0;
             if (t < T.n && resolve_row<H>(a, G, T, t, J)) {
                 const uint16_t* ys = J.is_tree ? a.tree.y : a.leaf.y;
                 const int d = J.d;
-                s0 = lower_bound_u16(ys, J.b, J.e, G.ylo >> d);
-                const uint32_t s1 = lower_bound_u16(ys, s0, J.e, (G.yhi + (1 << d) - 1) >> d);
+                uint32_t s1;
+                lower_bound2_kary(ys, J.b, J.e, G.ylo >> d, (G.yhi + (1 << d) - 1) >> d, s0, s1);
                 n = static_cast<int>(s1 - s0);
                 const uint32_t rbase = static_cast<uint32_t>(J.r00 + G.by0);
                 info = static_cast<uint32_t>(d) | (J.is_tree << 5) | (J.inner << 6) |
@@ -408,9 +409,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
             }
             rsrc[t] = s0;
             rinfo[t] = info;
-            cnt[k] = n;
+            roff[t] = n;
         }
+        __syncthreads();
         // exclusive scan over rows (thread tid owns rows 4*tid .. 4*tid+3)
+        int cnt[kMaxSrcRows / kTileThreads];
+#pragma unroll
+        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) cnt[k] = roff[kMaxSrcRows / kTileThreads * tid + k];
+        __syncthreads();
         int sum = 0;
 #pragma unroll
         for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) sum += cnt[k];
