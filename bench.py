@@ -100,6 +100,23 @@ def workload(cfg: str):
     raise SystemExit(f"unknown config {cfg}")
 
 
+def ncu_traffic(config: str, stencil: int, accum: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one conv pass, from the
+    committed ncu capture of this workload (profiles/<round>/traffic.json,
+    written by tools/traffic.py from tools/gpu_round.sh's ncu pass), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)
+            v = t.get(f"{config}_k{stencil}_{accum}")
+            if v is not None:
+                return int(v), os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def algorithmic_bytes(apr) -> int:
     """Per conv pass: y_idx u16 + value in f32 + out f32 per particle, y_idx u16 +
     value f32 per interior node, one u32 row begin per row (device layout)."""
@@ -203,6 +220,7 @@ def run_ours(args, rank, world):
     B = algorithmic_bytes(apr)
     peak, peak_kind = peaks()
     achieved = B / tc / 1e9
+    traffic, traffic_src = ncu_traffic(args.config, k, args.accum)
     res = {
         "metric": METRIC,
         "value": round(world * 4 * n_pix / tc / 1e9, 3),
@@ -225,9 +243,11 @@ def run_ours(args, rank, world):
         "paper_protocol": {"ms_per_step": round(tp * 1e3, 4), "gbps_pixel_equiv": round(4 * n_pix / tp / 1e9, 3),
                            "includes": "fill_tree + convolve_apr (row index prebuilt at upload)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
-                     "note": f"algorithmic bytes {B} per pass (10/particle + 6/node + 4/row) / conv-pass time; "
-                             f"peak {peak_kind}"},
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "note": f"algorithmic bytes {B} per pass (10/particle + 6/node + 4/row) / conv-pass time "
+                             f"(CUDA events on the launching stream); peak {peak_kind} (MEASURED_PEAKS.json hbm_gbs); "
+                             f"traffic = ncu dram bytes of one cold conv pass"
+                             + (f" ({traffic_src})" if traffic_src else " (no committed capture)")},
         "e2e": {"value": round(world * 4 * n_pix / te / 1e9, 3), "unit": "GB/s (pixel-equivalent)",
                 "ms_per_step": round(te * 1e3, 4),
                 "h2d_bytes_per_step": int(4 * n_p + 4 * dapr.n_tree), "d2h_bytes_per_step": int(4 * n_p)},
@@ -333,7 +353,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c3"))
     ap.add_argument("--stencil", type=int, default=3)
-    ap.add_argument("--accum", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--accum", default="fast", choices=["exact", "fast"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -58,7 +58,7 @@ constexpr int kTZ = 8, kTX = 8, kTY = APRGPU_TILE_Y, kTileThreads = 128;
 constexpr int kBlocks = (kTZ / 2) * (kTX / 2) * (kTY / 2);  // 2x2x2 output blocks per tile
 constexpr int kProbeH = 2;
 constexpr int kMaxSrcRows = 512;   // >= 2*(8+2*2)^2 + coarse rows of a 5^3 box
-constexpr int kMaxFlat = 4096;     // source particles per flattened chunk
+constexpr int kMaxFlat = 2048;     // source particles per flattened chunk
 constexpr int kPadY = 4;           // box y origin = y0 - kPadY (>= H, multiple of 4)
 enum : uint8_t { kMetaDepth = 0x1f, kMetaOverlap = 0x20, kMetaHoles = 0x40 };
 
