@@ -43,6 +43,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -70,6 +71,8 @@ struct TileLaunch {
     const float* tval;
     const uint32_t* tiles;   // tile ids of all levels (absolute indexing)
     const uint8_t* meta;     // one byte per tile
+    const uint2* runs;       // per-tile source runs (see k_tile_runs)
+    const uint32_t* run_off; // n_tiles + 1
     uint32_t tile_base;      // first tile of the launch (blocks map to consecutive tiles)
     int n_levels;                   // level segments in this launch
     int lvl[kMaxLevels];            // level of each segment
@@ -289,6 +292,93 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_consta
     }
 }
 
+// --------------------------------------------------------------- tile runs --
+// Once per APR and stencil half-width: for every tile, the non-empty source
+// rows of its box and their particle ranges inside the box's y-extent --
+// {first particle, row slot | count << 16}, in row-slot (= reference fill)
+// order.  This is the structure-only part of the convolution's row phase
+// (row lookups + dependent searches), hoisted out of every call.
+template <int H>
+__global__ void __launch_bounds__(kTileThreads) k_tile_runs(const __grid_constant__ TileLaunch a, int mode,
+                                                           uint32_t* __restrict__ counts, uint2* __restrict__ runs) {
+    __shared__ SrcTable T;
+    __shared__ int cnt[kMaxSrcRows];
+    __shared__ int wsum[kTileThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
+    const int l = a.lvl[s];
+    const uint32_t tix = a.tile_base + blockIdx.x;
+    const Geo G = make_geo<H>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], a.leaf.g[l]);
+    const int tree = (l >= a.tree_lmin && l <= a.tree_lmax) ? 1 : 0;
+    if (tid == 0) make_src_table<H>(G, a.meta[tix] & kMetaDepth, tree, T);
+    __syncthreads();
+    uint32_t s0v[kMaxSrcRows / kTileThreads];
+#pragma unroll
+    for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
+        const int t = tid + k * kTileThreads;
+        RowJob J;
+        int n = 0;
+        uint32_t s0 = 0;
+        if (t < T.n && resolve_row<H>(a, G, T, t, J)) {
+            const uint16_t* ys = J.is_tree ? a.tree.y : a.leaf.y;
+            uint32_t s1;
+            lower_bound2_kary(ys, J.b, J.e, G.ylo >> J.d, (G.yhi + (1 << J.d) - 1) >> J.d, s0, s1);
+            n = static_cast<int>(s1 - s0);
+        }
+        s0v[k] = s0;
+        // mode 0: non-empty flag; mode 1: flag in bit 0, count above it
+        cnt[t] = mode == 0 ? (n > 0) : (n > 0 ? (n << 1) | 1 : 0);
+    }
+    __syncthreads();
+    if (mode == 0) {
+        int c = 0;
+        for (int t = tid; t < kMaxSrcRows; t += kTileThreads) c += cnt[t];
+        c = warp_sum(c);
+        if (lane == 0) wsum[warp] = c;
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < kTileThreads / 32; ++w) tot += wsum[w];
+            counts[blockIdx.x] = static_cast<uint32_t>(tot);
+        }
+        return;
+    }
+    // mode 1: ordered compaction (rows 4*tid .. 4*tid+3 per thread for the scan)
+    int f[4], fsum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        f[k] = cnt[4 * tid + k] & 1;
+        fsum += f[k];
+    }
+    const int incl = warp_incl_scan(fsum, lane);
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int base = incl - fsum;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+    int pos[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        pos[k] = base;
+        base += f[k];
+    }
+    __syncthreads();
+    // publish positions through cnt (flag bit 0 | n << 1 stays in the high bits)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (f[k]) cnt[4 * tid + k] = (cnt[4 * tid + k] >> 1) | (pos[k] << 16);
+    __syncthreads();
+    const uint32_t o = a.run_off[tix];
+#pragma unroll
+    for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
+        const int t = tid + k * kTileThreads;
+        if (t >= T.n) continue;
+        const int c = cnt[t];
+        const int n = c & 0xffff;
+        if (!n) continue;
+        runs[o + (c >> 16)] = make_uint2(s0v[k], static_cast<uint32_t>(t) | (static_cast<uint32_t>(n) << 16));
+    }
+}
+
 // ------------------------------------------------------------ convolution --
 template <typename Acc>
 __device__ __forceinline__ Acc fma_t(Acc w, Acc u, Acc acc);
@@ -354,6 +444,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     __shared__ SrcTable T;
     __shared__ uint32_t rinfo[kMaxSrcRows];  // packed row geometry
     __shared__ uint32_t rsrc[kMaxSrcRows];   // global index of the row's first particle in the box
+    __shared__ uint16_t rslot[kMaxSrcRows];  // run -> source-row slot
     __shared__ int roff[kMaxSrcRows + 1];    // flattened offsets; roff[kMaxSrcRows] = total
     __shared__ int wsum[kTileThreads / 32];
     __shared__ uint16_t rid[kMaxFlat];       // row of each flattened particle (current chunk)
@@ -383,36 +474,35 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     }
     __syncthreads();
 
-    // ---- rows: range inside the box and packed geometry, one thread per row
+    // ---- rows: the tile's precomputed non-empty source runs (k_tile_runs) and
+    // their packed box geometry, one thread per run:
     //   rinfo = d | is_tree << 5 | inner << 6 | (nz-1) << 7 | (nx-1) << 11 | rbase << 15
     //   rbase = box offset of the row's first clipped (z, x) at y = by0
+    const uint32_t run0 = a.run_off[tix];
+    const int nruns = min(static_cast<int>(a.run_off[tix + 1] - run0), kMaxSrcRows);
     {
-        // rows are interleaved over the threads (the level-l rows come first
-        // and would otherwise all land in one warp); counts go through roff
 #pragma unroll
         for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
-            const int t = tid + k * kTileThreads;
-            RowJob J;
+            const int j = tid + k * kTileThreads;
             int n = 0;
-            uint32_t s0 = 0, info = 0;
-            if (t < T.n && resolve_row<H>(a, G, T, t, J)) {
-                const uint16_t* ys = J.is_tree ? a.tree.y : a.leaf.y;
-                const int d = J.d;
-                uint32_t s1;
-                lower_bound2_kary(ys, J.b, J.e, G.ylo >> d, (G.yhi + (1 << d) - 1) >> d, s0, s1);
-                n = static_cast<int>(s1 - s0);
+            if (j < nruns) {
+                const uint2 e = __ldg(a.runs + run0 + j);
+                const int t = static_cast<int>(e.y & 0xffff);
+                n = static_cast<int>(e.y >> 16);
+                RowJob J;
+                resolve_row<H, false>(a, G, T, t, J);  // geometry only
                 const uint32_t rbase = static_cast<uint32_t>(J.r00 + G.by0);
-                info = static_cast<uint32_t>(d) | (J.is_tree << 5) | (J.inner << 6) |
-                       (static_cast<uint32_t>(J.zB - J.zA - 1) << 7) | (static_cast<uint32_t>(J.xB - J.xA - 1) << 11) |
-                       (rbase << 15);
-                if (J.inner) orow[J.obase] = s0;
+                rinfo[j] = static_cast<uint32_t>(J.d) | (J.is_tree << 5) | (J.inner << 6) |
+                           (static_cast<uint32_t>(J.zB - J.zA - 1) << 7) |
+                           (static_cast<uint32_t>(J.xB - J.xA - 1) << 11) | (rbase << 15);
+                rsrc[j] = e.x;
+                rslot[j] = static_cast<uint16_t>(t);
+                if (J.inner) orow[J.obase] = e.x;
             }
-            rsrc[t] = s0;
-            rinfo[t] = info;
-            roff[t] = n;
+            roff[j] = n;
         }
         __syncthreads();
-        // exclusive scan over rows (thread tid owns rows 4*tid .. 4*tid+3)
+        // exclusive scan over runs (thread tid owns runs 4*tid .. 4*tid+3)
         int cnt[kMaxSrcRows / kTileThreads];
 #pragma unroll
         for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) cnt[k] = roff[kMaxSrcRows / kTileThreads * tid + k];
@@ -526,13 +616,19 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
         }
     };
     if (!(meta & kMetaOverlap)) {
-        scatter_range(0, T.n);
+        scatter_range(0, nruns);
         fill_regions();
     } else {
-        // reference order: level l, l-1, ..., l-D, then interior nodes (last writer wins)
+        // reference order: level l, l-1, ..., l-D, then interior nodes (last writer
+        // wins); runs are in row-slot order, so each phase is a run range
+        int j0 = 0;
         for (int ph = 0; ph <= T.D + 1; ++ph) {
-            scatter_range(T.base[ph], ph <= T.D ? T.base[ph + 1] : T.n);
+            const int t1 = ph <= T.D ? T.base[ph + 1] : T.n;
+            int j1 = j0;
+            while (j1 < nruns && rslot[j1] < t1) ++j1;
+            scatter_range(j0, j1);
             fill_regions();
+            j0 = j1;
         }
     }
     __syncthreads();
@@ -750,6 +846,58 @@ void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
     L.tile_meta = meta;
 }
 
+// First use of an APR with stencil half-width H: the per-tile source runs.
+template <int H>
+void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
+    DevAccess& L = apr->leaf;
+    if (L.tile_runs[H - 1] || !L.tiles) return;
+    std::lock_guard<std::mutex> lk(apr->ctx->mu);
+    if (L.tile_runs[H - 1]) return;
+    const uint64_t n = L.tile_off[L.l_max + 1];
+    TileLaunch a = base_launch(apr);
+    uint32_t total = 0;
+    for (int l = L.l_min; l <= L.l_max; ++l) {
+        const uint32_t c = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
+        if (!c) continue;
+        total += c;
+        set_level(a, L, l, total);
+    }
+    uint32_t* off = nullptr;
+    APR_CUDA(cudaMalloc(&off, 4 * (n + 1)));
+    APR_CUDA(cudaMemsetAsync(off, 0, 4 * (n + 1), s));
+    uint2* runs = nullptr;
+    uint32_t nruns = 0;
+    if (total) {
+        a.tiles = L.tiles;
+        a.meta = L.tile_meta;
+        a.tile_base = static_cast<uint32_t>(L.tile_off[L.l_min]);
+        GpuBuf counts, temp;
+        counts.ensure(4 * (n + 1));
+        APR_CUDA(cudaMemsetAsync(counts.p, 0, 4 * (n + 1), s));
+        k_tile_runs<H><<<total, kTileThreads, 0, s>>>(a, 0, counts.as<uint32_t>() + a.tile_base, nullptr);
+        count_launch(apr->ctx);
+        APR_CUDA(cudaGetLastError());
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.as<uint32_t>(), off, static_cast<int64_t>(n + 1), s);
+        temp.ensure(tb + 16);
+        tb = temp.bytes;
+        APR_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, counts.as<uint32_t>(), off, static_cast<int64_t>(n + 1), s));
+        count_launch(apr->ctx);
+        APR_CUDA(cudaMemcpyAsync(&nruns, off + n, 4, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+        APR_CUDA(cudaMalloc(&runs, 8ull * nruns + 8));
+        a.run_off = off;
+        k_tile_runs<H><<<total, kTileThreads, 0, s>>>(a, 1, nullptr, runs);
+        count_launch(apr->ctx);
+        APR_CUDA(cudaGetLastError());
+        APR_CUDA(cudaStreamSynchronize(s));
+    } else {
+        APR_CUDA(cudaMalloc(&runs, 8));
+    }
+    L.tile_run_off[H - 1] = off;
+    L.tile_runs[H - 1] = runs;
+}
+
 template <typename Acc, int H>
 void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
     constexpr int bytes = Box<H>::NC * static_cast<int>(sizeof(Acc));
@@ -854,8 +1002,11 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
             b.pad = pad;
             b.out = out;
             b.epi = epi;
+            if (H == 1) ensure_tile_runs<1>(apr, s); else ensure_tile_runs<2>(apr, s);
             b.tiles = L.tiles;
             b.meta = L.tile_meta;
+            b.runs = L.tile_runs[H - 1];
+            b.run_off = L.tile_run_off[H - 1];
             const int first = l;
             uint32_t total = 0;
             for (; l <= L.l_max && ok(l); ++l) {

@@ -39,6 +39,12 @@ void DevAccess::release() {
     cudaFree(tiles);
     cudaFree(tile_meta);
     tile_meta = nullptr;
+    for (int h = 0; h < 2; ++h) {
+        cudaFree(tile_runs[h]);
+        cudaFree(tile_run_off[h]);
+        tile_runs[h] = nullptr;
+        tile_run_off[h] = nullptr;
+    }
     y = nullptr;
     rb = nullptr;
     work = nullptr;

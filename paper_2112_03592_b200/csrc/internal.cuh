@@ -65,6 +65,9 @@ struct DevAccess {
     std::vector<uint64_t> tile_off;        // l_max+2 offsets into tiles
     std::vector<int> tile_dims;            // 3 per level: tile grid (z, x, y)
     uint8_t* tile_meta = nullptr;          // device, one byte per tile (coarse depth, fill flags); lazy
+    // per tile, the non-empty source rows of its (H = 1, 2) box: {first particle, row slot | count << 16}
+    uint2* tile_runs[2] = {nullptr, nullptr};
+    uint32_t* tile_run_off[2] = {nullptr, nullptr};  // n_tiles + 1 offsets into tile_runs
     AccessView view() const;
     void release();
 };
