@@ -445,9 +445,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     __shared__ uint32_t rinfo[kMaxSrcRows];  // packed row geometry
     __shared__ uint32_t rsrc[kMaxSrcRows];   // global index of the row's first particle in the box
     __shared__ uint16_t rslot[kMaxSrcRows];  // run -> source-row slot
+    __shared__ int8_t rorid[kMaxSrcRows];    // run -> inner output row of the tile (-1: none)
     __shared__ int roff[kMaxSrcRows + 1];    // flattened offsets; roff[kMaxSrcRows] = total
     __shared__ int wsum[kTileThreads / 32];
-    __shared__ uint16_t rid[kMaxFlat];       // row of each flattened particle (current chunk)
+    __shared__ __align__(16) uint16_t rid[kMaxFlat];  // run of each flattened particle (current chunk)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
                            (static_cast<uint32_t>(J.xB - J.xA - 1) << 11) | (rbase << 15);
                 rsrc[j] = e.x;
                 rslot[j] = static_cast<uint16_t>(t);
+                rorid[j] = static_cast<int8_t>(J.inner ? J.obase : -1);
                 if (J.inner) orow[J.obase] = e.x;
             }
             roff[j] = n;
@@ -525,8 +527,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     __syncthreads();
 
     // ---- fill: one thread per source particle
+    int chunk0 = 0;  // first flattened index of the current rid chunk
     auto put = [&](int p) {
-        const int t = rid[p & (kMaxFlat - 1)];
+        const int t = rid[p - chunk0];
         const uint32_t info = rinfo[t];
         const int d = info & 31;
         const bool is_tree = (info >> 5) & 1;
@@ -536,11 +539,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
         const Acc v = static_cast<Acc>(__ldg((is_tree ? a.tval : a.val) + gi));
         if (d == 0) {
             S[rbase - G.by0 + yy] = v;
-            if (((info >> 6) & 1) && static_cast<unsigned>(yy - G.y0) < static_cast<unsigned>(kTY)) {
-                const int row = rbase / B::BY;  // box row = bz * BX + bx
-                const int orid = (row / B::BX - H) * kTX + (row % B::BX - H);
-                omap[orid * kTY + yy - G.y0] = static_cast<uint8_t>(gi - orow[orid]);
-            }
+            const int orid = rorid[t];  // inner output row of the tile, or -1
+            if (orid >= 0 && static_cast<unsigned>(yy - G.y0) < static_cast<unsigned>(kTY))
+                omap[orid * kTY + yy - G.y0] = static_cast<uint8_t>(p - roff[t]);  // orow[orid] = rsrc[t]
             return;
         }
         const int nzr = ((info >> 7) & 15) + 1, nxr = ((info >> 11) & 15) + 1;
@@ -608,9 +609,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
             const int c1 = min(c0 + kMaxFlat, q1);
             for (int t = r0 + tid; t < r1; t += kTileThreads) {
                 const int lo = max(roff[t], c0), hi = min(roff[t + 1], c1);
-                for (int q = lo; q < hi; ++q) rid[q & (kMaxFlat - 1)] = static_cast<uint16_t>(t);
+                for (int q = lo; q < hi; ++q) rid[q - c0] = static_cast<uint16_t>(t);
             }
             __syncthreads();
+            chunk0 = c0;
             for (int q = c0 + tid; q < c1; q += kTileThreads) put(q);
             __syncthreads();
         }
