@@ -424,7 +424,7 @@ template <> struct Vec<double> {
 };
 
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 3) : (H == 2 ? 4 : 5))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 4) : (H == 2 ? 4 : 6))
     k_conv_tile(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
     using VT = Vec<Acc>;
