@@ -149,6 +149,25 @@ int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_valu
 int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, int kx, int ky, int iterations,
               double epsilon, int accum, float* out, int ptr_kind, void* stream);
 
+/* ---- z-slab decomposition (multi-GPU) ----------------------
+ * Every rank holds the whole structure; a slab is the finest-level pixel
+ * planes [z_lo, z_hi) (z_lo, z_hi multiples of 2^(l_max - lc)).  Levels >= lc
+ * are partitioned (a cell fits in a slab), levels < lc are replicated.  All
+ * buffers are device pointers in the global particle / node numbering.
+ *
+ * fp64 tree sums of interior levels [lt_lo, lt_hi], parent rows in the slab
+ * only (z_hi < 0: all rows); the scratch holds n_tree doubles each and is what
+ * ranks exchange at the cut level. */
+int aprgpu_fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi,
+                          void* stream);
+int aprgpu_tree_scratch(aprgpu_apr* apr, double** vsum, double** wsum);
+/* tree[i] = float(vsum[i] / wsum[i]) (0 when wsum is 0), tree.hpp:146-148 */
+int aprgpu_fill_tree_finalize(aprgpu_apr* apr, float* tree, void* stream);
+/* convolve_apr computing the outputs of levels >= lc in the slab's rows and of
+ * every level < lc; other outputs are left untouched. */
+int aprgpu_convolve_slab(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
+                         int pad_mode, int accum, int lc, int z_lo, int z_hi, float* out, void* stream);
+
 /* rl_apr resumed from a running estimate (estimate_in[n_particles]; NULL =
  * start from the clamped observation, i.e. aprgpu_rl).  The reference's state
  * between iterations is exactly (u, epsilon, estimate), so running k iterations

@@ -545,6 +545,57 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
     });
 }
 
+int aprgpu_fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi,
+                          void* stream) {
+    return guard([&] {
+        need(apr && (leaf || apr->leaf.n_particles == 0), "null argument");
+        DeviceGuard g(apr->ctx->device);
+        aprgpu::fill_tree_sums(apr, leaf, lt_lo, lt_hi, z_lo, z_hi, aprgpu::pick_stream(apr->ctx, stream));
+    });
+}
+
+int aprgpu_tree_scratch(aprgpu_apr* apr, double** vsum, double** wsum) {
+    return guard([&] {
+        need(apr && vsum && wsum, "null argument");
+        DeviceGuard g(apr->ctx->device);
+        const uint64_t nt = apr->tree.n_particles;
+        if (!apr->vsum.p || apr->vsum.bytes < sizeof(double) * nt) {
+            apr->vsum.ensure(sizeof(double) * nt + 8);
+            apr->wsum.ensure(sizeof(double) * nt + 8);
+        }
+        *vsum = apr->vsum.as<double>();
+        *wsum = apr->wsum.as<double>();
+    });
+}
+
+int aprgpu_fill_tree_finalize(aprgpu_apr* apr, float* tree, void* stream) {
+    return guard([&] {
+        need(apr && (tree || apr->tree.n_particles == 0), "null argument");
+        DeviceGuard g(apr->ctx->device);
+        aprgpu::fill_tree_finalize(apr, tree, aprgpu::pick_stream(apr->ctx, stream));
+    });
+}
+
+int aprgpu_convolve_slab(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
+                         int pad_mode, int accum, int lc, int z_lo, int z_hi, float* out, void* stream) {
+    return guard([&] {
+        need(apr && values && pyr && out, "null argument");
+        need(tree_values || apr->tree.n_particles == 0, "tree values are required");
+        need(pad_mode == APRGPU_PAD_ZERO || pad_mode == APRGPU_PAD_REFLECT, "bad pad mode");
+        need(accum == APRGPU_ACCUM_EXACT || accum == APRGPU_ACCUM_FAST, "bad accumulation mode");
+        need(pyr->ctx == apr->ctx, "pyramid belongs to another context");
+        need(z_lo >= 0 && z_lo <= z_hi, "bad slab");
+        DeviceGuard g(apr->ctx->device);
+        aprgpu::Slab slab;
+        slab.lc = lc;
+        slab.z_lo = z_lo;
+        slab.z_hi = z_hi;
+        aprgpu::EpiArgs epi;
+        aprgpu::convolve_device(apr, values, tree_values, pyr, pad_mode, accum, out, epi,
+                                aprgpu::pick_stream(apr->ctx, stream), slab);
+    });
+}
+
 int aprgpu_generate_spheres(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, double min_radius,
                             double max_radius, double background, double min_intensity, double max_intensity,
                             double blur_sigma, uint64_t seed, float* out, int ptr_kind) {

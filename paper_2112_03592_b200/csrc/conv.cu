@@ -43,6 +43,7 @@ struct ConvArgs {
     int win, wbuf;
     float* out;
     EpiArgs epi;
+    int z_lo, z_hi;  // output rows processed: z in [z_lo, z_hi) (slab decomposition)
 };
 
 template <typename Acc>
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256) k_conv(ConvArgs a) {
         const uint32_t row = __ldg(a.work + wi);
         const uint32_t loc = row - gl.row0;
         const int z = static_cast<int>(loc / gl.xd), x = static_cast<int>(loc % gl.xd);
+        if (z < a.z_lo || z >= a.z_hi) continue;  // another slab's rows
         const uint32_t rb = __ldg(a.leaf.rb + row), re = __ldg(a.leaf.rb + row + 1);
         // number of neighbour rows that are real (not zero-padded)
         int real_rows = 0;
@@ -305,7 +307,7 @@ void check_pyramid(const aprgpu_apr* apr, const aprgpu_pyramid* pyr) {
 }
 
 void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
-                     int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s) {
+                     int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s, const Slab& slab) {
     check_pyramid(apr, pyr);
     const DevAccess& L = apr->leaf;
     const DevAccess& T = apr->tree;
@@ -318,7 +320,7 @@ void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_val
     a.out = out;
     a.epi = epi;
     bool done[kMaxLevels] = {};
-    if (use_tiles()) conv_tile_levels(apr, pyr, values, tree_values, pad, accum, out, epi, s, done);
+    if (use_tiles()) conv_tile_levels(apr, pyr, values, tree_values, pad, accum, out, epi, slab, s, done);
     for (int l = L.l_max; l >= L.l_min; --l) {
         if (done[l]) continue;
         a.n_work = L.work_off[l + 1] - L.work_off[l];
@@ -332,6 +334,13 @@ void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_val
         a.wf = pyr->w_dev + pyr->off[li];
         a.wd = pyr->wd_dev + pyr->off[li];
         a.tree_at_l = (T.n_particles > 0 && l >= T.l_min && l <= T.l_max) ? 1 : 0;
+        a.z_lo = 0;
+        a.z_hi = 1 << 30;
+        if (l >= slab.lc) {
+            const int sh = L.l_max - l;
+            a.z_lo = slab.z_lo >> sh;
+            a.z_hi = (slab.z_hi + (1 << sh) - 1) >> sh;
+        }
         if (accum == APRGPU_ACCUM_EXACT)
             dispatch<double>(apr->ctx, a, s);
         else

@@ -85,6 +85,7 @@ struct TileLaunch {
     int pad;
     float* out;
     EpiArgs epi;
+    int slab_lc, slab_zlo, slab_zhi;  // z-slab restriction (Slab, internal.cuh)
 };
 
 struct Geo {
@@ -456,6 +457,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     const LevelG g = a.leaf.g[l];
     const uint32_t tix = a.tile_base + blockIdx.x;
     const Geo G = make_geo<H>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], g);
+    if (l >= a.slab_lc) {  // slab decomposition: only tiles touching this slab's planes
+        const int sh = a.leaf.l_max - l;
+        if ((G.z0 + kTZ) << sh <= a.slab_zlo || G.z0 << sh >= a.slab_zhi) return;
+    }
     const int meta = a.meta[tix];
     const int tree = (l >= a.tree_lmin && l <= a.tree_lmax) ? 1 : 0;
 
@@ -974,7 +979,8 @@ void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a) {
 // kernel (one launch per extent and run of consecutive levels, coarse levels
 // first); sets done[l] for them.
 void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* values, const float* tree_values,
-                      int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s, bool* done) {
+                      int pad, int accum, float* out, const EpiArgs& epi, const Slab& slab, cudaStream_t s,
+                      bool* done) {
     const DevAccess& L = apr->leaf;
     if (!L.tiles) return;
     ensure_tile_meta(apr, s);
@@ -1004,6 +1010,9 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
             b.pad = pad;
             b.out = out;
             b.epi = epi;
+            b.slab_lc = slab.lc;
+            b.slab_zlo = slab.z_lo;
+            b.slab_zhi = slab.z_hi;
             if (H == 1) ensure_tile_runs<1>(apr, s); else ensure_tile_runs<2>(apr, s);
             b.tiles = L.tiles;
             b.meta = L.tile_meta;

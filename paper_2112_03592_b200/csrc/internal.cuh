@@ -124,12 +124,22 @@ void row_spans(aprgpu_ctx* ctx, const DevAccess& a, int level, int32_t* z, int32
 // conv_tile.cu
 void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a);
 void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* values, const float* tree_values,
-                      int pad, int accum, float* out, const struct EpiArgs& epi, cudaStream_t s, bool* done);
+                      int pad, int accum, float* out, const struct EpiArgs& epi, const struct Slab& slab,
+                      cudaStream_t s, bool* done);
 
 // tree.cu
 void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s);
+void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi, cudaStream_t s);
+void fill_tree_finalize(aprgpu_apr* apr, float* tree, cudaStream_t s);
+
+// z-slab restriction of a convolution: levels >= lc compute only
+// the tiles / rows that touch finest-level pixel planes [z_lo, z_hi); coarser
+// levels are computed whole.  lc > l_max: no restriction.
+struct Slab {
+    int lc = 1 << 20, z_lo = 0, z_hi = 1 << 30;
+};
 
 // conv.cu
 enum Epilogue { EPI_STORE = 0, EPI_RL_RATIO = 1, EPI_RL_MULT = 2 };
@@ -140,7 +150,7 @@ struct EpiArgs {
     float* est = nullptr;      // RL estimate (multiply epilogue; also the output)
 };
 void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
-                     int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s);
+                     int pad, int accum, float* out, const EpiArgs& epi, cudaStream_t s, const Slab& slab = Slab());
 void check_pyramid(const aprgpu_apr* apr, const aprgpu_pyramid* pyr);
 
 // build.cu

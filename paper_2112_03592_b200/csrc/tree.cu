@@ -166,6 +166,7 @@ struct FillArgs {
     uint64_t n_work;
     int lt, c, leaf_ok, tree_ok;  // c = lt+1; children are leaves / interior nodes
     int czd, cxd, glm, nz, nx, ny;
+    int pz_lo, pz_hi;  // parent rows processed: z in [pz_lo, pz_hi) (slab decomposition)
 };
 
 __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
         const uint32_t prow = a.work[wi];
         const uint32_t loc = prow - pg.row0;
         const int pz = static_cast<int>(loc / pg.xd), px = static_cast<int>(loc % pg.xd);
+        if (pz < a.pz_lo || pz >= a.pz_hi) continue;  // another slab's rows
         const uint32_t pb = a.tree.rb[prow], pe = a.tree.rb[prow + 1];
         // child row ranges (4 leaf + 4 interior), held by lanes 0..7 and broadcast
         uint32_t cb = 0, ce = 0;
@@ -392,13 +394,20 @@ void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr) {
     if (bad) fail(APRGPU_ERR_INTEGRITY, "synchronized_parent_pass: missing parent for a child node");
 }
 
-void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s) {
+// fp64 sums (vsum, wsum) of interior levels [lt_lo, lt_hi] (finest first),
+// restricted to parent rows whose cells lie in the finest-level pixel planes
+// [z_lo, z_hi) (z_hi < 0: every row).  Slab-decomposed callers run the levels
+// whose cells fit in a slab locally, exchange the cut level's sums and run the
+// coarser levels everywhere; fill_tree_device is all of it.
+void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi, cudaStream_t s) {
     aprgpu_ctx* ctx = apr->ctx;
     const DevAccess& L = apr->leaf;
     const DevAccess& T = apr->tree;
     if (T.n_particles == 0) return;
-    apr->vsum.ensure(sizeof(double) * T.n_particles);
-    apr->wsum.ensure(sizeof(double) * T.n_particles);
+    if (!apr->vsum.p || apr->vsum.bytes < sizeof(double) * T.n_particles) {
+        apr->vsum.ensure(sizeof(double) * T.n_particles);
+        apr->wsum.ensure(sizeof(double) * T.n_particles);
+    }
     FillArgs a{};
     a.leaf = L.view();
     a.tree = T.view();
@@ -409,13 +418,15 @@ void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStrea
     a.nz = apr->dims[0];
     a.nx = apr->dims[1];
     a.ny = apr->dims[2];
-    for (int lt = T.l_max; lt >= T.l_min; --lt) {
+    for (int lt = std::min(lt_hi, T.l_max); lt >= std::max(lt_lo, T.l_min); --lt) {
         a.lt = lt;
         a.c = lt + 1;
         a.leaf_ok = (a.c >= L.l_min && a.c <= L.l_max) ? 1 : 0;
         a.tree_ok = (a.c <= T.l_max) ? 1 : 0;
         a.czd = grid_dim_dev(a.nz, a.glm, a.c);
         a.cxd = grid_dim_dev(a.nx, a.glm, a.c);
+        a.pz_lo = z_hi < 0 ? 0 : (z_lo >> (a.glm - lt));
+        a.pz_hi = z_hi < 0 ? (1 << 30) : ((z_hi + (1 << (a.glm - lt)) - 1) >> (a.glm - lt));
         a.work = T.work + T.work_off[lt];
         a.n_work = T.work_off[lt + 1] - T.work_off[lt];
         if (a.n_work == 0) continue;
@@ -423,10 +434,21 @@ void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStrea
         k_fill_tree_level<<<grid, 256, 0, s>>>(a);
         count_launch(ctx);
     }
-    k_tree_finalize<<<std::min<unsigned>(blocks_for(T.n_particles, 256), ctx->sm_count * 8), 256, 0, s>>>(
-        apr->vsum.as<double>(), apr->wsum.as<double>(), T.n_particles, tree);
-    count_launch(ctx);
     APR_CUDA(cudaGetLastError());
+}
+
+void fill_tree_finalize(aprgpu_apr* apr, float* tree, cudaStream_t s) {
+    const DevAccess& T = apr->tree;
+    if (T.n_particles == 0) return;
+    k_tree_finalize<<<std::min<unsigned>(blocks_for(T.n_particles, 256), apr->ctx->sm_count * 8), 256, 0, s>>>(
+        apr->vsum.as<double>(), apr->wsum.as<double>(), T.n_particles, tree);
+    count_launch(apr->ctx);
+    APR_CUDA(cudaGetLastError());
+}
+
+void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s) {
+    fill_tree_sums(apr, leaf, 0, 1 << 20, 0, -1, s);
+    fill_tree_finalize(apr, tree, s);
 }
 
 }  // namespace aprgpu
