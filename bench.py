@@ -223,6 +223,18 @@ def run_ours(args, rank, world):
         if i >= args.warmup:
             e2e.append(b - a)
 
+    # C5: rl_apr, 10 Richardson-Lucy iterations on the same APR (deconv.hpp:75-107:
+    # 2 tree refreshes + 2 convolutions per iteration, ratio/multiply fused)
+    rl_out = torch.empty_like(out)
+    rl_t = []
+    for i in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dapr.rl_ptr(v.data_ptr(), w, args.rl_iters, 0.0, accum, rl_out.data_ptr(), s)
+        e1.record(stream)
+        e1.synchronize()
+        rl_t.append(e0.elapsed_time(e1) / 1e3)
+
     def agg(x):
         t = float(np.mean(x))
         if world > 1:
@@ -255,7 +267,7 @@ def run_ours(args, rank, world):
                        particles=n_p, interior_nodes=apr.tree_access.particle_count(), pixels=n_pix,
                        cr=round(n_pix / n_p, 2), l2="flushed between timed steps (256 MB write)",
                        protocol="conv-only (tree filled outside the timed region, bench.hpp:158-169)",
-                       parallelism=f"{world} independent replicas" if world > 1 else "single GPU"),
+                       parallelism="single GPU"),
         "particles_per_s": round(world * n_p / tc, 1),
         "paper_protocol": {"ms_per_step": round(tp * 1e3, 4), "gbps_pixel_equiv": round(4 * n_pix / tp / 1e9, 3),
                            "includes": "fill_tree + convolve_apr (row index prebuilt at upload)"},
@@ -271,10 +283,142 @@ def run_ours(args, rank, world):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 2),
+        "rl_apr": {"iterations": args.rl_iters, "ms": round(rl_t[-1] * 1e3, 3),
+                   "ms_per_iteration": round(rl_t[-1] * 1e3 / max(args.rl_iters, 1), 4),
+                   "psf": f"gaussian(1.0,{k}), restricted pyramids of w and flip(w)",
+                   "note": "C5; second of two runs, includes the pyramid setup and one D2H for the mean"},
     }
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(apr, values, tv[:dapr.n_tree].cpu().numpy(), pyr, args)
     return res
+
+
+# ------------------------------------------------------- multi-GPU z-slabs ---
+def run_slab(args, rank, world):
+    """N > 1: ONE volume (strong scaling) cut into z-slabs, one per GPU
+    (paper_2112_03592_b200.slab).  A conv-only step is the halo
+    exchange of leaf and tree values over NCCL plus each rank's slab
+    convolution; the paper step adds the slab tree fill with its cut-level
+    all-gather.  Time = max over ranks of the CUDA-event step time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2112_03592_b200 as P
+    from paper_2112_03592_b200 import _lib as L
+    from paper_2112_03592_b200.slab import GpuRankState, SlabConvolver, SlabPlan, TorchComm
+
+    dev_id = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev_id)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.default_context(dev_id)
+    apr, values, desc = workload(args.config)
+    dapr = apr.device(ctx)
+    k = args.stencil
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, k), apr.access.l_min, apr.access.l_max, P.PyramidMode.Restricted)
+    dpyr = pyr.device(ctx)
+    accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
+    plan = SlabPlan.make(apr.access, apr.tree_access, apr.source_dims, world, rank, halo=max(k // 2, 1))
+    st = GpuRankState(plan, dapr, dev_id, stream)
+    st.values.copy_(torch.from_numpy(np.ascontiguousarray(values, np.float32)).to(st.device))
+    comm = TorchComm()
+    sc = SlabConvolver([st], comm)
+    sc.fill_tree()
+    leaf_x, tree_x = plan.halo_transfers("leaf"), plan.halo_transfers("tree")
+
+    def conv():
+        comm.exchange([st], "values", leaf_x)
+        comm.exchange([st], "tree", tree_x)
+        st.convolve_slab(dpyr, 1, accum)
+
+    def paper_step():
+        sc.convolve(dpyr, 1, accum)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=st.device)
+
+    def timed(fn, steps):
+        times = []
+        for _ in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        return times
+
+    for _ in range(args.warmup):
+        conv()
+        paper_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    l0 = ctx.launch_count()
+    with ClockSampler(dev_id) as clk:
+        t_conv = timed(conv, args.steps)
+        launches = ctx.launch_count() - l0
+        t_paper = timed(paper_step, args.steps)
+
+    # end to end: this rank's owned values from pinned host memory, the step,
+    # its owned outputs back to the host
+    owned = plan.owned("leaf") + [plan.replicated("leaf")]
+    hv = torch.from_numpy(np.ascontiguousarray(values, np.float32)).pin_memory()
+    hout = torch.empty(dapr.n_particles, dtype=torch.float32).pin_memory()
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        a = time.perf_counter()
+        for b, e in owned:
+            st.values[b:e].copy_(hv[b:e], non_blocking=True)
+        sc.convolve(dpyr, 1, accum)
+        for b, e in owned:
+            hout[b:e].copy_(st.out[b:e], non_blocking=True)
+        stream.synchronize()
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - a)
+    h2d = sum(4 * (e - b) for b, e in owned)
+
+    def agg(x):
+        tt = torch.tensor([float(np.mean(x))], dtype=torch.float64, device=st.device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    tc, tp, te = agg(t_conv), agg(t_paper), agg(e2e)
+    n_pix, n_p = apr.pixel_count(), apr.access.particle_count()
+    B = algorithmic_bytes(apr)
+    peak, peak_kind = peaks()
+    achieved = B / world / tc / 1e9  # per GPU: each owns ~1/N of the bytes
+    return {
+        "metric": METRIC,
+        "value": round(4 * n_pix / tc / 1e9, 3),
+        "unit": "GB/s (pixel-equivalent)",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(tc * 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 values, " + ("f64 accumulate (bit-exact)" if accum == L.ACCUM_EXACT else "f32 accumulate"),
+        "data": "synthetic",
+        "config": dict(desc, stencil=f"gaussian(1.0,{k}) restricted pyramid", pad="reflect", particles=n_p,
+                       pixels=n_pix, l2="flushed between timed steps (256 MB write)",
+                       protocol="conv-only: NCCL halo exchange (leaf + tree) + slab convolution",
+                       parallelism=f"z-slabs x{world} (cut level {plan.lc}, halo {plan.halo} rows/level)"),
+        "particles_per_s": round(n_p / tc, 1),
+        "paper_protocol": {"ms_per_step": round(tp * 1e3, 4), "gbps_pixel_equiv": round(4 * n_pix / tp / 1e9, 3),
+                           "includes": "halo exchange + slab fill_tree (cut-level all-gather) + slab convolution"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "note": f"per GPU: algorithmic bytes / N / step time; peak {peak_kind}"},
+        "e2e": {"value": round(4 * n_pix / te / 1e9, 3), "unit": "GB/s (pixel-equivalent)",
+                "ms_per_step": round(te * 1e3, 4), "h2d_bytes_per_step": int(h2d * world),
+                "d2h_bytes_per_step": int(h2d * world)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
 
 
 # -------------------------------------------------------------- CPU baseline --
@@ -366,7 +510,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c3"))
     ap.add_argument("--stencil", type=int, default=3)
@@ -374,6 +518,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rl-iters", type=int, default=10)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -388,7 +533,7 @@ def main():
         import torch
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         torch.distributed.init_process_group("nccl")
-    res = run_ours(args, rank, world)
+    res = run_slab(args, rank, world) if world > 1 else run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

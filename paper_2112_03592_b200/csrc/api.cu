@@ -131,6 +131,51 @@ __global__ void k_clamp_copy(const float* __restrict__ in, float* __restrict__ u
     }
 }
 
+// Exactness test + exact sum of the RL observations (see aprgpu_rl_resume).
+constexpr int kNoLowBit = 1 << 20;
+struct MeanStats {
+    double abs_sum;        // sum |v| (any order: an upper bound of every partial sum)
+    int neg_gexp_max;      // kNoLowBit - (smallest low-bit exponent); 0 = all values zero
+    int nonfinite;
+    unsigned long long isum;  // sum of v / 2^g as two's-complement int64 (order-free, exact)
+};
+
+__device__ __forceinline__ int low_bit_exp(float v) {  // exponent of the lowest set bit of v (v != 0, finite)
+    const uint32_t b = __float_as_uint(v);
+    const int e = static_cast<int>((b >> 23) & 0xff);
+    uint32_t m = b & 0x7fffff;
+    if (e) m |= 0x800000;
+    return (e ? e : 1) - 150 + __ffs(static_cast<int>(m)) - 1;
+}
+
+__global__ void k_mean_bound(const float* __restrict__ u, uint64_t n, MeanStats* st) {
+    double as = 0.0;
+    int gmin = kNoLowBit;
+    int bad = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = u[i];
+        if (!isfinite(v)) {
+            bad = 1;
+            continue;
+        }
+        as += fabs(static_cast<double>(v));
+        if (v != 0.0f) gmin = min(gmin, low_bit_exp(v));
+    }
+    atomicAdd(&st->abs_sum, as);
+    if (gmin != kNoLowBit) atomicMax(&st->neg_gexp_max, kNoLowBit - gmin);
+    if (bad) atomicOr(&st->nonfinite, 1);
+}
+
+__global__ void k_mean_exact(const float* __restrict__ u, uint64_t n, MeanStats* st) {
+    if (st->nonfinite || st->neg_gexp_max == 0) return;
+    const int g = kNoLowBit - st->neg_gexp_max;
+    if (!(st->abs_sum < ldexp(1.0, 53 + g) * 0.999999)) return;
+    long long acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        acc += static_cast<long long>(ldexp(static_cast<double>(u[i]), -g));  // exact: |v / 2^g| < 2^53
+    atomicAdd(&st->isum, static_cast<unsigned long long>(acc));
+}
+
 }  // namespace
 
 extern "C" {
@@ -509,13 +554,36 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
         if (estimate_in && estimate_in != est)  // resume: the running estimate replaces the clamped observation
             APR_CUDA(cudaMemcpyAsync(est, estimate_in, 4 * np,
                                      ptr_kind == APRGPU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-        // mean of the clamped observations in the reference's sequential order (deconv.hpp:90-92)
-        host_obs.resize(np);
-        APR_CUDA(cudaMemcpyAsync(host_obs.data(), u, 4 * np, cudaMemcpyDeviceToHost, s));
-        APR_CUDA(cudaStreamSynchronize(s));
+        // mean of the clamped observations in the reference's sequential order
+        // (deconv.hpp:90-92).  When every partial sum of that double loop is
+        // provably exact (all values are multiples of 2^g and sum|v| < 2^(53+g))
+        // the sequential sum IS the exact sum, computed on the device as an
+        // order-free int64 sum of v / 2^g; otherwise the host replays the loop.
         double mean = 0.0;
-        for (float v : host_obs) mean += v;
-        mean /= static_cast<double>(std::max<uint64_t>(np, 1));
+        if (epsilon <= 0.0) {
+            apr->tmp.ensure(64);
+            MeanStats* ms = apr->tmp.as<MeanStats>();
+            APR_CUDA(cudaMemsetAsync(ms, 0, sizeof(MeanStats), s));
+            const unsigned grid = std::min<unsigned>(aprgpu::blocks_for(np, 256), ctx->sm_count * 8);
+            k_mean_bound<<<grid, 256, 0, s>>>(u, np, ms);
+            k_mean_exact<<<grid, 256, 0, s>>>(u, np, ms);
+            aprgpu::count_launch(ctx, 2);
+            MeanStats h{};
+            APR_CUDA(cudaMemcpyAsync(&h, ms, sizeof(MeanStats), cudaMemcpyDeviceToHost, s));
+            APR_CUDA(cudaStreamSynchronize(s));
+            const int g = kNoLowBit - h.neg_gexp_max;  // smallest low-bit exponent of the values
+            const bool exact = !h.nonfinite && (np == 0 || h.neg_gexp_max == 0 ||
+                                                h.abs_sum < std::ldexp(1.0, 53 + g) * 0.999999);
+            if (exact) {
+                mean = h.neg_gexp_max == 0 ? 0.0 : std::ldexp(static_cast<double>(static_cast<int64_t>(h.isum)), g);
+            } else {
+                host_obs.resize(np);
+                APR_CUDA(cudaMemcpyAsync(host_obs.data(), u, 4 * np, cudaMemcpyDeviceToHost, s));
+                APR_CUDA(cudaStreamSynchronize(s));
+                for (float v : host_obs) mean += v;
+            }
+            mean /= static_cast<double>(std::max<uint64_t>(np, 1));
+        }
         const double eps = epsilon > 0.0 ? epsilon : 1e-6 * std::max(mean, 1e-30);  // rl_epsilon, deconv.hpp:36-38
         float* ratio = apr->rl_ratio.as<float>();
         float* tv = apr->rl_tv.as<float>();

@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -69,7 +70,40 @@ uint64_t restrict_budget() {
 
 }  // namespace
 
+namespace {
+HostStencil restrict_stencil_compute(const HostStencil& w, int delta);
+
+// restrict_stencil is a pure function of (w, delta) and its bit-exact replay
+// costs seconds at delta 8-9 (rl_apr builds two pyramids per call): memoised.
+struct RestrictKey {
+    int kz, kx, ky, delta;
+    std::vector<float> w;
+    bool operator==(const RestrictKey& o) const {
+        return kz == o.kz && kx == o.kx && ky == o.ky && delta == o.delta &&
+               std::memcmp(w.data(), o.w.data(), sizeof(float) * w.size()) == 0 && w.size() == o.w.size();
+    }
+};
+std::mutex g_restrict_mu;
+std::vector<std::pair<RestrictKey, HostStencil>> g_restrict_cache;  // small: a few pyramids
+}  // namespace
+
 HostStencil restrict_stencil_host(const HostStencil& w, int delta) {
+    if (delta <= 0) return restrict_stencil_compute(w, delta);
+    RestrictKey key{w.kz, w.kx, w.ky, delta, w.w};
+    {
+        std::lock_guard<std::mutex> lk(g_restrict_mu);
+        for (const auto& e : g_restrict_cache)
+            if (e.first == key) return e.second;
+    }
+    HostStencil r = restrict_stencil_compute(w, delta);
+    std::lock_guard<std::mutex> lk(g_restrict_mu);
+    if (g_restrict_cache.size() >= 256) g_restrict_cache.erase(g_restrict_cache.begin());
+    g_restrict_cache.emplace_back(std::move(key), r);
+    return r;
+}
+
+namespace {
+HostStencil restrict_stencil_compute(const HostStencil& w, int delta) {
     if (delta < 0) fail(APRGPU_ERR_RANGE, "restrict_stencil: delta must be >= 0");
     if (delta == 0) return w;
     if (delta > 30) fail(APRGPU_ERR_CAPABILITY, "restrict_stencil: delta too large");
@@ -165,6 +199,7 @@ HostStencil restrict_stencil_host(const HostStencil& w, int delta) {
     (void)floor_div;
     return out;
 }
+}  // namespace
 
 HostStencil gaussian_stencil_host(double sigma, int size) {
     // stencil.hpp:59-79
