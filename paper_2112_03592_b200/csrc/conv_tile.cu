@@ -59,7 +59,7 @@ constexpr int kTZ = 8, kTX = 8, kTY = APRGPU_TILE_Y, kTileThreads = 128;
 constexpr int kBlocks = (kTZ / 2) * (kTX / 2) * (kTY / 2);  // 2x2x2 output blocks per tile
 constexpr int kProbeH = 2;
 constexpr int kMaxSrcRows = 512;   // >= 2*(8+2*2)^2 + coarse rows of a 5^3 box
-constexpr int kMaxFlat = 2048;     // source particles per flattened chunk
+constexpr int kMaxFlat = 1536;     // source particles per flattened chunk
 constexpr int kPadY = 4;           // box y origin = y0 - kPadY (>= H, multiple of 4)
 enum : uint8_t { kMetaDepth = 0x1f, kMetaOverlap = 0x20, kMetaHoles = 0x40 };
 
@@ -398,7 +398,7 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // fma.
 __device__ __forceinline__ float to_f(double v) { return __double2float_rn(v); }
 __device__ __forceinline__ float to_f(float v) { return v; }
 
-constexpr int kMaxRegions = 64;
+constexpr int kMaxRegions = 32;
 
 // A leaf >= 3 levels coarser than the tile's level: the box offset of its
 // first clipped row (z, x at y = by0), nz x nx clipped rows, and nq quads of 4
@@ -425,7 +425,7 @@ template <> struct Vec<double> {
 };
 
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 4) : (H == 2 ? 4 : 6))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 4) : (H == 2 ? 4 : 7))
     k_conv_tile(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
     using VT = Vec<Acc>;
@@ -582,12 +582,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
         const int n = min(nreg, kMaxRegions);
         if (n == 0) return;
         if (warp == 0) {
-            int c0 = 0, c1 = 0;
-            if (2 * lane < n) c0 = reg[2 * lane].nz * reg[2 * lane].nx * reg[2 * lane].nq;
-            if (2 * lane + 1 < n) c1 = reg[2 * lane + 1].nz * reg[2 * lane + 1].nx * reg[2 * lane + 1].nq;
-            const int incl = warp_incl_scan(c0 + c1, lane);
-            rpre[2 * lane] = incl - c0 - c1;
-            rpre[2 * lane + 1] = incl - c1;
+            static_assert(kMaxRegions == 32, "one region per lane");
+            const int c0 = lane < n ? reg[lane].nz * reg[lane].nx * reg[lane].nq : 0;
+            const int incl = warp_incl_scan(c0, lane);
+            rpre[lane] = incl - c0;
             if (lane == 31) rpre[kMaxRegions] = incl;
         }
         __syncthreads();
