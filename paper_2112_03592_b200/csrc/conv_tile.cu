@@ -57,9 +57,10 @@ namespace aprgpu {
 
 constexpr int kTZ = 8, kTX = 8, kTY = APRGPU_TILE_Y, kTileThreads = 128;
 constexpr int kBlocks = (kTZ / 2) * (kTX / 2) * (kTY / 2);  // 2x2x2 output blocks per tile
+static_assert(kBlocks <= 256, "block ids are bytes");
 constexpr int kProbeH = 2;
 constexpr int kMaxSrcRows = 512;   // >= 2*(8+2*2)^2 + coarse rows of a 5^3 box
-constexpr int kMaxFlat = 1536;     // source particles per flattened chunk
+constexpr int kMaxFlat = 960;      // source particles per flattened chunk (fits 8 CTAs/SM)
 constexpr int kPadY = 4;           // box y origin = y0 - kPadY (>= H, multiple of 4)
 enum : uint8_t { kMetaDepth = 0x1f, kMetaOverlap = 0x20, kMetaHoles = 0x40 };
 
@@ -425,12 +426,15 @@ template <> struct Vec<double> {
 };
 
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 4) : (H == 2 ? 4 : 7))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 4) : (H == 2 ? 4 : 8))
     k_conv_tile(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
     using VT = Vec<Acc>;
     using V2 = typename VT::T2;
     constexpr int K = 2 * H + 1, N = 2 + 2 * H, KW = K * K * K;
+    // runs of a tile <= its source rows: 2*(8+2H)^2 level-l leaf + interior rows
+    // plus <= 61 + 4 per extra depth coarse rows (<= 325 for H = 1, <= 493 for H = 2)
+    constexpr int kRuns = H == 1 ? 384 : 512;
     extern __shared__ __align__(16) unsigned char box_smem[];
     Acc* S = reinterpret_cast<Acc*>(box_smem);  // B::NC cells
     // output map: per inner cell the particle's offset from its row's first
@@ -438,16 +442,16 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     __shared__ __align__(16) uint8_t omap[kTZ * kTX * kTY];
     __shared__ uint32_t orow[kTZ * kTX];
     __shared__ Acc W[KW];
-    __shared__ uint16_t blist[kBlocks];
+    __shared__ uint8_t blist[kBlocks];
     __shared__ int nblk, nreg;
     __shared__ Region<Acc> reg[kMaxRegions];
     __shared__ int rpre[kMaxRegions + 1];
     __shared__ SrcTable T;
-    __shared__ uint32_t rinfo[kMaxSrcRows];  // packed row geometry
-    __shared__ uint32_t rsrc[kMaxSrcRows];   // global index of the row's first particle in the box
-    __shared__ uint16_t rslot[kMaxSrcRows];  // run -> source-row slot
-    __shared__ int8_t rorid[kMaxSrcRows];    // run -> inner output row of the tile (-1: none)
-    __shared__ int roff[kMaxSrcRows + 1];    // flattened offsets; roff[kMaxSrcRows] = total
+    __shared__ uint32_t rinfo[kRuns];  // packed row geometry
+    __shared__ uint32_t rsrc[kRuns];   // global index of the row's first particle in the box
+    __shared__ uint16_t rslot[kRuns];  // run -> source-row slot
+    __shared__ int8_t rorid[kRuns];    // run -> inner output row of the tile (-1: none)
+    __shared__ int roff[kRuns + 1];    // flattened offsets; roff[kRuns] = total
     __shared__ int wsum[kTileThreads / 32];
     __shared__ __align__(16) uint16_t rid[kMaxFlat];  // run of each flattened particle (current chunk)
 
@@ -485,10 +489,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     //   rinfo = d | is_tree << 5 | inner << 6 | (nz-1) << 7 | (nx-1) << 11 | rbase << 15
     //   rbase = box offset of the row's first clipped (z, x) at y = by0
     const uint32_t run0 = a.run_off[tix];
-    const int nruns = min(static_cast<int>(a.run_off[tix + 1] - run0), kMaxSrcRows);
+    const int nruns = min(static_cast<int>(a.run_off[tix + 1] - run0), kRuns);
     {
 #pragma unroll
-        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
+        for (int k = 0; k < kRuns / kTileThreads; ++k) {
             const int j = tid + k * kTileThreads;
             int n = 0;
             if (j < nruns) {
@@ -510,24 +514,24 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
         }
         __syncthreads();
         // exclusive scan over runs (thread tid owns runs 4*tid .. 4*tid+3)
-        int cnt[kMaxSrcRows / kTileThreads];
+        int cnt[kRuns / kTileThreads];
 #pragma unroll
-        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) cnt[k] = roff[kMaxSrcRows / kTileThreads * tid + k];
+        for (int k = 0; k < kRuns / kTileThreads; ++k) cnt[k] = roff[kRuns / kTileThreads * tid + k];
         __syncthreads();
         int sum = 0;
 #pragma unroll
-        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) sum += cnt[k];
+        for (int k = 0; k < kRuns / kTileThreads; ++k) sum += cnt[k];
         const int incl = warp_incl_scan(sum, lane);
         if (lane == 31) wsum[warp] = incl;
         __syncthreads();
         int base = incl - sum;
         for (int w = 0; w < warp; ++w) base += wsum[w];
 #pragma unroll
-        for (int k = 0; k < kMaxSrcRows / kTileThreads; ++k) {
-            roff[kMaxSrcRows / kTileThreads * tid + k] = base;
+        for (int k = 0; k < kRuns / kTileThreads; ++k) {
+            roff[kRuns / kTileThreads * tid + k] = base;
             base += cnt[k];
         }
-        if (tid == kTileThreads - 1) roff[kMaxSrcRows] = base;
+        if (tid == kTileThreads - 1) roff[kRuns] = base;
     }
     __syncthreads();
 
@@ -665,7 +669,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
         const unsigned m = *reinterpret_cast<const uint16_t*>(o) & *reinterpret_cast<const uint16_t*>(o + kTY) &
                            *reinterpret_cast<const uint16_t*>(o + kTX * kTY) &
                            *reinterpret_cast<const uint16_t*>(o + kTX * kTY + kTY);
-        if (m != 0xffffu) blist[atomicAdd(&nblk, 1)] = static_cast<uint16_t>(b);
+        if (m != 0xffffu) blist[atomicAdd(&nblk, 1)] = static_cast<uint8_t>(b);
     }
     __syncthreads();
 
