@@ -426,17 +426,16 @@ template <> struct Vec<double> {
 };
 
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 : 4) : (H == 2 ? 4 : 8))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 8))
     k_conv_tile(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
-    using VT = Vec<Acc>;
-    using V2 = typename VT::T2;
+    using VT = Vec<float>;  // the box holds the particle values themselves (floats) in both modes
     constexpr int K = 2 * H + 1, N = 2 + 2 * H, KW = K * K * K;
     // runs of a tile <= its source rows: 2*(8+2H)^2 level-l leaf + interior rows
     // plus <= 61 + 4 per extra depth coarse rows (<= 325 for H = 1, <= 493 for H = 2)
     constexpr int kRuns = H == 1 ? 384 : 512;
     extern __shared__ __align__(16) unsigned char box_smem[];
-    Acc* S = reinterpret_cast<Acc*>(box_smem);  // B::NC cells
+    float* S = reinterpret_cast<float*>(box_smem);  // B::NC cells
     // output map: per inner cell the particle's offset from its row's first
     // particle in the box (0xff: no output particle); per inner row that index
     __shared__ __align__(16) uint8_t omap[kTZ * kTX * kTY];
@@ -444,7 +443,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     __shared__ Acc W[KW];
     __shared__ uint8_t blist[kBlocks];
     __shared__ int nblk, nreg;
-    __shared__ Region<Acc> reg[kMaxRegions];
+    __shared__ Region<float> reg[kMaxRegions];
     __shared__ int rpre[kMaxRegions + 1];
     __shared__ SrcTable T;
     __shared__ uint32_t rinfo[kRuns];  // packed row geometry
@@ -476,7 +475,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
         for (int i = tid; i < kTZ * kTX * kTY / 16; i += kTileThreads) om[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
     }
     if (meta & kMetaHoles)
-        for (int i = tid; i < B::NC; i += kTileThreads) S[i] = Acc(0);
+        for (int i = tid; i < B::NC; i += kTileThreads) S[i] = 0.0f;
     if (tid == 0) {
         nblk = 0;
         nreg = 0;
@@ -545,7 +544,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
         const int rbase = static_cast<int>(info >> 15);
         const uint32_t gi = rsrc[t] + static_cast<uint32_t>(p - roff[t]);
         const int yy = __ldg((is_tree ? a.tree.y : a.leaf.y) + gi);
-        const Acc v = static_cast<Acc>(__ldg((is_tree ? a.tval : a.val) + gi));
+        const float v = __ldg((is_tree ? a.tval : a.val) + gi);
         if (d == 0) {
             S[rbase - G.by0 + yy] = v;
             const int orid = rorid[t];  // inner output row of the tile, or -1
@@ -554,7 +553,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
             return;
         }
         const int nzr = ((info >> 7) & 15) + 1, nxr = ((info >> 11) & 15) + 1;
-        Acc* p0 = S + rbase - G.by0 + (yy << d);
+        float* p0 = S + rbase - G.by0 + (yy << d);
         if (d == 1) {
             VT::st2(p0, v);
             if (nxr == 2) VT::st2(p0 + B::BY, v);
@@ -572,7 +571,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
             const int c0 = max((yy << d) - G.by0, 0), c1 = min(((yy + 1) << d) - G.by0, B::BY);
             const int slot = atomicAdd(&nreg, 1);
             if (slot < kMaxRegions) {
-                reg[slot] = Region<Acc>{rbase, nzr, nxr, c0 >> 2, (c1 - c0) >> 2, v};
+                reg[slot] = Region<float>{rbase, nzr, nxr, c0 >> 2, (c1 - c0) >> 2, v};
             } else {
                 for (int z = 0; z < nzr; ++z)
                     for (int x = 0; x < nxr; ++x)
@@ -600,7 +599,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
                 const int mid = (lo + hi + 1) >> 1;
                 if (rpre[mid] <= c) lo = mid; else hi = mid - 1;
             }
-            const Region<Acc> R = reg[lo];
+            const Region<float> R = reg[lo];
             const int j = c - rpre[lo];
             const int row = j / R.nq, qd = j - row * R.nq;
             const int zz = row / R.nx, xx = row - zz * R.nx;
@@ -651,12 +650,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
             if (zz >= g.zd + H || xx >= g.xd + H) continue;  // read by no output
             const bool row_out = zz < 0 || zz >= g.zd || xx < 0 || xx >= g.xd;
             const int rz = reflect_dev(zz, g.zd) - G.bz0, rx = reflect_dev(xx, g.xd) - G.bx0;
-            Acc* dst = S + r * B::BY - G.by0;
-            const Acc* src = S + (rz * B::BX + rx) * B::BY - G.by0;
+            float* dst = S + r * B::BY - G.by0;
+            const float* src = S + (rz * B::BX + rx) * B::BY - G.by0;
             for (int yy = G.y0 - H; yy < min(G.y0 + kTY + H, g.yd + H); ++yy) {
                 const bool out = row_out || yy < 0 || yy >= g.yd;
                 if (!out) continue;
-                dst[yy] = a.pad == APRGPU_PAD_ZERO ? Acc(0) : src[reflect_dev(yy, g.yd)];
+                dst[yy] = a.pad == APRGPU_PAD_ZERO ? 0.0f : src[reflect_dev(yy, g.yd)];
             }
         }
         __syncthreads();
@@ -682,7 +681,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
     for (int q = tid; q < nb; q += kTileThreads) {
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
-        const Acc* base = S + ((2 * qz) * B::BX + 2 * qx) * B::BY + 2 * qy + YA;
+        const float* base = S + ((2 * qz) * B::BX + 2 * qx) * B::BY + 2 * qy + YA;
         Acc acc[8];
         if constexpr (sizeof(Acc) == 4) {
             // FAST: the block's two y-outputs share every tap's weight -> packed
@@ -737,10 +736,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 2 :
                 for (int nx = 0; nx < N; ++nx) {
                     Acc r[2 * NP];
 #pragma unroll
-                    for (int pp = 0; pp < NP; ++pp) {
-                        const V2 t2 = *reinterpret_cast<const V2*>(base + (nz * B::BX + nx) * B::BY + 2 * pp);
-                        r[2 * pp] = t2.x;
-                        r[2 * pp + 1] = t2.y;
+                    for (int pp = 0; pp < NP; ++pp) {  // exact: every float is a double
+                        const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * B::BX + nx) * B::BY + 2 * pp);
+                        r[2 * pp] = static_cast<Acc>(t2.x);
+                        r[2 * pp + 1] = static_cast<Acc>(t2.y);
                     }
 #pragma unroll
                     for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
@@ -909,7 +908,7 @@ void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
 
 template <typename Acc, int H>
 void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
-    constexpr int bytes = Box<H>::NC * static_cast<int>(sizeof(Acc));
+    constexpr int bytes = Box<H>::NC * static_cast<int>(sizeof(float));
     static const bool attr = [] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_tile<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         return true;
