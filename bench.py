@@ -152,23 +152,44 @@ def run_ours(args, rank, world):
     dev_id = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev_id)
     ctx = P.default_context(dev_id)
-    apr, values, desc = workload(args.config)
-    t0 = time.time()
-    dapr = apr.device(ctx)
-    k = args.stencil
-    w = P.gaussian_stencil(1.0, k)
-    pyr = P.make_pyramid(w, apr.access.l_min, apr.access.l_max, P.PyramidMode.Restricted)
-    dpyr = pyr.device(ctx)
-    setup_s = time.time() - t0
-    accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
-
     # an explicit stream: torch's legacy default stream has handle 0, which the
     # C-ABI reads as "the context's own stream"
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     s = stream.cuda_stream
     assert s != 0
-    v = torch.from_numpy(np.ascontiguousarray(values, np.float32)).cuda()
+    t0 = time.time()
+    if args.config == "c4":
+        # C3 built on the device, tiled 4(z) x 4(x) x 2(y) on the device
+        from paper_2112_03592_b200 import synth
+        apr3, values3, _ = workload("c3")
+        d3 = apr3.device(ctx)
+        dapr = synth.tile_apr(d3, 4, 4, 2)
+        v3 = torch.from_numpy(np.ascontiguousarray(values3, np.float32)).cuda()
+        v = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")
+        synth.tile_values(d3, dapr, 4, 4, 2, v3.data_ptr(), v.data_ptr())
+        del v3
+        apr, values = None, None
+        li, ti = dapr.info(L.LEAF), dapr.info(L.TREE)
+        n_p, n_t, n_rows = int(li.n_particles), int(ti.n_particles), int(li.n_rows + ti.n_rows)
+        l_min, l_max = int(li.l_min), int(li.l_max)
+        n_pix = int(np.prod(dapr.dims, dtype=np.int64))
+        desc = {"workload": "C4: the C3 APR tiled 4(z) x 4(x) x 2(y) -> 4096 x 4096 x 2048 pixel-equivalent "
+                            "(device tiler, paper's concatenated copies)"}
+    else:
+        apr, values, desc = workload(args.config)
+        dapr = apr.device(ctx)
+        v = torch.from_numpy(np.ascontiguousarray(values, np.float32)).cuda()
+        n_p, n_t = apr.access.particle_count(), apr.tree_access.particle_count()
+        n_rows = apr.access.row_count() + apr.tree_access.row_count()
+        l_min, l_max = apr.access.l_min, apr.access.l_max
+        n_pix = apr.pixel_count()
+    k = args.stencil
+    w = P.gaussian_stencil(1.0, k)
+    pyr = P.make_pyramid(w, l_min, l_max, P.PyramidMode.Restricted)
+    dpyr = pyr.device(ctx)
+    setup_s = time.time() - t0
+    accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
     tv = torch.empty(max(dapr.n_tree, 1), dtype=torch.float32, device="cuda")
     out = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")
     dapr.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
@@ -210,7 +231,7 @@ def run_ours(args, rank, world):
         torch.distributed.barrier()
 
     # end to end through the C-ABI with pinned host buffers (H2D + conv + D2H per step)
-    hv = torch.from_numpy(np.ascontiguousarray(values, np.float32)).pin_memory()
+    hv = v.cpu().pin_memory()
     htv = tv[:dapr.n_tree].cpu().pin_memory() if dapr.n_tree else torch.zeros(1).pin_memory()
     hout = torch.empty(dapr.n_particles, dtype=torch.float32).pin_memory()
     e2e = []
@@ -244,9 +265,7 @@ def run_ours(args, rank, world):
         return t
 
     tc, tp, te = agg(t_conv), agg(t_paper), agg(e2e)
-    n_pix = apr.pixel_count()
-    n_p = apr.access.particle_count()
-    B = algorithmic_bytes(apr)
+    B = 10 * n_p + 6 * n_t + 4 * n_rows  # algorithmic_bytes()
     peak, peak_kind = peaks()
     achieved = B / tc / 1e9
     traffic, traffic_src = ncu_traffic(args.config, k, args.accum)
@@ -264,7 +283,7 @@ def run_ours(args, rank, world):
         "dtype": "f32 values, " + ("f64 accumulate (bit-exact)" if accum == L.ACCUM_EXACT else "f32 accumulate"),
         "data": "synthetic",
         "config": dict(desc, stencil=f"gaussian(1.0,{k}) restricted pyramid", pad="reflect",
-                       particles=n_p, interior_nodes=apr.tree_access.particle_count(), pixels=n_pix,
+                       particles=n_p, interior_nodes=n_t, pixels=n_pix,
                        cr=round(n_pix / n_p, 2), l2="flushed between timed steps (256 MB write)",
                        protocol="conv-only (tree filled outside the timed region, bench.hpp:158-169)",
                        parallelism="single GPU"),
@@ -288,7 +307,7 @@ def run_ours(args, rank, world):
                    "psf": f"gaussian(1.0,{k}), restricted pyramids of w and flip(w)",
                    "note": "C5; second of two runs, includes the pyramid setup and one D2H for the mean"},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and apr is not None:
         res["cpu_baseline"] = cpu_baseline(apr, values, tv[:dapr.n_tree].cpu().numpy(), pyr, args)
     return res
 
@@ -512,7 +531,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c3"))
+    ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c3"), choices=["c1", "c3", "c4"])
     ap.add_argument("--stencil", type=int, default=3)
     ap.add_argument("--accum", default="fast", choices=["exact", "fast"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

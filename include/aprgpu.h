@@ -188,6 +188,14 @@ int aprgpu_generate_spheres(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, 
  * leaf access + interior access + sampled particle values (aprgpu_apr_values). */
 int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny, double rel_error, int ptr_kind,
                      aprgpu_apr** out);
+/* The C4 tiler: a power-of-two cube APR tiled (tz, tx, ty) times into a new
+ * APR built directly in the device layout (structure + interior structure),
+ * and the matching tiling of particle values (device pointers; big_values
+ * holds n_particles of the tiled APR). */
+int aprgpu_tile_apr(aprgpu_apr* src, int tz, int tx, int ty, aprgpu_apr** out);
+int aprgpu_tile_values(aprgpu_apr* src, aprgpu_apr* big, int tz, int tx, int ty, const float* src_values,
+                       float* big_values);
+
 /* Copies the particle values sampled by aprgpu_build_apr (sample_particles,
  * build.hpp:252-284) into out[n_particles]. */
 int aprgpu_apr_values(const aprgpu_apr* apr, float* out, int ptr_kind);

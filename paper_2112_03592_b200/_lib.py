@@ -72,6 +72,8 @@ _SIGS = {
     "aprgpu_fill_tree_finalize": [C.c_void_p, C.c_void_p, C.c_void_p],
     "aprgpu_convolve_slab": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_void_p, C.c_void_p],
+    "aprgpu_tile_apr": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)],
+    "aprgpu_tile_values": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p],
     "aprgpu_launch_count": [C.c_void_p, C.POINTER(C.c_uint64)],
     "aprgpu_generate_spheres": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                 C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_void_p, C.c_int],

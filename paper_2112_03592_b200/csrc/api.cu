@@ -720,6 +720,37 @@ int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int n
     return st;
 }
 
+int aprgpu_tile_apr(aprgpu_apr* src, int tz, int tx, int ty, aprgpu_apr** out) {
+    aprgpu_apr* big = nullptr;
+    int st = guard([&] {
+        need(src && out && tz > 0 && tx > 0 && ty > 0, "bad argument");
+        aprgpu_ctx* ctx = src->ctx;
+        DeviceGuard g(ctx->device);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        big = new aprgpu_apr;
+        big->ctx = ctx;
+        aprgpu::tile_apr_device(ctx, src, tz, tx, ty, big, nullptr, nullptr, ctx->stream);
+        *out = big;
+    });
+    if (st != APRGPU_OK && big) {
+        free_apr(big);
+        delete big;
+    }
+    return st;
+}
+
+int aprgpu_tile_values(aprgpu_apr* src, aprgpu_apr* big, int tz, int tx, int ty, const float* src_values,
+                       float* big_values) {
+    return guard([&] {
+        need(src && big && src_values && big_values, "null argument");
+        need(src->ctx == big->ctx, "APRs belong to different contexts");
+        DeviceGuard g(src->ctx->device);
+        if (big->dims[0] != src->dims[0] * tz || big->dims[1] != src->dims[1] * tx || big->dims[2] != src->dims[2] * ty)
+            fail(APRGPU_ERR_RANGE, "tile_values: big APR is not this tiling of the source");
+        aprgpu::tile_apr_device(src->ctx, src, tz, tx, ty, big, src_values, big_values, src->ctx->stream);
+    });
+}
+
 int aprgpu_apr_values(const aprgpu_apr* apr, float* out, int ptr_kind) {
     return guard([&] {
         need(apr && out, "null argument");

@@ -160,6 +160,10 @@ void generate_spheres_device(aprgpu_ctx* ctx, int nz, int nx, int ny, int count,
 void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny, double rel_error, aprgpu_apr* apr,
                       GpuBuf& values_out, cudaStream_t s);
 
+// tile.cu
+void tile_apr_device(aprgpu_ctx* ctx, const aprgpu_apr* src, int TZ, int TX, int TY, aprgpu_apr* big,
+                     const float* src_v, float* big_v, cudaStream_t s);
+
 // stencil.cpp (host)
 struct HostStencil {
     int kz = 1, kx = 1, ky = 1;

@@ -72,3 +72,18 @@ def build_spheres_apr(n, count: int, rmin: float, rmax: float, blur: float = 2.0
     finally:
         del vol
         torch.cuda.empty_cache()
+
+
+def tile_apr(dev: DeviceApr, tz: int, tx: int, ty: int) -> DeviceApr:
+    """The C4 tiler (aprgpu_tile_apr): a power-of-two cube APR on the device
+    tiled (tz, tx, ty) times, structure and interior structure built on the
+    device.  Returns the new device APR (no host copy: C4 is 548 M particles)."""
+    h = C.c_void_p()
+    L.check(L.lib().aprgpu_tile_apr(dev.handle, int(tz), int(tx), int(ty), C.byref(h)))
+    dims = (dev.dims[0] * tz, dev.dims[1] * tx, dev.dims[2] * ty)
+    return DeviceApr(dev.ctx, h, dims)
+
+
+def tile_values(src: DeviceApr, big: DeviceApr, tz: int, tx: int, ty: int, src_ptr: int, big_ptr: int) -> None:
+    """Particle values of `src` (device pointer) tiled like tile_apr into big_ptr."""
+    L.check(L.lib().aprgpu_tile_values(src.handle, big.handle, int(tz), int(tx), int(ty), src_ptr, big_ptr))
