@@ -10,6 +10,8 @@ timeout 900 python bench.py --accum exact --no-cpu-baseline > $O/bench_c3_k3_exa
 timeout 900 python bench.py --stencil 5 --no-cpu-baseline > $O/bench_c3_k5_fast.json 2>&1
 timeout 900 python bench.py --stencil 5 --accum exact --no-cpu-baseline > $O/bench_c3_k5_exact.json 2>&1
 timeout 600 python bench.py --config c1 --no-cpu-baseline > $O/bench_c1_k3_fast.json 2>&1
+timeout 1200 python bench.py --config c4 --steps 10 --no-cpu-baseline > $O/bench_c4_k3_fast.json 2>&1
+timeout 1200 python bench.py --config c4 --steps 10 --stencil 5 --no-cpu-baseline > $O/bench_c4_k5_fast.json 2>&1
 [ "$1" = "quick" ] && exit 0
 timeout 1200 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_reference.json 2>&1
 # launch list of the bench command (cold-cache, serialised: compare shares)
