@@ -87,6 +87,10 @@ struct TileLaunch {
     float* out;
     EpiArgs epi;
     int slab_lc, slab_zlo, slab_zhi;  // z-slab restriction (Slab, internal.cuh)
+    uint32_t* map[kMaxLevels];        // per segment: gather-map records (k_conv_map), or the build target
+    uint32_t* flat;                   // per H flattened source lists (DevAccess::tile_flat)
+    const uint32_t* flat_off;         // n_tiles + 1 offsets into flat
+    int* map_overflow;                // set by the build when a tile has > MapBox::NC sources
 };
 
 struct Geo {
@@ -103,6 +107,29 @@ struct Box {
     static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * kPadY;
     static constexpr int NR = BZ * BX, NC = BZ * BX * BY;
 };
+
+// Gather-map record of a tile (k_conv_map): the box as (8+2H) x (8+2H) rows
+// of kTY + 2H cells (y origin y0 - H: exactly the cells the stencil reads),
+// one 16-bit code per cell -- kFlat0 + the index of its source particle in the
+// tile's flattened source list (the concatenation of its source runs,
+// k_tile_runs), ZERO for a zero cell -- then per inner row an output mask over
+// y0 .. y0+kTY-1 and the index of its first output particle.  The flattened
+// source list itself (particle | interior << 31 per entry, padded to 4) lives
+// in DevAccess::tile_flat, shared by both pad modes.  In a valid APR every box
+// cell has one source, so a tile has at most NC sources (the build checks; a
+// malformed APR's overlapping sources can exceed it, and its levels then
+// reconstruct).
+constexpr int kFlat0 = 4;  // F[0 .. 3]: the zero (and 16-byte alignment of the copied list)
+template <int H>
+struct MapBox {
+    static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * H;
+    static constexpr int NC = BZ * BX * BY;
+    static_assert(NC % 8 == 0, "whole 16-byte code groups");
+    static constexpr int REC = NC / 2 + 2 * kTZ * kTX;  // 32-bit words per record
+    static constexpr uint32_t ZERO = 0;
+    static constexpr int NF = kFlat0 + ((NC + 3) & ~3);  // F entries
+};
+static_assert(kTY == 32, "one 32-bit output mask per inner row");
 
 template <int H>
 __device__ __forceinline__ Geo make_geo(int l, uint32_t id, int txd, int tyd, const LevelG& g) {
@@ -425,7 +452,184 @@ template <> struct Vec<double> {
     }
 };
 
-template <typename Acc, int H>
+// One 2x2x2 output block (qz, qx, qy) of a box with rows of BY cells whose y
+// origin is PADY cells below the tile's: all 8 outputs, taps accumulated in
+// the reference's (az, ax, ay) order (convolve.hpp:154-169).  The
+// neighbourhood's y window (box index 2qy + PADY - H .. +N) is loaded as
+// aligned pairs from the even index at or below it.
+template <typename Acc, int H, int BX, int BY, int PADY>
+__device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz, int qx, int qy, Acc (&acc)[8]) {
+    constexpr int K = 2 * H + 1, N = 2 + 2 * H;
+    constexpr int Y0 = PADY - H;
+    constexpr int YA = Y0 & ~1, SH = Y0 - YA, NP = (SH + N + 1) / 2;
+    const float* base = S + ((2 * qz) * BX + 2 * qx) * BY + 2 * qy + YA;
+    if constexpr (sizeof(Acc) == 4) {
+        // FAST: the block's two y-outputs share every tap's weight -> packed
+        // fp32x2 FMA (same per-element rounding as two FFMAs)
+        float2 acc2[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int nz = N - 1; nz >= 0; --nz) {
+            float v[N][N];
+#pragma unroll
+            for (int nx = 0; nx < N; ++nx) {
+                float r[2 * NP];
+#pragma unroll
+                for (int pp = 0; pp < NP; ++pp) {
+                    const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * BX + nx) * BY + 2 * pp);
+                    r[2 * pp] = t2.x;
+                    r[2 * pp + 1] = t2.y;
+                }
+#pragma unroll
+                for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
+            }
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz) {
+                const int az = oz + 2 * H - nz;
+                if (az < 0 || az > 2 * H) continue;
+#pragma unroll
+                for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+                    for (int ax = 0; ax < K; ++ax)
+#pragma unroll
+                        for (int ay = 0; ay < K; ++ay) {
+                            const float w = W[(az * K + ax) * K + ay];
+                            const int vx = ox + 2 * H - ax, vy = 2 * H - ay;
+                            acc2[oz * 2 + ox] =
+                                ffma2(make_float2(w, w), make_float2(v[vx][vy], v[vx][vy + 1]), acc2[oz * 2 + ox]);
+                        }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            acc[2 * i] = acc2[i].x;
+            acc[2 * i + 1] = acc2[i].y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = Acc(0);
+#pragma unroll
+        for (int nz = N - 1; nz >= 0; --nz) {
+            Acc v[N][N];
+#pragma unroll
+            for (int nx = 0; nx < N; ++nx) {
+                Acc r[2 * NP];
+#pragma unroll
+                for (int pp = 0; pp < NP; ++pp) {  // exact: every float is a double
+                    const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * BX + nx) * BY + 2 * pp);
+                    r[2 * pp] = static_cast<Acc>(t2.x);
+                    r[2 * pp + 1] = static_cast<Acc>(t2.y);
+                }
+#pragma unroll
+                for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
+            }
+            // output (oz, ox, oy) reads neighbourhood cell (oz + 2H - az, ox + 2H - ax, oy + 2H - ay);
+            // planes stream from the top, so each output sees az ascending
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz) {
+                const int az = oz + 2 * H - nz;
+                if (az < 0 || az > 2 * H) continue;
+#pragma unroll
+                for (int ox = 0; ox < 2; ++ox)
+#pragma unroll
+                    for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+                        for (int ax = 0; ax < K; ++ax)
+#pragma unroll
+                            for (int ay = 0; ay < K; ++ay)
+                                acc[(oz * 2 + ox) * 2 + oy] =
+                                    fma_t<Acc>(W[(az * K + ax) * K + ay], v[ox + 2 * H - ax][oy + 2 * H - ay],
+                                               acc[(oz * 2 + ox) * 2 + oy]);
+            }
+        }
+    }
+}
+
+// Output i of the launch's epilogue (EpiArgs, internal.cuh).
+__device__ __forceinline__ void store_out(const TileLaunch& a, uint32_t i, float r) {
+    if (a.epi.mode == EPI_STORE) {
+        a.out[i] = r;
+    } else if (a.epi.mode == EPI_RL_RATIO) {
+        // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
+        const double bd = static_cast<double>(r);
+        const double den = bd < a.epi.eps ? a.epi.eps : bd;
+        a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
+    } else {
+        a.epi.est[i] = __fmul_rn(a.epi.est[i], r);  // deconv.hpp:102
+    }
+}
+
+// ---- async copies (sm_90+ bulk copy with an mbarrier; sm_80+ cp.async) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// one bulk global -> shared copy completing on bar (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Ordered compaction of the tile's 2x2x2 output blocks (block-id order, so a
+// warp's blocks are mostly y-neighbours: conflict-free pair loads in apply).
+template <typename Pred>
+__device__ __forceinline__ int compact_blocks(Pred active, uint8_t* blist, int* wcnt) {
+    static_assert(kBlocks == 2 * kTileThreads, "two blocks per thread");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kTileThreads / 32;
+    bool f[2];
+    unsigned bal[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        f[k] = active(k * kTileThreads + tid);
+        bal[k] = __ballot_sync(~0u, f[k]);
+        if (lane == 0) wcnt[k * NW + warp] = __popc(bal[k]);
+    }
+    __syncthreads();
+    // k = 0 blocks come first: this warp's k = 0 blocks follow the lower warps'
+    // k = 0 blocks; its k = 1 blocks follow all k = 0 blocks and the lower warps' k = 1
+    int pre = 0, all0 = 0, pre1 = 0, all1 = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        pre += i < warp ? wcnt[i] : 0;
+        all0 += wcnt[i];
+        pre1 += i < warp ? wcnt[NW + i] : 0;
+        all1 += wcnt[NW + i];
+    }
+    pre1 += all0;
+    const int total = all0 + all1;
+    const unsigned below = (1u << lane) - 1u;
+    if (f[0]) blist[pre + __popc(bal[0] & below)] = static_cast<uint8_t>(tid);
+    if (f[1]) blist[pre1 + __popc(bal[1] & below)] = static_cast<uint8_t>(kTileThreads + tid);
+    return total;
+}
+
+// MAP: instead of convolving, write the tile's gather-map record (k_conv_map):
+// the fill runs unchanged on particle CODES (leaf i -> i + 1, interior node
+// j -> 2^31 | j, 0 = zero) in place of values, so the map reproduces every
+// fill rule -- overlap order, holes, reflect / zero pad -- by construction.
+template <typename Acc, int H, bool MAP = false>
 __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 8))
     k_conv_tile(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
@@ -442,7 +646,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __shared__ uint32_t orow[kTZ * kTX];
     __shared__ Acc W[KW];
     __shared__ uint8_t blist[kBlocks];
-    __shared__ int nblk, nreg;
+    __shared__ int nreg;
     __shared__ Region<float> reg[kMaxRegions];
     __shared__ int rpre[kMaxRegions + 1];
     __shared__ SrcTable T;
@@ -452,6 +656,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __shared__ int8_t rorid[kRuns];    // run -> inner output row of the tile (-1: none)
     __shared__ int roff[kRuns + 1];    // flattened offsets; roff[kRuns] = total
     __shared__ int wsum[kTileThreads / 32];
+    __shared__ int wcnt[2 * kTileThreads / 32];
     __shared__ __align__(16) uint16_t rid[kMaxFlat];  // run of each flattened particle (current chunk)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -474,10 +679,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         uint4* om = reinterpret_cast<uint4*>(omap);
         for (int i = tid; i < kTZ * kTX * kTY / 16; i += kTileThreads) om[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
     }
-    if (meta & kMetaHoles)
-        for (int i = tid; i < B::NC; i += kTileThreads) S[i] = 0.0f;
+    if (MAP || (meta & kMetaHoles))  // (a map record must hold no stale codes)
+        for (int i = tid; i < B::NC; i += kTileThreads) S[i] = MAP ? __uint_as_float(MapBox<H>::ZERO) : 0.0f;
     if (tid == 0) {
-        nblk = 0;
         nreg = 0;
         make_src_table<H>(G, meta & kMetaDepth, tree, T);
     }
@@ -535,6 +739,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __syncthreads();
 
     // ---- fill: one thread per source particle
+    const uint32_t flat0 = MAP ? a.flat_off[tix] : 0;
     int chunk0 = 0;  // first flattened index of the current rid chunk
     auto put = [&](int p) {
         const int t = rid[p - chunk0];
@@ -544,7 +749,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         const int rbase = static_cast<int>(info >> 15);
         const uint32_t gi = rsrc[t] + static_cast<uint32_t>(p - roff[t]);
         const int yy = __ldg((is_tree ? a.tree.y : a.leaf.y) + gi);
-        const float v = __ldg((is_tree ? a.tval : a.val) + gi);
+        float v;
+        if constexpr (MAP) {
+            if (p < MapBox<H>::NC) a.flat[flat0 + p] = gi | static_cast<uint32_t>(is_tree) << 31;
+            v = __uint_as_float(static_cast<uint32_t>(kFlat0 + p));
+        } else {
+            v = __ldg((is_tree ? a.tval : a.val) + gi);
+        }
         if (d == 0) {
             S[rbase - G.by0 + yy] = v;
             const int orid = rorid[t];  // inner output row of the tile, or -1
@@ -657,115 +868,56 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
             for (int yy = G.y0 - H; yy < min(G.y0 + kTY + H, g.yd + H); ++yy) {
                 const bool out = row_out || yy < 0 || yy >= g.yd;
                 if (!out) continue;
-                dst[yy] = a.pad == APRGPU_PAD_ZERO ? 0.0f : src[reflect_dev(yy, g.yd)];
+                dst[yy] = a.pad == APRGPU_PAD_ZERO ? (MAP ? __uint_as_float(MapBox<H>::ZERO) : 0.0f)
+                                                   : src[reflect_dev(yy, g.yd)];
             }
         }
         __syncthreads();
     }
 
-    // ---- compact the 2x2x2 blocks that hold output particles
-    for (int b = tid; b < kBlocks; b += kTileThreads) {
-        const int qz = b / (kBlocks / 4), qx = (b / (kTY / 2)) & 3, qy = b & (kTY / 2 - 1);
-        const uint8_t* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
-        const unsigned m = *reinterpret_cast<const uint16_t*>(o) & *reinterpret_cast<const uint16_t*>(o + kTY) &
-                           *reinterpret_cast<const uint16_t*>(o + kTX * kTY) &
-                           *reinterpret_cast<const uint16_t*>(o + kTX * kTY + kTY);
-        if (m != 0xffffu) blist[atomicAdd(&nblk, 1)] = static_cast<uint8_t>(b);
+    if constexpr (MAP) {
+        using M = MapBox<H>;
+        uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
+        if (tid == 0 && roff[nruns] > M::NC) atomicOr(a.map_overflow, 1);
+        auto code = [&](int c) -> uint32_t {
+            const int r = c / M::BY;
+            return __float_as_uint(S[r * B::BY + (c - r * M::BY) + (kPadY - H)]);
+        };
+        for (int u = tid; u < M::NC / 2; u += kTileThreads) rec[u] = code(2 * u) | code(2 * u + 1) << 16;
+        if (tid < kTZ * kTX) {  // per inner row: output mask over y0 .. y0+31 and the first output's index
+            uint32_t m = 0;
+            int first = -1;
+            for (int y = 0; y < kTY; ++y) {
+                const int o = omap[tid * kTY + y];
+                if (o == 0xff) continue;
+                m |= 1u << y;
+                if (first < 0) first = o;
+            }
+            rec[M::NC / 2 + tid] = m;
+            rec[M::NC / 2 + kTZ * kTX + tid] = m ? orow[tid] + first : 0u;
+        }
+        return;
     }
+
+    // ---- compact the 2x2x2 blocks that hold output particles
+    const int nb = compact_blocks(
+        [&](int b) {
+            const int qz = b / (kBlocks / 4), qx = (b / (kTY / 2)) & 3, qy = b & (kTY / 2 - 1);
+            const uint8_t* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
+            const unsigned m = *reinterpret_cast<const uint16_t*>(o) & *reinterpret_cast<const uint16_t*>(o + kTY) &
+                               *reinterpret_cast<const uint16_t*>(o + kTX * kTY) &
+                               *reinterpret_cast<const uint16_t*>(o + kTX * kTY + kTY);
+            return m != 0xffffu;
+        },
+        blist, wcnt);
     __syncthreads();
 
     // ---- apply: one thread per active block, 8 outputs
-    // neighbourhood y window of block qy: box index 2qy + kPadY - H .. +N,
-    // loaded as aligned pairs from the even index at or below it
-    constexpr int Y0 = kPadY - H;
-    constexpr int YA = Y0 & ~1, SH = Y0 - YA, NP = (SH + N + 1) / 2;
-    const int nb = nblk;
     for (int q = tid; q < nb; q += kTileThreads) {
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
-        const float* base = S + ((2 * qz) * B::BX + 2 * qx) * B::BY + 2 * qy + YA;
         Acc acc[8];
-        if constexpr (sizeof(Acc) == 4) {
-            // FAST: the block's two y-outputs share every tap's weight -> packed
-            // fp32x2 FMA (same per-element rounding as two FFMAs)
-            float2 acc2[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc2[i] = make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int nz = N - 1; nz >= 0; --nz) {
-                float v[N][N];
-#pragma unroll
-                for (int nx = 0; nx < N; ++nx) {
-                    float r[2 * NP];
-#pragma unroll
-                    for (int pp = 0; pp < NP; ++pp) {
-                        const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * B::BX + nx) * B::BY + 2 * pp);
-                        r[2 * pp] = t2.x;
-                        r[2 * pp + 1] = t2.y;
-                    }
-#pragma unroll
-                    for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
-                }
-#pragma unroll
-                for (int oz = 0; oz < 2; ++oz) {
-                    const int az = oz + 2 * H - nz;
-                    if (az < 0 || az > 2 * H) continue;
-#pragma unroll
-                    for (int ox = 0; ox < 2; ++ox)
-#pragma unroll
-                        for (int ax = 0; ax < K; ++ax)
-#pragma unroll
-                            for (int ay = 0; ay < K; ++ay) {
-                                const float w = W[(az * K + ax) * K + ay];
-                                const int vx = ox + 2 * H - ax, vy = 2 * H - ay;
-                                acc2[oz * 2 + ox] =
-                                    ffma2(make_float2(w, w), make_float2(v[vx][vy], v[vx][vy + 1]), acc2[oz * 2 + ox]);
-                            }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[2 * i] = acc2[i].x;
-                acc[2 * i + 1] = acc2[i].y;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = Acc(0);
-#pragma unroll
-            for (int nz = N - 1; nz >= 0; --nz) {
-                Acc v[N][N];
-#pragma unroll
-                for (int nx = 0; nx < N; ++nx) {
-                    Acc r[2 * NP];
-#pragma unroll
-                    for (int pp = 0; pp < NP; ++pp) {  // exact: every float is a double
-                        const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * B::BX + nx) * B::BY + 2 * pp);
-                        r[2 * pp] = static_cast<Acc>(t2.x);
-                        r[2 * pp + 1] = static_cast<Acc>(t2.y);
-                    }
-#pragma unroll
-                    for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
-                }
-                // output (oz, ox, oy) reads neighbourhood cell (oz + 2H - az, ox + 2H - ax, oy + 2H - ay);
-                // planes stream from the top, so each output sees az ascending
-#pragma unroll
-                for (int oz = 0; oz < 2; ++oz) {
-                    const int az = oz + 2 * H - nz;
-                    if (az < 0 || az > 2 * H) continue;
-#pragma unroll
-                    for (int ox = 0; ox < 2; ++ox)
-#pragma unroll
-                        for (int oy = 0; oy < 2; ++oy)
-#pragma unroll
-                            for (int ax = 0; ax < K; ++ax)
-#pragma unroll
-                                for (int ay = 0; ay < K; ++ay)
-                                    acc[(oz * 2 + ox) * 2 + oy] =
-                                        fma_t<Acc>(W[(az * K + ax) * K + ay], v[ox + 2 * H - ax][oy + 2 * H - ay],
-                                                   acc[(oz * 2 + ox) * 2 + oy]);
-                }
-            }
-        }
+        apply_block<Acc, H, B::BX, B::BY, kPadY>(S, W, qz, qx, qy, acc);
         const uint8_t* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
 #pragma unroll
         for (int oz = 0; oz < 2; ++oz)
@@ -775,19 +927,102 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                 for (int oy = 0; oy < 2; ++oy) {
                     const int off = o[(oz * kTX + ox) * kTY + oy];
                     if (off == 0xff) continue;
-                    const uint32_t i = orow[(2 * qz + oz) * kTX + 2 * qx + ox] + off;
-                    const float r = to_f(acc[(oz * 2 + ox) * 2 + oy]);
-                    if (a.epi.mode == EPI_STORE) {
-                        a.out[i] = r;
-                    } else if (a.epi.mode == EPI_RL_RATIO) {
-                        // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
-                        const double bd = static_cast<double>(r);
-                        const double den = bd < a.epi.eps ? a.epi.eps : bd;
-                        a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
-                    } else {
-                        a.epi.est[i] = __fmul_rn(a.epi.est[i], r);  // deconv.hpp:102
-                    }
+                    store_out(a, orow[(2 * qz + oz) * kTX + 2 * qx + ox] + off, to_f(acc[(oz * 2 + ox) * 2 + oy]));
                 }
+    }
+}
+
+// Convolution of one tile through its resident gather map: the box is one
+// streamed pass over the record (4 codes per 16-byte load) with a gather of
+// each code's value, then the same block-compacted apply as k_conv_tile.
+// Results are bit-identical to k_conv_tile's (same box contents, same taps).
+template <typename Acc, int H>
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 6))
+    k_conv_map(const __grid_constant__ TileLaunch a) {
+    using M = MapBox<H>;
+    constexpr int K = 2 * H + 1, KW = K * K * K;
+    // dynamic: the box, the tile's map record, the zero + its flattened source values
+    extern __shared__ __align__(16) unsigned char map_smem[];
+    float* S = reinterpret_cast<float*>(map_smem);
+    uint32_t* Mb = reinterpret_cast<uint32_t*>(S + M::NC);
+    float* F = reinterpret_cast<float*>(Mb + M::REC);
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ Acc W[KW];
+    __shared__ uint8_t blist[kBlocks];
+    __shared__ int wcnt[2 * kTileThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
+    const int l = a.lvl[s];
+    const uint32_t tix = a.tile_base + blockIdx.x;
+    if (l >= a.slab_lc) {  // slab decomposition: only tiles touching this slab's planes
+        const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
+        const int sh = a.leaf.l_max - l;
+        if ((z0 + kTZ) << sh <= a.slab_zlo || z0 << sh >= a.slab_zhi) return;
+    }
+    const uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
+    // the record and the flattened source list stream in by two bulk copies
+    const uint32_t f0 = __ldg(a.flat_off + tix), nflat = __ldg(a.flat_off + tix + 1) - f0;
+    uint32_t* Fi = reinterpret_cast<uint32_t*>(F + kFlat0);
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        mbar_expect(&mbar, (M::REC + nflat) * 4);
+        bulk_copy(Mb, rec, M::REC * 4, &mbar);
+        if (nflat) bulk_copy(Fi, a.flat + f0, nflat * 4, &mbar);
+    }
+    if (tid < kFlat0) F[tid] = 0.0f;
+    for (int i = tid; i < KW; i += kTileThreads)
+        W[i] = sizeof(Acc) == 8 ? static_cast<Acc>(a.wd[a.woff[s] + i]) : static_cast<Acc>(a.wf[a.woff[s] + i]);
+    __syncthreads();  // (the barrier's init is visible)
+    mbar_wait(&mbar, 0);
+    // every source value copied once, in place over its list entry (entry q is
+    // read and overwritten by the same thread); a warp's entries are mostly
+    // consecutive particles
+    for (uint32_t q = tid; q < nflat; q += kTileThreads) {
+        const uint32_t g = Fi[q];
+        cp_async4(Fi + q, ((g >> 31) ? a.tval : a.val) + (g & 0x7fffffffu));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // the box: 8 cells per step, values from F (shared memory only)
+    {
+        const uint4* c4 = reinterpret_cast<const uint4*>(Mb);
+        float4* S4 = reinterpret_cast<float4*>(S);
+        for (int i = tid; i < M::NC / 8; i += kTileThreads) {
+            const uint4 c = c4[i];
+            S4[2 * i] = make_float4(F[c.x & 0xffffu], F[c.x >> 16], F[c.y & 0xffffu], F[c.y >> 16]);
+            S4[2 * i + 1] = make_float4(F[c.z & 0xffffu], F[c.z >> 16], F[c.w & 0xffffu], F[c.w >> 16]);
+        }
+    }
+    __syncthreads();
+    const uint32_t* omask = Mb + M::NC / 2;
+    const uint32_t* ofirst = omask + kTZ * kTX;
+    const int nb = compact_blocks(
+        [&](int b) {
+            const int qz = b / (kBlocks / 4), qx = (b / (kTY / 2)) & 3, qy = b & (kTY / 2 - 1);
+            const int r = 2 * qz * kTX + 2 * qx;
+            const uint32_t m = omask[r] | omask[r + 1] | omask[r + kTX] | omask[r + kTX + 1];
+            return ((m >> (2 * qy)) & 3u) != 0;
+        },
+        blist, wcnt);
+    __syncthreads();
+    for (int q = tid; q < nb; q += kTileThreads) {
+        const int bidx = blist[q];
+        const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
+        Acc acc[8];
+        apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+#pragma unroll
+        for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+            for (int ox = 0; ox < 2; ++ox) {
+                const int r = (2 * qz + oz) * kTX + 2 * qx + ox;
+                const uint32_t m = omask[r];
+#pragma unroll
+                for (int oy = 0; oy < 2; ++oy) {
+                    const int y = 2 * qy + oy;
+                    if (!((m >> y) & 1u)) continue;
+                    store_out(a, ofirst[r] + __popc(m & ((1u << y) - 1u)), to_f(acc[(oz * 2 + ox) * 2 + oy]));
+                }
+            }
     }
 }
 
@@ -908,17 +1143,140 @@ void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
     L.tile_runs[H - 1] = runs;
 }
 
-template <typename Acc, int H>
+// per tile: its flattened source count (sum of its run lengths), padded to 4
+__global__ void k_tile_nflat(const uint32_t* __restrict__ run_off, const uint2* __restrict__ runs, uint64_t n,
+                             uint32_t* __restrict__ counts) {
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t c = 0;
+        for (uint32_t j = run_off[t]; j < run_off[t + 1]; ++j) c += runs[j].y >> 16;
+        counts[t] = (c + 3) & ~3u;
+    }
+}
+
+// The flattened source lists' layout for half-width H (allocated zeroed; the
+// map build writes them).
+template <int H>
+void ensure_tile_flat(aprgpu_apr* apr, cudaStream_t s) {
+    DevAccess& L = apr->leaf;
+    if (L.tile_flat[H - 1]) return;
+    const uint64_t n = L.tile_off[L.l_max + 1];
+    uint32_t* off = nullptr;
+    APR_CUDA(cudaMalloc(&off, 4 * (n + 1)));
+    GpuBuf counts, temp;
+    counts.ensure(4 * (n + 1));
+    APR_CUDA(cudaMemsetAsync(counts.p, 0, 4 * (n + 1), s));
+    if (n) {
+        k_tile_nflat<<<std::min<unsigned>(blocks_for(n, 256), apr->ctx->sm_count * 8), 256, 0, s>>>(
+            L.tile_run_off[H - 1], L.tile_runs[H - 1], n, counts.as<uint32_t>());
+        count_launch(apr->ctx);
+        APR_CUDA(cudaGetLastError());
+    }
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.as<uint32_t>(), off, static_cast<int64_t>(n + 1), s);
+    temp.ensure(tb + 16);
+    tb = temp.bytes;
+    APR_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, counts.as<uint32_t>(), off, static_cast<int64_t>(n + 1), s));
+    count_launch(apr->ctx);
+    uint32_t total = 0;
+    APR_CUDA(cudaMemcpyAsync(&total, off + n, 4, cudaMemcpyDeviceToHost, s));
+    APR_CUDA(cudaStreamSynchronize(s));
+    uint32_t* flat = nullptr;
+    APR_CUDA(cudaMalloc(&flat, 4ull * total + 16));
+    APR_CUDA(cudaMemsetAsync(flat, 0, 4ull * total + 16, s));  // padding entries: particle 0
+    L.tile_flat_off[H - 1] = off;
+    L.tile_flat[H - 1] = flat;
+}
+
+template <typename Acc, int H, bool MAP = false>
 void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
     constexpr int bytes = Box<H>::NC * static_cast<int>(sizeof(float));
     static const bool attr = [] {
-        APR_CUDA(cudaFuncSetAttribute(k_conv_tile<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        APR_CUDA(cudaFuncSetAttribute(k_conv_tile<Acc, H, MAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         return true;
     }();
     (void)attr;
-    k_conv_tile<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
+    k_conv_tile<Acc, H, MAP><<<n, kTileThreads, bytes, s>>>(a);
     count_launch(ctx);
     APR_CUDA(cudaGetLastError());
+}
+
+template <typename Acc, int H>
+void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
+    constexpr int bytes = (MapBox<H>::NC + MapBox<H>::REC + MapBox<H>::NF) * 4;
+    static const bool attr = [] {
+        APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        return true;
+    }();
+    (void)attr;
+    k_conv_map<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
+    count_launch(ctx);
+    APR_CUDA(cudaGetLastError());
+}
+
+// APRGPU_TILE_MAP=0: no resident gather maps (every call reconstructs its boxes)
+bool maps_enabled() {
+    const char* e = std::getenv("APRGPU_TILE_MAP");
+    return !(e && e[0] == '0');
+}
+
+// The gather maps of launch b's levels for half-width H and pad mode: built on
+// first use (one map-mode launch of k_conv_tile), kept with the APR.  Returns
+// false -- the caller reconstructs -- when the missing maps would take more
+// than half of the free device memory.
+template <int H>
+bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, cudaStream_t s) {
+    DevAccess& L = apr->leaf;
+    const int pm = pad == APRGPU_PAD_ZERO ? 1 : 0;
+    auto rec_bytes = [&](int l) { return (L.tile_off[l + 1] - L.tile_off[l]) * MapBox<H>::REC * sizeof(uint32_t); };
+    for (int i = 0; i < b.n_levels; ++i)
+        if (L.tile_map_fail[H - 1][pm][b.lvl[i]]) return false;
+    auto missing = [&] {
+        size_t need = 0;
+        for (int i = 0; i < b.n_levels; ++i)
+            if (!L.tile_map[H - 1][pm][b.lvl[i]]) need += rec_bytes(b.lvl[i]);
+        return need;
+    };
+    if (missing()) {
+        std::lock_guard<std::mutex> lk(apr->ctx->mu);
+        const size_t need = missing();
+        if (need) {
+            size_t free_b = 0, total_b = 0;
+            APR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (need > free_b / 2) {
+                for (int i = 0; i < b.n_levels; ++i) L.tile_map_fail[H - 1][pm][b.lvl[i]] = 1;
+                return false;
+            }
+            ensure_tile_flat<H>(apr, s);
+            for (int i = 0; i < b.n_levels; ++i)
+                if (!L.tile_map[H - 1][pm][b.lvl[i]]) APR_CUDA(cudaMalloc(&L.tile_map[H - 1][pm][b.lvl[i]], rec_bytes(b.lvl[i])));
+            TileLaunch m = b;
+            for (int i = 0; i < b.n_levels; ++i) m.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
+            m.flat = L.tile_flat[H - 1];
+            m.flat_off = L.tile_flat_off[H - 1];
+            m.slab_lc = 1 << 20;  // every tile: a map serves every slab
+            GpuBuf flag;
+            flag.ensure(16);
+            APR_CUDA(cudaMemsetAsync(flag.p, 0, 4, s));
+            m.map_overflow = flag.as<int>();
+            launch_tiles<float, H, true>(apr->ctx, m, total, s);
+            int over = 0;
+            APR_CUDA(cudaMemcpyAsync(&over, flag.p, 4, cudaMemcpyDeviceToHost, s));
+            APR_CUDA(cudaStreamSynchronize(s));
+            if (over) {  // some tile has too many sources for k_conv_map: reconstruct these levels
+                for (int i = 0; i < b.n_levels; ++i) {
+                    cudaFree(L.tile_map[H - 1][pm][b.lvl[i]]);
+                    L.tile_map[H - 1][pm][b.lvl[i]] = nullptr;
+                    L.tile_map_fail[H - 1][pm][b.lvl[i]] = 1;
+                }
+                return false;
+            }
+        }
+    }
+    for (int i = 0; i < b.n_levels; ++i) b.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
+    b.flat = L.tile_flat[H - 1];
+    b.flat_off = L.tile_flat_off[H - 1];
+    return true;
 }
 
 }  // namespace
@@ -1037,7 +1395,15 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
             }
             if (!total) continue;
             b.tile_base = static_cast<uint32_t>(L.tile_off[first]);
-            if (H == 1) {
+            const bool map = maps_enabled() && (H == 1 ? ensure_tile_maps<1>(apr, b, total, pad, s)
+                                                       : ensure_tile_maps<2>(apr, b, total, pad, s));
+            if (map) {
+                if (H == 1) {
+                    if (exact) launch_map<double, 1>(apr->ctx, b, total, s); else launch_map<float, 1>(apr->ctx, b, total, s);
+                } else {
+                    if (exact) launch_map<double, 2>(apr->ctx, b, total, s); else launch_map<float, 2>(apr->ctx, b, total, s);
+                }
+            } else if (H == 1) {
                 if (exact) launch_tiles<double, 1>(apr->ctx, b, total, s); else launch_tiles<float, 1>(apr->ctx, b, total, s);
             } else {
                 if (exact) launch_tiles<double, 2>(apr->ctx, b, total, s); else launch_tiles<float, 2>(apr->ctx, b, total, s);

@@ -44,6 +44,15 @@ void DevAccess::release() {
         cudaFree(tile_run_off[h]);
         tile_runs[h] = nullptr;
         tile_run_off[h] = nullptr;
+        cudaFree(tile_flat[h]);
+        cudaFree(tile_flat_off[h]);
+        tile_flat[h] = nullptr;
+        tile_flat_off[h] = nullptr;
+        for (int pm = 0; pm < 2; ++pm)
+            for (int l = 0; l < kMaxLevels; ++l) {
+                cudaFree(tile_map[h][pm][l]);
+                tile_map[h][pm][l] = nullptr;
+            }
     }
     y = nullptr;
     rb = nullptr;

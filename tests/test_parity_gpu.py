@@ -76,8 +76,16 @@ def test_fill_tree_bit_exact(name):
     assert np.array_equal(G.bits(tv), G.bits(d["tree_values"]))
 
 
+@pytest.fixture(params=["map", "reconstruct"])
+def tile_path(request, monkeypatch):
+    """Both box-tile paths: the resident gather map (default) and the per-call
+    reconstruction (APRGPU_TILE_MAP=0, conv_tile.cu)."""
+    monkeypatch.setenv("APRGPU_TILE_MAP", "1" if request.param == "map" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("name", STRUCT_CASES)
-def test_convolve_exact_bit_identical_to_reference(name):
+def test_convolve_exact_bit_identical_to_reference(name, tile_path):
     d = G.load(name)
     apr = G.product_apr(d)
     for c in G.conv_names(d):
@@ -101,6 +109,25 @@ def test_convolve_fast_within_tolerance(name):
         # (2197 cancelling fp32 terms)
         tol = 1e-5 if c.startswith("g") else (1e-3 if "13" in c else 1e-4)
         assert rel_err(out, d[f"conv_{c}_out"]) <= tol, c
+
+
+@pytest.mark.parametrize("name", ["spheres64", "c1_256", "dense16", "blobs32_0"] + G.names("random_apr_*")[::4])
+def test_map_and_reconstruction_paths_bit_identical(name, monkeypatch):
+    d = G.load(name)
+    apr = G.product_apr(d)
+    rng = np.random.default_rng(7)
+    v = rng.uniform(0, 1000, d["values"].size).astype(np.float32)
+    tv = P.fill_tree(apr, v)
+    for k in (3, 5):
+        w = P.Stencil(k, k, k, weights=rng.uniform(0, 1, k ** 3))
+        pyr = P.make_pyramid(w, apr.access.l_min, apr.access.l_max, P.PyramidMode.Restricted)
+        for pad in (P.PadMode.Zero, P.PadMode.Reflect):
+            for accum in ("exact", "fast"):
+                out = {}
+                for path in ("1", "0"):
+                    monkeypatch.setenv("APRGPU_TILE_MAP", path)
+                    out[path] = P.convolve_apr(apr, v, tv, pyr, pad, P.ConvolveOptions(accum=accum))
+                assert np.array_equal(G.bits(out["1"]), G.bits(out["0"])), (k, pad, accum)
 
 
 @pytest.mark.parametrize("name", ["rl_spheres64"])
