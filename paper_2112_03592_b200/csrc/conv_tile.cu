@@ -124,8 +124,12 @@ template <int H>
 struct MapBox {
     static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * H;
     static constexpr int NC = BZ * BX * BY;
-    static_assert(NC % 8 == 0, "whole 16-byte code groups");
-    static constexpr int REC = NC / 2 + 2 * kTZ * kTX;  // 32-bit words per record
+    // codes in 128-cell chunks, lane-transposed: word pair 32k + i of chunk k
+    // holds cells 128k + i + 32j (j = 0..3), so a warp's reads of F for one j
+    // are consecutive cells (consecutive / repeated sources: no bank conflicts)
+    static constexpr int NCH = (NC + 127) / 128, NCP = NCH * 128;
+    static constexpr int CW = NCP / 2;                  // code words
+    static constexpr int REC = CW + 2 * kTZ * kTX;      // 32-bit words per record
     static constexpr uint32_t ZERO = 0;
     static constexpr int NF = kFlat0 + ((NC + 3) & ~3);  // F entries
 };
@@ -880,10 +884,15 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
         if (tid == 0 && roff[nruns] > M::NC) atomicOr(a.map_overflow, 1);
         auto code = [&](int c) -> uint32_t {
+            if (c >= M::NC) return M::ZERO;
             const int r = c / M::BY;
             return __float_as_uint(S[r * B::BY + (c - r * M::BY) + (kPadY - H)]);
         };
-        for (int u = tid; u < M::NC / 2; u += kTileThreads) rec[u] = code(2 * u) | code(2 * u + 1) << 16;
+        for (int u = tid; u < M::NCH * 32; u += kTileThreads) {
+            const int c = (u >> 5) * 128 + (u & 31);
+            rec[2 * u] = code(c) | code(c + 32) << 16;
+            rec[2 * u + 1] = code(c + 64) | code(c + 96) << 16;
+        }
         if (tid < kTZ * kTX) {  // per inner row: output mask over y0 .. y0+31 and the first output's index
             uint32_t m = 0;
             int first = -1;
@@ -893,8 +902,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                 m |= 1u << y;
                 if (first < 0) first = o;
             }
-            rec[M::NC / 2 + tid] = m;
-            rec[M::NC / 2 + kTZ * kTX + tid] = m ? orow[tid] + first : 0u;
+            rec[M::CW + tid] = m;
+            rec[M::CW + kTZ * kTX + tid] = m ? orow[tid] + first : 0u;
         }
         return;
     }
@@ -944,7 +953,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     // dynamic: the box, the tile's map record, the zero + its flattened source values
     extern __shared__ __align__(16) unsigned char map_smem[];
     float* S = reinterpret_cast<float*>(map_smem);
-    uint32_t* Mb = reinterpret_cast<uint32_t*>(S + M::NC);
+    uint32_t* Mb = reinterpret_cast<uint32_t*>(S + M::NCP);
     float* F = reinterpret_cast<float*>(Mb + M::REC);
     __shared__ __align__(8) uint64_t mbar;
     __shared__ Acc W[KW];
@@ -983,18 +992,21 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     }
     cp_async_wait_all();
     __syncthreads();
-    // the box: 8 cells per step, values from F (shared memory only)
+    // the box, from F (shared memory only)
     {
-        const uint4* c4 = reinterpret_cast<const uint4*>(Mb);
-        float4* S4 = reinterpret_cast<float4*>(S);
-        for (int i = tid; i < M::NC / 8; i += kTileThreads) {
-            const uint4 c = c4[i];
-            S4[2 * i] = make_float4(F[c.x & 0xffffu], F[c.x >> 16], F[c.y & 0xffffu], F[c.y >> 16]);
-            S4[2 * i + 1] = make_float4(F[c.z & 0xffffu], F[c.z >> 16], F[c.w & 0xffffu], F[c.w >> 16]);
+        const uint2* c2 = reinterpret_cast<const uint2*>(Mb);
+        const int lane = tid & 31;
+        for (int u = tid; u < M::NCH * 32; u += kTileThreads) {
+            const uint2 c = c2[u];
+            float* dst = S + (u >> 5) * 128 + lane;
+            dst[0] = F[c.x & 0xffffu];
+            dst[32] = F[c.x >> 16];
+            dst[64] = F[c.y & 0xffffu];
+            dst[96] = F[c.y >> 16];
         }
     }
     __syncthreads();
-    const uint32_t* omask = Mb + M::NC / 2;
+    const uint32_t* omask = Mb + M::CW;
     const uint32_t* ofirst = omask + kTZ * kTX;
     const int nb = compact_blocks(
         [&](int b) {
@@ -1203,7 +1215,7 @@ void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t
 
 template <typename Acc, int H>
 void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
-    constexpr int bytes = (MapBox<H>::NC + MapBox<H>::REC + MapBox<H>::NF) * 4;
+    constexpr int bytes = (MapBox<H>::NCP + MapBox<H>::REC + MapBox<H>::NF) * 4;
     static const bool attr = [] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         return true;
