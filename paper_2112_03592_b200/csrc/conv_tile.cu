@@ -113,8 +113,10 @@ struct Box {
 // one 16-bit code per cell -- kFlat0 + the index of its source particle in the
 // tile's flattened source list (the concatenation of its source runs,
 // k_tile_runs), ZERO for a zero cell -- then per inner row an output mask over
-// y0 .. y0+kTY-1 and the index of its first output particle.  The flattened
-// source list itself (particle | interior << 31 per entry, padded to 4) lives
+// y0 .. y0+kTY-1 and the index of its first output particle, then the number
+// of leaf sources (the list holds the leaf runs' particles, then the interior
+// runs' nodes, so each part copies from one base pointer).  The flattened
+// source list itself (particle or node index per entry, padded to 4) lives
 // in DevAccess::tile_flat, shared by both pad modes.  In a valid APR every box
 // cell has one source, so a tile has at most NC sources (the build checks; a
 // malformed APR's overlapping sources can exceed it, and its levels then
@@ -129,7 +131,7 @@ struct MapBox {
     // are consecutive cells (consecutive / repeated sources: no bank conflicts)
     static constexpr int NCH = (NC + 127) / 128, NCP = NCH * 128;
     static constexpr int CW = NCP / 2;                  // code words
-    static constexpr int REC = CW + 2 * kTZ * kTX;      // 32-bit words per record
+    static constexpr int REC = CW + 2 * kTZ * kTX + 4;  // 32-bit words per record (+ nleaf, pad)
     static constexpr uint32_t ZERO = 0;
     static constexpr int NF = kFlat0 + ((NC + 3) & ~3);  // F entries
 };
@@ -755,7 +757,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         const int yy = __ldg((is_tree ? a.tree.y : a.leaf.y) + gi);
         float v;
         if constexpr (MAP) {
-            if (p < MapBox<H>::NC) a.flat[flat0 + p] = gi | static_cast<uint32_t>(is_tree) << 31;
+            if (p < MapBox<H>::NC) a.flat[flat0 + p] = gi;
             v = __uint_as_float(static_cast<uint32_t>(kFlat0 + p));
         } else {
             v = __ldg((is_tree ? a.tval : a.val) + gi);
@@ -905,6 +907,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
             rec[M::CW + tid] = m;
             rec[M::CW + kTZ * kTX + tid] = m ? orow[tid] + first : 0u;
         }
+        if (tid == 0) {  // runs are in row-slot order: interior rows come last
+            int j = 0;
+            while (j < nruns && !((rinfo[j] >> 5) & 1u)) ++j;
+            rec[M::CW + 2 * kTZ * kTX] = static_cast<uint32_t>(roff[j]);
+            rec[M::CW + 2 * kTZ * kTX + 1] = rec[M::CW + 2 * kTZ * kTX + 2] = rec[M::CW + 2 * kTZ * kTX + 3] = 0u;
+        }
         return;
     }
 
@@ -986,9 +994,11 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     // every source value copied once, in place over its list entry (entry q is
     // read and overwritten by the same thread); a warp's entries are mostly
     // consecutive particles
-    for (uint32_t q = tid; q < nflat; q += kTileThreads) {
-        const uint32_t g = Fi[q];
-        cp_async4(Fi + q, ((g >> 31) ? a.tval : a.val) + (g & 0x7fffffffu));
+    {
+        const uint32_t nleaf = Mb[M::CW + 2 * kTZ * kTX];
+        uint32_t q = tid;
+        for (; q < nleaf; q += kTileThreads) cp_async4(Fi + q, a.val + Fi[q]);
+        for (; q < nflat; q += kTileThreads) cp_async4(Fi + q, a.tval + Fi[q]);
     }
     cp_async_wait_all();
     __syncthreads();

@@ -70,7 +70,7 @@ struct DevAccess {
     uint32_t* tile_run_off[2] = {nullptr, nullptr};  // n_tiles + 1 offsets into tile_runs
     // resident gather maps of the box-tile kernel, [H-1][pad][level] (lazy; conv_tile.cu)
     uint32_t* tile_map[2][2][kMaxLevels] = {};
-    // per H: every tile's flattened sources (particle | interior << 31), tiles padded to 4
+    // per H: every tile's flattened sources (leaf particles, then interior nodes), tiles padded to 4
     uint32_t* tile_flat[2] = {nullptr, nullptr};
     uint32_t* tile_flat_off[2] = {nullptr, nullptr};  // n_tiles + 1 offsets into tile_flat
     uint8_t tile_map_fail[2][2][kMaxLevels] = {};  // a level that reconstructs (no map)
