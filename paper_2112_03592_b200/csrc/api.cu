@@ -89,7 +89,7 @@ void upload_one(aprgpu_ctx* ctx, const aprgpu_access_desc* d, aprgpu::DevAccess&
 void free_apr(aprgpu_apr* apr) {
     apr->leaf.release();
     apr->tree.release();
-    for (aprgpu::GpuBuf* b : {&apr->vsum, &apr->wsum, &apr->h_in, &apr->h_tree, &apr->h_out, &apr->rl_u,
+    for (aprgpu::GpuBuf* b : {&apr->vsum, &apr->wsum, &apr->tree_links, &apr->h_in, &apr->h_tree, &apr->h_out, &apr->rl_u,
                               &apr->rl_ratio, &apr->rl_tv, &apr->tmp, &apr->built_values})
         b->release();
 }

@@ -159,9 +159,11 @@ __device__ __forceinline__ Geo make_geo(int l, uint32_t id, int txd, int tyd, co
     return G;
 }
 
+// Level segment of launch block b.  Searched from the last segment: levels run
+// coarse to fine, so most blocks (the finest level's) resolve at once.
 __device__ __forceinline__ int seg_of(const uint32_t* seg_end, int n, uint32_t b) {
-    int s = 0;
-    while (s + 1 < n && b >= seg_end[s]) ++s;
+    int s = n - 1;
+    while (s > 0 && b < seg_end[s - 1]) --s;
     return s;
 }
 

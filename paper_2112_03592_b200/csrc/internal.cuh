@@ -103,6 +103,7 @@ struct aprgpu_apr {
     aprgpu::DevAccess leaf, tree;
     // scratch (grown on demand)
     aprgpu::GpuBuf vsum, wsum;             // fill_tree fp64 sums [n_tree]
+    aprgpu::GpuBuf tree_links;             // per interior node, its children (tree.cu); lazy
     aprgpu::GpuBuf h_in, h_tree, h_out;    // staging for host-pointer calls
     aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
     aprgpu::GpuBuf tmp;                    // misc

@@ -157,6 +157,23 @@ __device__ __forceinline__ double footprint_dev(int l, int iz, int ix, int iy, i
     return __dmul_rn(__dmul_rn(dz, dx), dy);
 }
 
+// Child links of an interior node, one word per child row k (k = 0..3: leaf
+// rows (2pz + k/2, 2px + k%2); k = 4..7: the interior rows): b | f0 << 30 |
+// f1 << 31, b = lower_bound of 2py in the child row, f0 / f1 = children
+// y = 2py / 2py + 1 present (at b and b + f0).  Structure only: built once per
+// APR (the searches of synchronized_parent_pass, tree.hpp:88-103), then every
+// fill is a gather.
+struct Links {
+    uint4 leaf, tree;
+};
+__device__ __forceinline__ uint32_t link_of(const uint16_t* y, uint32_t b, uint32_t e, int y0) {
+    if (e <= b) return 0;
+    const uint32_t i = lower_bound_u16(y, b, e, y0);
+    const uint32_t f0 = (i < e && y[i] == y0) ? 1u : 0u;
+    const uint32_t f1 = (i + f0 < e && y[i + f0] == y0 + 1) ? 1u : 0u;
+    return i | f0 << 30 | f1 << 31;
+}
+
 struct FillArgs {
     AccessView leaf, tree;
     const float* leaf_v;
@@ -167,8 +184,10 @@ struct FillArgs {
     int lt, c, leaf_ok, tree_ok;  // c = lt+1; children are leaves / interior nodes
     int czd, cxd, glm, nz, nx, ny;
     int pz_lo, pz_hi;  // parent rows processed: z in [pz_lo, pz_hi) (slab decomposition)
+    Links* links;  // per interior node (written by the BUILD pass)
 };
 
+template <bool BUILD>
 __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -208,33 +227,47 @@ __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
         for (uint32_t j = pb + lane; j < pe; j += 32) {
             const int py = a.tree.y[j];
             const int y0 = 2 * py;
+            if (BUILD) {
+                uint32_t w[8];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    w[k] = link_of(a.leaf.y, rbk[k], rek[k], y0);
+                    w[k + 4] = link_of(a.tree.y, rbk[k + 4], rek[k + 4], y0);
+                }
+                a.links[j] = Links{make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7])};
+                continue;
+            }
+            const Links lk = a.links[j];
+            const uint32_t wl[4] = {lk.leaf.x, lk.leaf.y, lk.leaf.z, lk.leaf.w};
+            const uint32_t wt[4] = {lk.tree.x, lk.tree.y, lk.tree.z, lk.tree.w};
             double vs = 0.0, ws = 0.0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int cz = 2 * pz + (k >> 1), cx = 2 * px + (k & 1);
                 // leaf children (tree.hpp:124-132): w * value, w = clipped footprint
-                if (rek[k] > rbk[k]) {
-                    uint32_t i = lower_bound_u16(a.leaf.y, rbk[k], rek[k], y0);
-                    for (int t = 0; t < 2 && i < rek[k]; ++t) {
-                        const int yy = a.leaf.y[i];
-                        if (yy == y0 + t) {
-                            const double w = footprint_dev(a.c, cz, cx, yy, a.glm, a.nz, a.nx, a.ny);
-                            vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[i])));
-                            ws = __dadd_rn(ws, w);
-                            ++i;
-                        }
+                {
+                    const uint32_t b = wl[k] & 0x3fffffffu, f0 = (wl[k] >> 30) & 1u, f1 = wl[k] >> 31;
+                    if (f0) {
+                        const double w = footprint_dev(a.c, cz, cx, y0, a.glm, a.nz, a.nx, a.ny);
+                        vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b])));
+                        ws = __dadd_rn(ws, w);
+                    }
+                    if (f1) {
+                        const double w = footprint_dev(a.c, cz, cx, y0 + 1, a.glm, a.nz, a.nx, a.ny);
+                        vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b + f0])));
+                        ws = __dadd_rn(ws, w);
                     }
                 }
                 // interior children (tree.hpp:133-139): their own fp64 sums
-                if (rek[k + 4] > rbk[k + 4]) {
-                    uint32_t i = lower_bound_u16(a.tree.y, rbk[k + 4], rek[k + 4], y0);
-                    for (int t = 0; t < 2 && i < rek[k + 4]; ++t) {
-                        const int yy = a.tree.y[i];
-                        if (yy == y0 + t) {
-                            vs = __dadd_rn(vs, a.vsum[i]);
-                            ws = __dadd_rn(ws, a.wsum[i]);
-                            ++i;
-                        }
+                {
+                    const uint32_t b = wt[k] & 0x3fffffffu, f0 = (wt[k] >> 30) & 1u, f1 = wt[k] >> 31;
+                    if (f0) {
+                        vs = __dadd_rn(vs, a.vsum[b]);
+                        ws = __dadd_rn(ws, a.wsum[b]);
+                    }
+                    if (f1) {
+                        vs = __dadd_rn(vs, a.vsum[b + f0]);
+                        ws = __dadd_rn(ws, a.wsum[b + f0]);
                     }
                 }
             }
@@ -418,6 +451,30 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
     a.nz = apr->dims[0];
     a.nx = apr->dims[1];
     a.ny = apr->dims[2];
+    const bool build = !apr->tree_links.p;
+    if (build) {
+        if (L.n_particles >= (1ull << 30) || T.n_particles >= (1ull << 30))
+            fail(APRGPU_ERR_CAPABILITY, "fill_tree: child links need fewer than 2^30 particles per access");
+        apr->tree_links.ensure(sizeof(Links) * T.n_particles);
+    }
+    a.links = apr->tree_links.as<Links>();
+    // first use: the links of every level (no slab restriction: they serve every slab)
+    for (int lt = build ? T.l_max : -1; lt >= T.l_min; --lt) {
+        a.lt = lt;
+        a.c = lt + 1;
+        a.leaf_ok = (a.c >= L.l_min && a.c <= L.l_max) ? 1 : 0;
+        a.tree_ok = (a.c <= T.l_max) ? 1 : 0;
+        a.czd = grid_dim_dev(a.nz, a.glm, a.c);
+        a.cxd = grid_dim_dev(a.nx, a.glm, a.c);
+        a.pz_lo = 0;
+        a.pz_hi = 1 << 30;
+        a.work = T.work + T.work_off[lt];
+        a.n_work = T.work_off[lt + 1] - T.work_off[lt];
+        if (a.n_work == 0) continue;
+        const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), ctx->sm_count * 16);
+        k_fill_tree_level<true><<<grid, 256, 0, s>>>(a);
+        count_launch(ctx);
+    }
     for (int lt = std::min(lt_hi, T.l_max); lt >= std::max(lt_lo, T.l_min); --lt) {
         a.lt = lt;
         a.c = lt + 1;
@@ -431,7 +488,7 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
         a.n_work = T.work_off[lt + 1] - T.work_off[lt];
         if (a.n_work == 0) continue;
         const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), ctx->sm_count * 16);
-        k_fill_tree_level<<<grid, 256, 0, s>>>(a);
+        k_fill_tree_level<false><<<grid, 256, 0, s>>>(a);
         count_launch(ctx);
     }
     APR_CUDA(cudaGetLastError());
