@@ -148,7 +148,27 @@ __device__ __forceinline__ int low_bit_exp(float v) {  // exponent of the lowest
     return (e ? e : 1) - 150 + __ffs(static_cast<int>(m)) - 1;
 }
 
-__global__ void k_mean_bound(const float* __restrict__ u, uint64_t n, MeanStats* st) {
+// block reductions: one atomic per block (a per-thread fp64 / int64 atomic on
+// one address serialises the whole grid)
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < static_cast<int>(blockDim.x >> 5) ? sh[lane] : sh[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+    __syncthreads();
+    return v;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(256) k_mean_bound(const float* __restrict__ u, uint64_t n, MeanStats* st) {
+    __shared__ double shd[8];
+    __shared__ int shi[8];
     double as = 0.0;
     int gmin = kNoLowBit;
     int bad = 0;
@@ -161,19 +181,26 @@ __global__ void k_mean_bound(const float* __restrict__ u, uint64_t n, MeanStats*
         as += fabs(static_cast<double>(v));
         if (v != 0.0f) gmin = min(gmin, low_bit_exp(v));
     }
-    atomicAdd(&st->abs_sum, as);
-    if (gmin != kNoLowBit) atomicMax(&st->neg_gexp_max, kNoLowBit - gmin);
-    if (bad) atomicOr(&st->nonfinite, 1);
+    as = block_reduce(as, [](double x, double y) { return x + y; }, shd);
+    gmin = block_reduce(gmin, [](int x, int y) { return min(x, y); }, shi);
+    bad = block_reduce(bad, [](int x, int y) { return x | y; }, shi);
+    if (threadIdx.x == 0) {
+        atomicAdd(&st->abs_sum, as);  // (order-free: only compared against a bound with margin)
+        if (gmin != kNoLowBit) atomicMax(&st->neg_gexp_max, kNoLowBit - gmin);
+        if (bad) atomicOr(&st->nonfinite, 1);
+    }
 }
 
-__global__ void k_mean_exact(const float* __restrict__ u, uint64_t n, MeanStats* st) {
+__global__ void __launch_bounds__(256) k_mean_exact(const float* __restrict__ u, uint64_t n, MeanStats* st) {
+    __shared__ long long shl[8];
     if (st->nonfinite || st->neg_gexp_max == 0) return;
     const int g = kNoLowBit - st->neg_gexp_max;
     if (!(st->abs_sum < ldexp(1.0, 53 + g) * 0.999999)) return;
     long long acc = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         acc += static_cast<long long>(ldexp(static_cast<double>(u[i]), -g));  // exact: |v / 2^g| < 2^53
-    atomicAdd(&st->isum, static_cast<unsigned long long>(acc));
+    acc = block_reduce(acc, [](long long x, long long y) { return x + y; }, shl);  // integer: order-free
+    if (threadIdx.x == 0) atomicAdd(&st->isum, static_cast<unsigned long long>(acc));
 }
 
 }  // namespace
