@@ -113,6 +113,26 @@ int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, u
  * accumulation in the reference's per-parent order, bit-exact. */
 int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream);
 
+/* ---- dense reconstruction (reconstruct.hpp:73-129) ------------------------- */
+/* Patch window of reconstruct_patch (PatchSpec, reconstruct.hpp:28-35): level-l
+ * cells z in [z_begin, z_end), x in [x_begin, x_end), the full y span, pad cells
+ * per side filled by pad_mode (APRGPU_PAD_ZERO / APRGPU_PAD_REFLECT). */
+typedef struct {
+    int level, z_begin, z_end, x_begin, x_end, pad, pad_mode;
+} aprgpu_patch_spec;
+
+/* reconstruct_level (reconstruct.hpp:73-84): out[z_dim(l) * x_dim(l) * y_dim(l)],
+ * (z, x, y) at (z * x_dim + x) * y_dim + y.  Every cell takes its covering leaf's
+ * value (fill_level_row, :41-69), or with tree_values its level-l interior
+ * node's; tree_values NULL writes no interior nodes (reconstruct_full is
+ * level l_max with NULL).  RANGE: level outside [l_min, l_max]. */
+int aprgpu_reconstruct_level(aprgpu_apr* apr, const float* values, const float* tree_values, int level, float* out,
+                             int ptr_kind, void* stream);
+/* reconstruct_patch (reconstruct.hpp:94-129): out[(z_end - z_begin + 2 pad) *
+ * (x_end - x_begin + 2 pad) * (y_dim(l) + 2 pad)].  RANGE: spec outside the grid. */
+int aprgpu_reconstruct_patch(aprgpu_apr* apr, const float* values, const float* tree_values,
+                             const aprgpu_patch_spec* spec, float* out, int ptr_kind, void* stream);
+
 /* ---- stencils (host) ------------------------------------------------------ */
 /* restrict_stencil (stencil.hpp:127-160).  out_k3 gets the restricted extents;
  * out (may be NULL to query) gets the weights, bit-identical to the reference

@@ -251,3 +251,11 @@ inline LinearAccess download(aprgpu_apr* h, int which) {
 
 }  // namespace gpu
 }  // namespace aprkit
+
+// The reconstruct.hpp drop-in (include/aprkit_gpu/aprkit/reconstruct.hpp) is
+// pulled in by this header's own #include of "aprkit/reconstruct.hpp", before
+// the runtime above exists; its device implementations follow here.
+#define APRKIT_GPU_RUNTIME_DONE 1
+#ifdef APRKIT_GPU_RECONSTRUCT_OVERLAY
+#include "aprkit_gpu_reconstruct.hpp"
+#endif

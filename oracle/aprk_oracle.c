@@ -282,6 +282,36 @@ void orc_reconstruct_level(const orc_access* leaf, const float* values, const or
             orc_fill_level_row(leaf, values, tree, tree_values, l, z, x, out + ((size_t)z * xd + x) * yd, 0, yd);
 }
 
+void orc_reconstruct_patch(const orc_access* leaf, const float* values, const orc_access* tree,
+                           const float* tree_values, const int spec[7], float* out) {
+    /* reconstruct.hpp:94-129; spec = level, z_begin, z_end, x_begin, x_end, pad,
+     * pad_mode (0 Zero, 1 Reflect).  The caller checks the spec. */
+    const int l = spec[0], pad = spec[5], zero = spec[6] == 0;
+    const int zd = leaf->z_dim[l], xd = leaf->x_dim[l], yd = leaf->y_dim[l];
+    const int onz = spec[2] - spec[1] + 2 * pad, onx = spec[4] - spec[3] + 2 * pad, ony = yd + 2 * pad;
+    /* one row buffer for the whole patch, as the reference (:108): a cell no
+     * source covers keeps the previous row's value */
+    float* row = (float*)calloc((size_t)(yd > 0 ? yd : 1), sizeof(float));
+    memset(out, 0, sizeof(float) * (size_t)onz * onx * ony);
+    for (int oz = 0; oz < onz; ++oz) {
+        const int z = spec[1] - pad + oz;
+        for (int ox = 0; ox < onx; ++ox) {
+            const int x = spec[3] - pad + ox;
+            float* dst = out + ((size_t)oz * onx + ox) * ony;
+            const int inside = z >= 0 && z < zd && x >= 0 && x < xd;
+            if (!inside && zero) continue;
+            const int zr = inside ? z : orc_reflect_index(z, zd), xr = inside ? x : orc_reflect_index(x, xd);
+            orc_fill_level_row(leaf, values, tree, tree_values, l, zr, xr, row, 0, yd);
+            for (int y = 0; y < yd; ++y) dst[pad + y] = row[y];
+            for (int p = 0; p < pad; ++p) {
+                dst[p] = zero ? 0.0f : row[orc_reflect_index(p - pad, yd)];
+                dst[pad + yd + p] = zero ? 0.0f : row[orc_reflect_index(yd + p, yd)];
+            }
+        }
+    }
+    free(row);
+}
+
 /* -------------------------------------------------------------- stencil ---- */
 
 static int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }

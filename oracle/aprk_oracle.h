@@ -70,6 +70,12 @@ void orc_fill_level_row(const orc_access* leaf, const float* values, const orc_a
 void orc_reconstruct_level(const orc_access* leaf, const float* values, const orc_access* tree,
                            const float* tree_values, int l, float* out);
 
+/* reconstruct_patch (reconstruct.hpp:94-129): spec = level, z_begin, z_end,
+ * x_begin, x_end, pad, pad_mode (0 Zero, 1 Reflect); out is (z_end - z_begin +
+ * 2 pad) x (x_end - x_begin + 2 pad) x (y_dim + 2 pad).  tree_values may be NULL. */
+void orc_reconstruct_patch(const orc_access* leaf, const float* values, const orc_access* tree,
+                           const float* tree_values, const int spec[7], float* out);
+
 /* restrict_stencil (stencil.hpp:127-160).  out_k3 receives the extents; out may
  * be NULL to query them. */
 void orc_restrict_stencil(const float* w, int kz, int kx, int ky, int delta, int out_k3[3],

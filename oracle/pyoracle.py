@@ -96,6 +96,7 @@ class Oracle:
         L.orc_free_access.argtypes = [vp]
         L.orc_fill_tree.argtypes = [vp, vp, vp, vp, vp]
         L.orc_reconstruct_level.argtypes = [vp, vp, vp, vp, C.c_int, vp]
+        L.orc_reconstruct_patch.argtypes = [vp, vp, vp, vp, vp, vp]
         L.orc_restrict_stencil.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
         L.orc_convolve.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp]
         L.orc_rl_apr.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, C.c_double, vp]
@@ -145,8 +146,23 @@ class Oracle:
         a = as_access(leaf)
         out = np.zeros((int(a.z_dim[l]), int(a.x_dim[l]), int(a.y_dim[l])), np.float32)
         v = np.ascontiguousarray(values, np.float32)
-        tv = np.ascontiguousarray(tree_values, np.float32)
-        self.L.orc_reconstruct_level(C.byref(la), _p(v), C.byref(ta), _p(tv), l, out.ctypes.data)
+        tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
+        self.L.orc_reconstruct_level(C.byref(la), _p(v), C.byref(ta), None if tv is None else _p(tv), l,
+                                     out.ctypes.data)
+        return out
+
+    def reconstruct_patch(self, leaf, tree, values, tree_values, spec) -> np.ndarray:
+        """spec: (level, z_begin, z_end, x_begin, x_end, pad, pad_mode)."""
+        keep = []
+        la, ta = _orc_access(leaf, keep), _orc_access(tree, keep)
+        a = as_access(leaf)
+        l, zb, ze, xb, xe, pad, _ = (int(v) for v in spec)
+        out = np.zeros((ze - zb + 2 * pad, xe - xb + 2 * pad, int(a.y_dim[l]) + 2 * pad), np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
+        sp = np.array(spec, np.int32)
+        self.L.orc_reconstruct_patch(C.byref(la), _p(v), C.byref(ta), None if tv is None else _p(tv), _p(sp),
+                                     out.ctypes.data)
         return out
 
     def restrict_stencil(self, w: np.ndarray, k3, delta: int):
@@ -323,6 +339,8 @@ class Ref:
         L.ref_box_stencil.argtypes = [C.c_int, vp]
         L.ref_convolve.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]
         L.ref_reconstruct_level.argtypes = [vp, vp, vp, C.c_int, vp]
+        L.ref_reconstruct_full.argtypes = [vp, vp, vp]
+        L.ref_reconstruct_patch.argtypes = [vp, vp, vp, vp, vp]
         L.ref_rl_apr.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, vp]
         L.ref_resolve_threads.argtypes = [C.c_int]
         self.L = L
@@ -446,8 +464,27 @@ class Ref:
         a = apr.leaf
         out = np.zeros((int(a.z_dim[l]), int(a.x_dim[l]), int(a.y_dim[l])), np.float32)
         v = np.ascontiguousarray(values, np.float32)
-        tv = np.ascontiguousarray(tree_values, np.float32)
-        self._chk(self.L.ref_reconstruct_level(apr.h, _p(v), _p(tv), l, out.ctypes.data))
+        tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
+        self._chk(self.L.ref_reconstruct_level(apr.h, _p(v), None if tv is None else _p(tv), l, out.ctypes.data))
+        return out
+
+    def reconstruct_full(self, apr: RefApr, values):
+        a = apr.leaf
+        l = a.l_max
+        out = np.zeros((int(a.z_dim[l]), int(a.x_dim[l]), int(a.y_dim[l])), np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        self._chk(self.L.ref_reconstruct_full(apr.h, _p(v), out.ctypes.data))
+        return out
+
+    def reconstruct_patch(self, apr: RefApr, values, tree_values, spec):
+        a = apr.leaf
+        l, zb, ze, xb, xe, pad, _ = (int(v) for v in spec)
+        out = np.zeros((ze - zb + 2 * pad, xe - xb + 2 * pad, int(a.y_dim[l]) + 2 * pad), np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
+        sp = np.array(spec, np.int32)
+        self._chk(self.L.ref_reconstruct_patch(apr.h, _p(v), None if tv is None else _p(tv), _p(sp),
+                                               out.ctypes.data))
         return out
 
     def rl_apr(self, apr: RefApr, observed, w, k3, iterations, epsilon=0.0, threads=0):

@@ -357,8 +357,40 @@ REF_API int ref_reconstruct_level(void* hp, const float* values, const float* tr
     return guarded([&] {
         auto* h = static_cast<RefApr*>(hp);
         aprkit::ParticleValues v(values, values + h->apr.access.particle_count());
-        aprkit::ParticleValues t(tree, tree + h->apr.tree_access.particle_count());
+        aprkit::ParticleValues t;  // tree NULL: no interior nodes (as reconstruct_full)
+        if (tree) t.assign(tree, tree + h->apr.tree_access.particle_count());
         auto img = aprkit::reconstruct_level(h->apr, v, t, l);
+        std::memcpy(out, img.values.data(), 4 * img.values.size());
+    });
+}
+
+// reconstruct_full (reconstruct.hpp:87-90)
+REF_API int ref_reconstruct_full(void* hp, const float* values, float* out) {
+    return guarded([&] {
+        auto* h = static_cast<RefApr*>(hp);
+        aprkit::ParticleValues v(values, values + h->apr.access.particle_count());
+        auto img = aprkit::reconstruct_full(h->apr, v);
+        std::memcpy(out, img.values.data(), 4 * img.values.size());
+    });
+}
+
+// reconstruct_patch (reconstruct.hpp:94-129); spec = level, z_begin, z_end,
+// x_begin, x_end, pad, pad_mode (0 Zero, 1 Reflect)
+REF_API int ref_reconstruct_patch(void* hp, const float* values, const float* tree, const int* spec, float* out) {
+    return guarded([&] {
+        auto* h = static_cast<RefApr*>(hp);
+        aprkit::ParticleValues v(values, values + h->apr.access.particle_count());
+        aprkit::ParticleValues t;
+        if (tree) t.assign(tree, tree + h->apr.tree_access.particle_count());
+        aprkit::PatchSpec sp;
+        sp.level = spec[0];
+        sp.z_begin = spec[1];
+        sp.z_end = spec[2];
+        sp.x_begin = spec[3];
+        sp.x_end = spec[4];
+        sp.pad = spec[5];
+        sp.pad_mode = spec[6] == 0 ? aprkit::PadMode::Zero : aprkit::PadMode::Reflect;
+        auto img = aprkit::reconstruct_patch(h->apr, v, t, sp);
         std::memcpy(out, img.values.data(), 4 * img.values.size());
     });
 }

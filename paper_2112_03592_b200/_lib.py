@@ -37,6 +37,10 @@ class AccessInfo(C.Structure):
 _lib = None
 _lock = threading.Lock()
 
+class PatchSpecC(C.Structure):  # aprgpu_patch_spec
+    _fields_ = [(n, C.c_int) for n in ("level", "z_begin", "z_end", "x_begin", "x_end", "pad", "pad_mode")]
+
+
 _SIGS = {
     "aprgpu_init": [C.c_int, C.POINTER(C.c_void_p)],
     "aprgpu_ctx_free": [C.c_void_p],
@@ -80,6 +84,8 @@ _SIGS = {
     "aprgpu_build_apr": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                          C.POINTER(C.c_void_p)],
     "aprgpu_apr_values": [C.c_void_p, C.c_void_p, C.c_int],
+    "aprgpu_reconstruct_level": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p],
+    "aprgpu_reconstruct_patch": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p],
 }
 
 EXPORTED = sorted(list(_SIGS) + ["aprgpu_last_error"])

@@ -433,6 +433,49 @@ class DeviceApr:
                                   int(iterations), float(epsilon), accum, _ptr(out), L.HOST, None))
         return out
 
+    def reconstruct_level(self, values: np.ndarray, tree_values, level: int) -> np.ndarray:
+        values = np.ascontiguousarray(values, dtype=np.float32)
+        if values.size != self.n_particles:
+            raise RangeError("reconstruct_level: value count does not match the APR")
+        tv = None
+        if tree_values is not None and np.asarray(tree_values).size:
+            tv = np.ascontiguousarray(tree_values, dtype=np.float32)
+            if tv.size != self.n_tree:
+                raise RangeError("reconstruct_level: tree value count does not match the APR")
+        i = self.info(L.LEAF)
+        if level < i.l_min or level > i.l_max:
+            raise RangeError("reconstruct_level: level out of range")
+        a = self.download_dims()
+        nz, nx, ny = a[0][level], a[1][level], a[2][level]
+        out = np.empty((nz, nx, ny), np.float32)
+        L.check(L.lib().aprgpu_reconstruct_level(self.handle, _ptr(values), _ptr(tv) if tv is not None else None,
+                                                 int(level), _ptr(out), L.HOST, None))
+        return out
+
+    def reconstruct_patch(self, values: np.ndarray, tree_values, spec: "PatchSpec") -> np.ndarray:
+        values = np.ascontiguousarray(values, dtype=np.float32)
+        tv = None
+        if tree_values is not None and np.asarray(tree_values).size:
+            tv = np.ascontiguousarray(tree_values, dtype=np.float32)
+        c = L.PatchSpecC(spec.level, spec.z_begin, spec.z_end, spec.x_begin, spec.x_end, spec.pad, int(spec.pad_mode))
+        i = self.info(L.LEAF)
+        if spec.level < i.l_min or spec.level > i.l_max:
+            raise RangeError("reconstruct_patch: level out of range")
+        ny = self.download_dims()[2][spec.level]
+        shape = (max(spec.z_end - spec.z_begin + 2 * spec.pad, 0), max(spec.x_end - spec.x_begin + 2 * spec.pad, 0),
+                 ny + 2 * max(spec.pad, 0))
+        out = np.empty(shape, np.float32)
+        L.check(L.lib().aprgpu_reconstruct_patch(self.handle, _ptr(values), _ptr(tv) if tv is not None else None,
+                                                 C.byref(c), _ptr(out) if out.size else None, L.HOST, None))
+        return out
+
+    def download_dims(self):
+        """(z_dim, x_dim, y_dim) per level of the leaf access."""
+        if not hasattr(self, "_dims_cache"):
+            a = self.download(L.LEAF)
+            self._dims_cache = (list(a.z_dim), list(a.x_dim), list(a.y_dim))
+        return self._dims_cache
+
     # device-pointer entry points (stream-ordered; pointers are raw ints) -----
     def fill_tree_ptr(self, leaf_ptr: int, tree_ptr: int, stream: int = 0) -> None:
         L.check(L.lib().aprgpu_fill_tree(self.handle, leaf_ptr, tree_ptr, L.DEVICE, stream or None))
@@ -489,6 +532,34 @@ def convolve_apr(apr: APR, values, tree_values, pyramid: StencilPyramid, pad: Pa
             raise CapabilityError("convolve_apr: stencil extent exceeds the supported maximum")
     dev = apr.device()
     return dev.convolve(values, tree_values, pyramid.device(dev.ctx), int(pad), _accum(opt.accum))
+
+
+@dataclass
+class PatchSpec:                                          # reconstruct.hpp:28-35
+    level: int = 0
+    z_begin: int = 0
+    z_end: int = 0
+    x_begin: int = 0
+    x_end: int = 0
+    pad: int = 0
+    pad_mode: PadMode = PadMode.Reflect
+
+
+def reconstruct_level(apr: APR, values, tree_values, l: int) -> np.ndarray:
+    """reconstruct.hpp:73-84 on the device: (z_dim, x_dim, y_dim) of level l."""
+    if l < apr.access.l_min or l > apr.access.l_max:
+        raise RangeError("reconstruct_level: level out of range")
+    return apr.device().reconstruct_level(values, tree_values, l)
+
+
+def reconstruct_full(apr: APR, values) -> np.ndarray:
+    """reconstruct.hpp:87-90: every pixel takes its covering leaf's value."""
+    return reconstruct_level(apr, values, None, apr.access.l_max)
+
+
+def reconstruct_patch(apr: APR, values, tree_values, spec: PatchSpec) -> np.ndarray:
+    """reconstruct.hpp:94-129 on the device."""
+    return apr.device().reconstruct_patch(values, tree_values, spec)
 
 
 @dataclass

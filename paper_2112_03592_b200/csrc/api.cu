@@ -520,6 +520,75 @@ int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_valu
     });
 }
 
+}  // extern "C"
+
+namespace {
+// Shared body of the reconstruction entry points: host pointers are staged
+// through device buffers (values, tree values, the output volume).
+template <typename F>
+void reconstruct_call(aprgpu_apr* apr, const float* values, const float* tree_values, float* out, uint64_t cells,
+                      int ptr_kind, void* stream, F run) {
+    need(apr && values && out, "null argument");
+    need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
+    DeviceGuard g(apr->ctx->device);
+    cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
+    if (ptr_kind == APRGPU_DEVICE) {
+        run(values, tree_values, out, s);
+        return;
+    }
+    const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
+    apr->h_in.ensure(4 * np + 4);
+    APR_CUDA(cudaMemcpyAsync(apr->h_in.p, values, 4 * np, cudaMemcpyHostToDevice, s));
+    const float* tv = nullptr;
+    if (tree_values && nt) {
+        apr->h_tree.ensure(4 * nt + 4);
+        APR_CUDA(cudaMemcpyAsync(apr->h_tree.p, tree_values, 4 * nt, cudaMemcpyHostToDevice, s));
+        tv = apr->h_tree.as<float>();
+    }
+    aprgpu::GpuBuf dev_out;
+    dev_out.ensure(4 * cells + 4);
+    run(apr->h_in.as<float>(), tv, dev_out.as<float>(), s);
+    APR_CUDA(cudaMemcpyAsync(out, dev_out.p, 4 * cells, cudaMemcpyDeviceToHost, s));
+    APR_CUDA(cudaStreamSynchronize(s));
+    dev_out.release();
+}
+}  // namespace
+
+extern "C" {
+
+int aprgpu_reconstruct_level(aprgpu_apr* apr, const float* values, const float* tree_values, int level, float* out,
+                             int ptr_kind, void* stream) {
+    return guard([&] {
+        need(apr != nullptr, "null argument");
+        const aprgpu::DevAccess& L = apr->leaf;
+        if (level < L.l_min || level > L.l_max) aprgpu::fail(APRGPU_ERR_RANGE, "reconstruct_level: level out of range");
+        const uint64_t cells = static_cast<uint64_t>(L.zd[level]) * L.xd[level] * L.yd[level];
+        reconstruct_call(apr, values, tree_values, out, cells, ptr_kind, stream,
+                         [&](const float* v, const float* tv, float* o, cudaStream_t s) {
+                             aprgpu::reconstruct_level_device(apr, v, tv, level, o, s);
+                         });
+    });
+}
+
+int aprgpu_reconstruct_patch(aprgpu_apr* apr, const float* values, const float* tree_values,
+                             const aprgpu_patch_spec* spec, float* out, int ptr_kind, void* stream) {
+    return guard([&] {
+        need(apr && spec, "null argument");
+        const aprgpu::DevAccess& L = apr->leaf;
+        const int l = spec->level;
+        if (l < L.l_min || l > L.l_max) aprgpu::fail(APRGPU_ERR_RANGE, "reconstruct_patch: level out of range");
+        if (spec->z_begin < 0 || spec->z_end > L.zd[l] || spec->x_begin < 0 || spec->x_end > L.xd[l] ||
+            spec->z_begin > spec->z_end || spec->x_begin > spec->x_end || spec->pad < 0)
+            aprgpu::fail(APRGPU_ERR_RANGE, "reconstruct_patch: spec outside the level grid");
+        const uint64_t cells = static_cast<uint64_t>(spec->z_end - spec->z_begin + 2 * spec->pad) *
+                               (spec->x_end - spec->x_begin + 2 * spec->pad) * (L.yd[l] + 2 * spec->pad);
+        reconstruct_call(apr, values, tree_values, out, cells, ptr_kind, stream,
+                         [&](const float* v, const float* tv, float* o, cudaStream_t s) {
+                             aprgpu::reconstruct_patch_device(apr, v, tv, *spec, o, s);
+                         });
+    });
+}
+
 int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, int kx, int ky, int iterations,
               double epsilon, int accum, float* out, int ptr_kind, void* stream) {
     return aprgpu_rl_resume(apr, observed, nullptr, psf, kz, kx, ky, iterations, epsilon, accum, out, ptr_kind,

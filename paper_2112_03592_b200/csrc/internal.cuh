@@ -134,6 +134,12 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
                       int pad, int accum, float* out, const struct EpiArgs& epi, const struct Slab& slab,
                       cudaStream_t s, bool* done);
 
+// reconstruct.cu
+void reconstruct_level_device(aprgpu_apr* apr, const float* values, const float* tree_values, int l, float* out,
+                              cudaStream_t s);
+void reconstruct_patch_device(aprgpu_apr* apr, const float* values, const float* tree_values,
+                              const aprgpu_patch_spec& spec, float* out, cudaStream_t s);
+
 // tree.cu
 void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr);
