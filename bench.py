@@ -256,6 +256,26 @@ def run_ours(args, rank, world):
         e1.synchronize()
         rl_t.append(e0.elapsed_time(e1) / 1e3)
 
+    # reconstruct_full (reconstruct.hpp:87-90) of the same APR: the dense image,
+    # bound by writing it (4 bytes per pixel); skipped when it would not fit easily
+    recon = None
+    if 4 * n_pix <= 16e9:
+        img = torch.empty(n_pix, dtype=torch.float32, device="cuda")
+        lmax = int(dapr.info(L.LEAF).l_max)
+        rt = []
+        for i in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dapr.reconstruct_level_ptr(v.data_ptr(), 0, lmax, img.data_ptr(), s)
+            e1.record(stream)
+            e1.synchronize()
+            rt.append(e0.elapsed_time(e1) / 1e3)
+        del img
+        tr = min(rt[1:])
+        recon = {"ms": round(tr * 1e3, 4), "write_gbs": round(4 * n_pix / tr / 1e9, 1),
+                 "frac_of_peak": round(4 * n_pix / tr / 1e9 / peaks()[0], 4),
+                 "note": "reconstruct_full on the device (k_reconstruct), output bytes / time, best of 2 warm runs"}
+
     def agg(x):
         t = float(np.mean(x))
         if world > 1:
@@ -307,6 +327,8 @@ def run_ours(args, rank, world):
                    "psf": f"gaussian(1.0,{k}), restricted pyramids of w and flip(w)",
                    "note": "C5; second of two runs, includes the pyramid setup and one D2H for the mean"},
     }
+    if recon:
+        res["reconstruct_full"] = recon
     if rank == 0 and not args.no_cpu_baseline and apr is not None:
         res["cpu_baseline"] = cpu_baseline(apr, values, tv[:dapr.n_tree].cpu().numpy(), pyr, args)
     return res

@@ -485,6 +485,11 @@ class DeviceApr:
         L.check(L.lib().aprgpu_convolve(self.handle, values_ptr, tree_ptr, pyr.handle, int(pad), accum, out_ptr,
                                         L.DEVICE, stream or None))
 
+    def reconstruct_level_ptr(self, values_ptr: int, tree_ptr: int, level: int, out_ptr: int,
+                              stream: int = 0) -> None:
+        L.check(L.lib().aprgpu_reconstruct_level(self.handle, values_ptr, tree_ptr or None, int(level), out_ptr,
+                                                 L.DEVICE, stream or None))
+
     def rl_ptr(self, observed_ptr: int, psf: Stencil, iterations: int, epsilon: float, accum: int, out_ptr: int,
                stream: int = 0) -> None:
         L.check(L.lib().aprgpu_rl(self.handle, observed_ptr, _ptr(psf.weights), psf.kz, psf.kx, psf.ky,

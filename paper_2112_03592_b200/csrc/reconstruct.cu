@@ -38,16 +38,22 @@ __device__ __forceinline__ int reflect_i(int i, int n) {  // reflect_index (reco
 // fill_level_row (reconstruct.hpp:41-69) of level row (z, x), y in [0, yd), into dst
 __device__ void fill_row_warp(const ReconArgs& a, int z, int x, float* dst, int yd, int lane) {
     const int l = a.l;
+    // every covering row's particle range at once: lane d loads depth d's
+    uint32_t rb = 0, re = 0;
+    if (lane <= l - a.leaf.l_min && l - lane <= a.leaf.l_max) {
+        const LevelG g = a.leaf.g[l - lane];
+        const int cz = z >> lane, cx = x >> lane;
+        if (cz < g.zd && cx < g.xd) {
+            const uint32_t row = g.row0 + static_cast<uint32_t>(cz) * g.xd + cx;
+            rb = __ldg(a.leaf.rb + row);
+            re = __ldg(a.leaf.rb + row + 1);
+        }
+    }
     for (int y = lane; y < yd; y += 32) dst[y] = 0.0f;
     __syncwarp();
     for (int d = 0; d <= l - a.leaf.l_min; ++d) {
-        const int ll = l - d;
-        if (ll > a.leaf.l_max) continue;
-        const LevelG g = a.leaf.g[ll];
-        const int cz = z >> d, cx = x >> d;
-        if (cz >= g.zd || cx >= g.xd) continue;
-        const uint32_t row = g.row0 + static_cast<uint32_t>(cz) * g.xd + cx;
-        const uint32_t b = __ldg(a.leaf.rb + row), e = __ldg(a.leaf.rb + row + 1);
+        const uint32_t b = __shfl_sync(0xffffffffu, rb, d), e = __shfl_sync(0xffffffffu, re, d);
+        if (e <= b) continue;
         if (d <= 2) {
             for (uint32_t i = b + lane; i < e; i += 32) {
                 const int y0 = static_cast<int>(__ldg(a.leaf.y + i)) << d;
