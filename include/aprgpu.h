@@ -113,6 +113,14 @@ int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, u
  * accumulation in the reference's per-parent order, bit-exact. */
 int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream);
 
+/* validate (apr.hpp:61-134) of a leaf access and its image dims, on the device
+ * in O(particles + rows) instead of the reference's O(pixels) cover map: *ok = 1,
+ * or 0 with the reference's message for the first violation it reports copied
+ * to msg (msg_cap bytes, NUL-terminated; msg may be NULL).  Violations are
+ * results, not errors; errors are the usual status codes. */
+int aprgpu_validate_access(aprgpu_ctx* ctx, const aprgpu_access_desc* leaf, const int32_t source_dims[3], int* ok,
+                           char* msg, size_t msg_cap);
+
 /* ---- dense reconstruction (reconstruct.hpp:73-129) ------------------------- */
 /* Patch window of reconstruct_patch (PatchSpec, reconstruct.hpp:28-35): level-l
  * cells z in [z_begin, z_end), x in [x_begin, x_end), the full y span, pad cells

@@ -6,6 +6,7 @@
  */
 #include "aprk_oracle.h"
 
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -34,6 +35,80 @@ int orc_get_row(const orc_access* a, int l, int z, int x, uint64_t* begin, uint6
     *begin = r ? a->xz_end[r - 1] : 0;
     *end = a->xz_end[r];
     return 0;
+}
+
+/* validate (apr.hpp:61-134): the reference's checks in its order, with its
+ * messages (into msg, cap bytes); the partition property by marking every pixel
+ * (O(pixels): this is the checker, not the product).  Returns 1 if ok. */
+int orc_validate(const orc_access* a, const int dims[3], char* msg, size_t cap) {
+#define ORC_FAIL(...) do { if (msg && cap) snprintf(msg, cap, __VA_ARGS__); return 0; } while (0)
+    if (msg && cap) msg[0] = 0;
+    if (a->l_min > a->l_max) ORC_FAIL("l_min > l_max");
+    uint64_t expect = 0;
+    for (int l = a->l_min; l <= a->l_max; ++l) {
+        if (a->level_offset[l] != expect) ORC_FAIL("level_offset mismatch at level %d", l);
+        expect += (uint64_t)a->z_dim[l] * (uint64_t)a->x_dim[l];
+    }
+    if (a->n_rows != expect) ORC_FAIL("xz_end length does not match level grids");
+    uint64_t prev = 0;
+    for (uint64_t r = 0; r < a->n_rows; ++r) {
+        if (a->xz_end[r] < prev) ORC_FAIL("xz_end decreases at row %llu", (unsigned long long)r);
+        prev = a->xz_end[r];
+    }
+    if (a->n_rows && a->xz_end[a->n_rows - 1] != a->n_particles) ORC_FAIL("xz_end[last] != y_idx length");
+    if (!a->n_rows && a->n_particles) ORC_FAIL("particles present but no rows");
+    for (int l = a->l_min; l <= a->l_max; ++l)
+        for (int z = 0; z < a->z_dim[l]; ++z)
+            for (int x = 0; x < a->x_dim[l]; ++x) {
+                uint64_t b, e;
+                orc_get_row(a, l, z, x, &b, &e);
+                int last = -1;
+                for (uint64_t i = b; i < e; ++i) {
+                    const int y = a->y_idx[i];
+                    if (y <= last) ORC_FAIL("non-increasing y in row (%d, %d, %d)", l, z, x);
+                    if (y >= a->y_dim[l]) ORC_FAIL("y index out of level grid in level %d", l);
+                    last = y;
+                }
+            }
+    const uint64_t n_pixels = (uint64_t)dims[0] * (uint64_t)dims[1] * (uint64_t)dims[2];
+    if (n_pixels == 0) return 1;
+    uint8_t* cover = (uint8_t*)calloc(n_pixels, 1);
+    int dbl = 0, overflow = 0;
+    for (int l = a->l_min; l <= a->l_max; ++l) {
+        const int s = 1 << (a->l_max - l);  /* cell_size(geom_l_max = l_max, l) */
+        for (int z = 0; z < a->z_dim[l]; ++z)
+            for (int x = 0; x < a->x_dim[l]; ++x) {
+                uint64_t b, e;
+                orc_get_row(a, l, z, x, &b, &e);
+                for (uint64_t i = b; i < e; ++i) {
+                    const int64_t z0 = (int64_t)z * s, x0 = (int64_t)x * s, y0 = (int64_t)a->y_idx[i] * s;
+                    if (z0 >= dims[0] || x0 >= dims[1] || y0 >= dims[2]) { overflow = 1; continue; }
+                    const int64_t z1 = z0 + s < dims[0] ? z0 + s : dims[0];
+                    const int64_t x1 = x0 + s < dims[1] ? x0 + s : dims[1];
+                    const int64_t y1 = y0 + s < dims[2] ? y0 + s : dims[2];
+                    for (int64_t zz = z0; zz < z1; ++zz)
+                        for (int64_t xx = x0; xx < x1; ++xx)
+                            for (int64_t yy = y0; yy < y1; ++yy) {
+                                uint8_t* c = cover + ((uint64_t)zz * dims[1] + (uint64_t)xx) * dims[2] + (uint64_t)yy;
+                                if (*c) dbl = 1;
+                                *c = 1;
+                            }
+                }
+            }
+    }
+    int ok = 1;
+    if (overflow) { if (msg && cap) snprintf(msg, cap, "particle cell outside the image domain"); ok = 0; }
+    else if (dbl) { if (msg && cap) snprintf(msg, cap, "double coverage: overlapping particle cells"); ok = 0; }
+    else
+        for (uint64_t i = 0; i < n_pixels; ++i)
+            if (!cover[i]) {
+                if (msg && cap) snprintf(msg, cap, "uncovered pixel at flat index %llu", (unsigned long long)i);
+                ok = 0;
+                break;
+            }
+    free(cover);
+    return ok;
+#undef ORC_FAIL
 }
 
 /* ---------------------------------------------------------------- tree ---- */

@@ -12,6 +12,7 @@
  */
 #ifndef APRK_ORACLE_H
 #define APRK_ORACLE_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -30,6 +31,9 @@ typedef struct {
     uint64_t n_rows;
     const uint64_t* level_offset; /* l_max+1 */
 } orc_access;
+
+/* validate (apr.hpp:61-134): 1 if ok, else 0 with the reference's message in msg */
+int orc_validate(const orc_access* a, const int dims[3], char* msg, size_t cap);
 
 /* reflect_index (reconstruct.hpp:17-25) */
 int orc_reflect_index(int i, int n);

@@ -97,6 +97,8 @@ class Oracle:
         L.orc_fill_tree.argtypes = [vp, vp, vp, vp, vp]
         L.orc_reconstruct_level.argtypes = [vp, vp, vp, vp, C.c_int, vp]
         L.orc_reconstruct_patch.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.orc_validate.restype = C.c_int
+        L.orc_validate.argtypes = [vp, vp, vp, C.c_size_t]
         L.orc_restrict_stencil.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
         L.orc_convolve.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp]
         L.orc_rl_apr.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, C.c_double, vp]
@@ -150,6 +152,15 @@ class Oracle:
         self.L.orc_reconstruct_level(C.byref(la), _p(v), C.byref(ta), None if tv is None else _p(tv), l,
                                      out.ctypes.data)
         return out
+
+    def validate(self, leaf, dims):
+        """validate (apr.hpp:61-134): (ok, message)."""
+        keep = []
+        la = _orc_access(leaf, keep)
+        dm = np.array([int(v) for v in dims], np.int32)
+        buf = C.create_string_buffer(512)
+        ok = self.L.orc_validate(C.byref(la), dm.ctypes.data, buf, 512)
+        return bool(ok), buf.value.decode()
 
     def reconstruct_patch(self, leaf, tree, values, tree_values, spec) -> np.ndarray:
         """spec: (level, z_begin, z_end, x_begin, x_end, pad, pad_mode)."""
@@ -340,6 +351,9 @@ class Ref:
         L.ref_convolve.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]
         L.ref_reconstruct_level.argtypes = [vp, vp, vp, C.c_int, vp]
         L.ref_reconstruct_full.argtypes = [vp, vp, vp]
+        L.ref_validate_arrays.restype = C.c_int
+        L.ref_validate_arrays.argtypes = [C.c_int, C.c_int, vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64, vp,
+                                          C.c_int, C.c_int, C.c_int, vp, C.c_uint64]
         L.ref_reconstruct_patch.argtypes = [vp, vp, vp, vp, vp]
         L.ref_rl_apr.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, vp]
         L.ref_resolve_threads.argtypes = [C.c_int]
@@ -467,6 +481,16 @@ class Ref:
         tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
         self._chk(self.L.ref_reconstruct_level(apr.h, _p(v), None if tv is None else _p(tv), l, out.ctypes.data))
         return out
+
+    def validate_arrays(self, leaf, dims):
+        """validate (apr.hpp:61-134) of a leaf access: (ok, message)."""
+        a = as_access(leaf)
+        buf = C.create_string_buffer(512)
+        ok = self.L.ref_validate_arrays(a.l_min, a.l_max, a.z_dim.ctypes.data, a.x_dim.ctypes.data,
+                                        a.y_dim.ctypes.data, _p(a.y_idx), a.y_idx.size, _p(a.xz_end),
+                                        a.xz_end.size, a.level_offset.ctypes.data, int(dims[0]), int(dims[1]),
+                                        int(dims[2]), buf, 512)
+        return bool(ok), buf.value.decode()
 
     def reconstruct_full(self, apr: RefApr, values):
         a = apr.leaf

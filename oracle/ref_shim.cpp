@@ -240,6 +240,30 @@ REF_API std::uint64_t ref_apr_values(void* hp, float* out) {
 // validate (apr.hpp:61-134); returns 1 if ok
 REF_API int ref_validate(void* hp) { return aprkit::validate(static_cast<RefApr*>(hp)->apr).ok ? 1 : 0; }
 
+// validate (apr.hpp:61-134) of raw leaf arrays (no tree is built: malformed
+// structures are the point); returns ok, the report's message into msg
+REF_API int ref_validate_arrays(int l_min, int l_max, const int* zd, const int* xd, const int* yd,
+                                const std::uint16_t* y_idx, std::uint64_t n_particles, const std::uint64_t* xz_end,
+                                std::uint64_t n_rows, const std::uint64_t* level_offset, int nz, int nx, int ny,
+                                char* msg, std::uint64_t cap) {
+    aprkit::LinearAccess a;
+    a.l_min = l_min;
+    a.l_max = l_max;
+    a.z_dim.assign(zd, zd + l_max + 1);
+    a.x_dim.assign(xd, xd + l_max + 1);
+    a.y_dim.assign(yd, yd + l_max + 1);
+    a.y_idx.assign(y_idx, y_idx + n_particles);
+    a.xz_end.assign(xz_end, xz_end + n_rows);
+    a.level_offset.assign(level_offset, level_offset + l_max + 1);
+    const auto rep = aprkit::validate(a, std::array<int, 3>{nz, nx, ny});
+    if (msg && cap) {
+        const std::size_t n = std::min<std::size_t>(cap - 1, rep.message.size());
+        std::memcpy(msg, rep.message.data(), n);
+        msg[n] = 0;
+    }
+    return rep.ok ? 1 : 0;
+}
+
 // ---- hot path ----------------------------------------------------------------
 // fill_tree (tree.hpp:110-150)
 REF_API int ref_fill_tree(void* hp, const float* leaf, int threads, float* out) {

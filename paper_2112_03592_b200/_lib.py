@@ -84,6 +84,7 @@ _SIGS = {
     "aprgpu_build_apr": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                          C.POINTER(C.c_void_p)],
     "aprgpu_apr_values": [C.c_void_p, C.c_void_p, C.c_int],
+    "aprgpu_validate_access": [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int), C.c_char_p, C.c_size_t],
     "aprgpu_reconstruct_level": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p],
     "aprgpu_reconstruct_patch": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p],
 }

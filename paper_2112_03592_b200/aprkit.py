@@ -144,6 +144,29 @@ class APR:
         return h
 
 
+@dataclass
+class ValidationReport:                                   # apr.hpp:50-56
+    ok: bool = True
+    message: str = ""
+
+
+def validate(apr_or_access, source_dims=None, ctx: Optional["Context"] = None) -> ValidationReport:
+    """validate (apr.hpp:61-136) on the device in O(particles + rows): the
+    reference's checks, order and messages without its O(pixels) cover map.
+    Takes an APR, or a leaf LinearAccess and the image dims."""
+    if isinstance(apr_or_access, APR):
+        access, dims = apr_or_access.access, apr_or_access.source_dims
+    else:
+        access, dims = apr_or_access, source_dims
+    ctx = ctx or default_context()
+    d = access.desc()
+    dm = np.array([int(v) for v in dims], np.int32)
+    ok = C.c_int()
+    buf = C.create_string_buffer(512)
+    L.check(L.lib().aprgpu_validate_access(ctx.handle, C.byref(d), _ptr(dm), C.byref(ok), buf, 512))
+    return ValidationReport(bool(ok.value), buf.value.decode())
+
+
 def computational_ratio(apr: APR) -> float:              # apr.hpp:46-48
     return apr.pixel_count() / apr.access.particle_count()
 

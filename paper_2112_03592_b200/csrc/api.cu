@@ -1,3 +1,4 @@
+#include <algorithm>
 // The C-ABI (include/aprgpu.h): contexts, structure upload/download, stencil
 // pyramids, and the host/device-pointer front doors of fill_tree, convolve_apr
 // and rl_apr.  Exceptions never cross this boundary; aprgpu::Error carries the
@@ -274,6 +275,168 @@ int aprgpu_upload_access(aprgpu_ctx* ctx, const aprgpu_access_desc* leaf, const 
     if (st != APRGPU_OK && apr) {
         free_apr(apr);
         delete apr;
+    }
+    return st;
+}
+
+// The level grids are the image's (assemble_access geometry), which the
+// interior-structure partition check relies on.
+bool grids_match(const aprgpu_access_desc* d, const int32_t dims[3]) {
+    int lm = 0;
+    while ((1 << lm) < std::max(dims[0], std::max(dims[1], dims[2]))) ++lm;
+    if (lm != d->l_max) return false;
+    for (int l = d->l_min; l <= d->l_max; ++l) {
+        const int64_t s = int64_t(1) << (d->l_max - l);
+        if (d->z_dim[l] != (dims[0] + s - 1) / s || d->x_dim[l] != (dims[1] + s - 1) / s ||
+            d->y_dim[l] != (dims[2] + s - 1) / s)
+            return false;
+    }
+    return true;
+}
+
+// validate (apr.hpp:61-134), O(particles + rows) on the device; the reference's
+// checks in its order, with its messages.
+int aprgpu_validate_access(aprgpu_ctx* ctx, const aprgpu_access_desc* d, const int32_t source_dims[3], int* ok,
+                           char* msg, size_t msg_cap) {
+    aprgpu_apr* tmp = nullptr;
+    int st = guard([&] {
+        need(ctx && d && source_dims && ok, "null argument");
+        std::string m;
+        auto verdict = [&](std::string v) { m = std::move(v); };
+        // apr.hpp:62-83 (host: O(levels + rows))
+        if (d->l_min > d->l_max) {
+            verdict("l_min > l_max");
+        } else {
+            uint64_t expect = 0;
+            for (int l = d->l_min; l <= d->l_max && m.empty(); ++l) {
+                if (d->level_offset[l] != expect) verdict("level_offset mismatch at level " + std::to_string(l));
+                expect += static_cast<uint64_t>(d->z_dim[l]) * d->x_dim[l];
+            }
+            if (m.empty() && d->n_rows != expect) verdict("xz_end length does not match level grids");
+            uint64_t prev = 0;
+            for (uint64_t r = 0; r < d->n_rows && m.empty(); ++r) {
+                if (d->xz_end[r] < prev) verdict("xz_end decreases at row " + std::to_string(r));
+                prev = d->xz_end[r];
+            }
+            if (m.empty() && d->n_rows && d->xz_end[d->n_rows - 1] != d->n_particles)
+                verdict("xz_end[last] != y_idx length");
+            if (m.empty() && !d->n_rows && d->n_particles) verdict("particles present but no rows");
+        }
+        const uint64_t n_pixels = static_cast<uint64_t>(source_dims[0]) * source_dims[1] * source_dims[2];
+        if (m.empty()) {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            DeviceGuard g(ctx->device);
+            cudaStream_t s = ctx->stream;
+            tmp = new aprgpu_apr;
+            tmp->ctx = ctx;
+            for (int i = 0; i < 3; ++i) tmp->dims[i] = source_dims[i];
+            upload_one(ctx, d, tmp->leaf, false);
+            // rows (apr.hpp:85-101) and cell origins (:112-116)
+            struct Flags {
+                unsigned long long first_y, min_unc;
+                int overflow, dbl;
+            };
+            aprgpu::GpuBuf fb;
+            fb.ensure(sizeof(Flags));
+            const Flags init{~0ull, ~0ull, 0, 0};
+            APR_CUDA(cudaMemcpyAsync(fb.p, &init, sizeof(Flags), cudaMemcpyHostToDevice, s));
+            Flags* f = fb.as<Flags>();
+            aprgpu::validate_rows_device(ctx, tmp->leaf, source_dims, &f->first_y, &f->overflow, s);
+            Flags h{};
+            APR_CUDA(cudaMemcpyAsync(&h, fb.p, sizeof(Flags), cudaMemcpyDeviceToHost, s));
+            APR_CUDA(cudaStreamSynchronize(s));
+            if (h.first_y != ~0ull) {
+                const uint64_t i = h.first_y >> 1;
+                // the row of particle i: the first row ending after it
+                const uint64_t r = static_cast<uint64_t>(
+                    std::upper_bound(d->xz_end, d->xz_end + d->n_rows, i) - d->xz_end);
+                int l = d->l_max;
+                while (l > d->l_min && r < d->level_offset[l]) --l;
+                const uint64_t loc = r - d->level_offset[l];
+                const int z = static_cast<int>(loc / d->x_dim[l]), x = static_cast<int>(loc % d->x_dim[l]);
+                if (h.first_y & 1)
+                    verdict("y index out of level grid in level " + std::to_string(l));
+                else
+                    verdict("non-increasing y in row (" + std::to_string(l) + ", " + std::to_string(z) + ", " +
+                            std::to_string(x) + ")");
+            } else if (n_pixels == 0) {
+                // success (apr.hpp:106)
+            } else if (h.overflow) {
+                verdict("particle cell outside the image domain");
+            } else if (!grids_match(d, source_dims)) {
+                // level grids that are not the image's: the reference's cover map, on the device
+                aprgpu::validate_cover_device(ctx, tmp->leaf, source_dims, &f->dbl, &f->min_unc, s);
+                APR_CUDA(cudaMemcpyAsync(&h, fb.p, sizeof(Flags), cudaMemcpyDeviceToHost, s));
+                APR_CUDA(cudaStreamSynchronize(s));
+                if (h.dbl)
+                    verdict("double coverage: overlapping particle cells");
+                else if (h.min_unc != ~0ull)
+                    verdict("uncovered pixel at flat index " + std::to_string(h.min_unc));
+            } else {
+                // partition (apr.hpp:103-131) through the leaves' interior structure
+                tmp->geom_l_max = tmp->leaf.l_max;
+                aprgpu::build_tree_structure(ctx, tmp);
+                aprgpu::tree_partition_check(tmp, &f->dbl, &f->min_unc, s);
+                APR_CUDA(cudaMemcpyAsync(&h, fb.p, sizeof(Flags), cudaMemcpyDeviceToHost, s));
+                // the coarsest level's own cells: each in-image cell exactly one leaf or node
+                const aprgpu::DevAccess& T = tmp->tree;
+                const int top = T.n_particles ? T.l_min : d->l_min;
+                std::vector<uint16_t> ty;
+                std::vector<uint32_t> trb;
+                if (T.n_particles && top <= T.l_max) {
+                    const uint64_t r0 = T.level_offset[top], nr = static_cast<uint64_t>(T.zd[top]) * T.xd[top];
+                    trb.resize(nr + 1);
+                    APR_CUDA(cudaMemcpyAsync(trb.data(), T.rb + r0, 4 * (nr + 1), cudaMemcpyDeviceToHost, s));
+                    APR_CUDA(cudaStreamSynchronize(s));
+                    ty.resize(trb[nr] - trb[0]);
+                    if (!ty.empty())
+                        APR_CUDA(cudaMemcpy(ty.data(), T.y + trb[0], 2 * ty.size(), cudaMemcpyDeviceToHost));
+                }
+                APR_CUDA(cudaStreamSynchronize(s));
+                const int64_t cs = int64_t(1) << (d->l_max - top);
+                const int tzd = static_cast<int>((source_dims[0] + cs - 1) / cs),
+                          txd = static_cast<int>((source_dims[1] + cs - 1) / cs),
+                          tyd = static_cast<int>((source_dims[2] + cs - 1) / cs);
+                for (int z = 0; z < tzd; ++z)
+                    for (int x = 0; x < txd; ++x)
+                        for (int y = 0; y < tyd; ++y) {
+                            int c = 0;
+                            if (top >= d->l_min && z < d->z_dim[top] && x < d->x_dim[top]) {
+                                const uint64_t r = d->level_offset[top] + static_cast<uint64_t>(z) * d->x_dim[top] + x;
+                                const uint64_t b = r ? d->xz_end[r - 1] : 0, e = d->xz_end[r];
+                                c += std::binary_search(d->y_idx + b, d->y_idx + e, static_cast<uint16_t>(y)) ? 1 : 0;
+                            }
+                            if (!trb.empty() && z < T.zd[top] && x < T.xd[top]) {
+                                const uint64_t r = static_cast<uint64_t>(z) * T.xd[top] + x;
+                                const uint16_t* yb = ty.data() + (trb[r] - trb[0]);
+                                const uint16_t* ye = ty.data() + (trb[r + 1] - trb[0]);
+                                c += std::binary_search(yb, ye, static_cast<uint16_t>(y)) ? 1 : 0;
+                            }
+                            if (c > 1) h.dbl = 1;
+                            if (c == 0) {
+                                const unsigned long long p =
+                                    (static_cast<unsigned long long>(z * cs) * source_dims[1] + x * cs) *
+                                        source_dims[2] + y * cs;
+                                h.min_unc = std::min(h.min_unc, p);
+                            }
+                        }
+                if (h.dbl)
+                    verdict("double coverage: overlapping particle cells");
+                else if (h.min_unc != ~0ull)
+                    verdict("uncovered pixel at flat index " + std::to_string(h.min_unc));
+            }
+            fb.release();
+        }
+        *ok = m.empty() ? 1 : 0;
+        if (msg && msg_cap) {
+            const size_t n = std::min(msg_cap - 1, m.size());
+            std::memcpy(msg, m.data(), n);
+            msg[n] = '\0';
+        }
+    });
+    if (tmp) {
+        free_apr(tmp);
+        delete tmp;
     }
     return st;
 }

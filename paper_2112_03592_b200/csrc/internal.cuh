@@ -146,6 +146,16 @@ void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s);
 void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi, cudaStream_t s);
 void fill_tree_finalize(aprgpu_apr* apr, float* tree, cudaStream_t s);
+void ensure_tree_links(aprgpu_apr* apr, cudaStream_t s);
+void tree_partition_check(aprgpu_apr* apr, int* dbl, unsigned long long* min_unc, cudaStream_t s);
+
+// validate.cu: the per-row part of validate (apr.hpp:85-101) plus the cell
+// origins' domain check; first_y = min(particle << 1 | out-of-grid)
+void validate_rows_device(aprgpu_ctx* ctx, const DevAccess& L, const int dims[3], unsigned long long* first_y,
+                          int* overflow, cudaStream_t s);
+// the partition check by a per-pixel bitmap (structures whose grids are not the image's)
+void validate_cover_device(aprgpu_ctx* ctx, const DevAccess& L, const int dims[3], int* dbl,
+                           unsigned long long* min_unc, cudaStream_t s);
 
 // z-slab restriction of a convolution: levels >= lc compute only
 // the tiles / rows that touch finest-level pixel planes [z_lo, z_hi); coarser

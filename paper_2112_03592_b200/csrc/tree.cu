@@ -427,6 +427,121 @@ void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr) {
     if (bad) fail(APRGPU_ERR_INTEGRITY, "synchronized_parent_pass: missing parent for a child node");
 }
 
+namespace {
+
+// Per-level launch parameters of the parent-row kernels (k_fill_tree_level,
+// k_partition_check) for interior level lt.
+void set_fill_level(FillArgs& a, const DevAccess& L, const DevAccess& T, int lt) {
+    a.lt = lt;
+    a.c = lt + 1;
+    a.leaf_ok = (a.c >= L.l_min && a.c <= L.l_max) ? 1 : 0;
+    a.tree_ok = (a.c <= T.l_max) ? 1 : 0;
+    a.czd = grid_dim_dev(a.nz, a.glm, a.c);
+    a.cxd = grid_dim_dev(a.nx, a.glm, a.c);
+    a.pz_lo = 0;
+    a.pz_hi = 1 << 30;
+    a.work = T.work + T.work_off[lt];
+    a.n_work = T.work_off[lt + 1] - T.work_off[lt];
+}
+
+FillArgs base_fill_args(aprgpu_apr* apr) {
+    FillArgs a{};
+    a.leaf = apr->leaf.view();
+    a.tree = apr->tree.view();
+    a.glm = apr->leaf.l_max;
+    a.nz = apr->dims[0];
+    a.nx = apr->dims[1];
+    a.ny = apr->dims[2];
+    return a;
+}
+
+// Domain-partition check of validate (apr.hpp:103-131) without pixels: one lane
+// per interior node; every child cell whose origin lies in the image must be a
+// leaf or an interior node, and not both.  (Leaves never have a leaf ancestor
+// then: the ancestor would be an interior node too.)  min_unc = smallest
+// uncovered pixel's flat index (a cell's smallest pixel is its origin).
+__global__ void __launch_bounds__(256) k_partition_check(FillArgs a, int* dbl, unsigned long long* min_unc) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const LevelG pg = a.tree.g[a.lt];
+    const int s = 1 << (a.glm - a.c);  // child cell size
+    for (uint64_t wi = warp; wi < a.n_work; wi += nwarps) {
+        const uint32_t prow = a.work[wi];
+        const uint32_t loc = prow - pg.row0;
+        const int pz = static_cast<int>(loc / pg.xd), px = static_cast<int>(loc % pg.xd);
+        const uint32_t pb = a.tree.rb[prow], pe = a.tree.rb[prow + 1];
+        for (uint32_t j = pb + lane; j < pe; j += 32) {
+            const int py = a.tree.y[j];
+            const Links lk = a.links[j];
+            const uint32_t wl[4] = {lk.leaf.x, lk.leaf.y, lk.leaf.z, lk.leaf.w};
+            const uint32_t wt[4] = {lk.tree.x, lk.tree.y, lk.tree.z, lk.tree.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int cz = 2 * pz + (k >> 1), cx = 2 * px + (k & 1);
+                if (static_cast<int64_t>(cz) * s >= a.nz || static_cast<int64_t>(cx) * s >= a.nx) continue;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int cy = 2 * py + t;
+                    if (static_cast<int64_t>(cy) * s >= a.ny) continue;
+                    const uint32_t fl = a.leaf_ok ? (wl[k] >> (30 + t)) & 1u : 0u;
+                    const uint32_t ft = a.tree_ok ? (wt[k] >> (30 + t)) & 1u : 0u;
+                    if (fl && ft) atomicOr(dbl, 1);
+                    if (!fl && !ft) {
+                        const unsigned long long px0 =
+                            (static_cast<unsigned long long>(cz) * s * a.nx + static_cast<unsigned long long>(cx) * s) *
+                                a.ny +
+                            static_cast<unsigned long long>(cy) * s;
+                        atomicMin(min_unc, px0);
+                    }
+                }
+            }
+        }
+    }
+}
+
+}  // namespace
+
+// Child links of every interior node (structure only; built on first use).
+void ensure_tree_links(aprgpu_apr* apr, cudaStream_t s) {
+    if (apr->tree_links.p) return;
+    const DevAccess& L = apr->leaf;
+    const DevAccess& T = apr->tree;
+    if (T.n_particles == 0) return;
+    if (L.n_particles >= (1ull << 30) || T.n_particles >= (1ull << 30))
+        fail(APRGPU_ERR_CAPABILITY, "fill_tree: child links need fewer than 2^30 particles per access");
+    apr->tree_links.ensure(sizeof(Links) * T.n_particles);
+    FillArgs a = base_fill_args(apr);
+    a.links = apr->tree_links.as<Links>();
+    for (int lt = T.l_max; lt >= T.l_min; --lt) {
+        set_fill_level(a, L, T, lt);
+        if (a.n_work == 0) continue;
+        const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), apr->ctx->sm_count * 16);
+        k_fill_tree_level<true><<<grid, 256, 0, s>>>(a);
+        count_launch(apr->ctx);
+    }
+    APR_CUDA(cudaGetLastError());
+}
+
+// validate's partition property over the interior levels (k_partition_check);
+// the caller checks the coarsest level's own cells.
+void tree_partition_check(aprgpu_apr* apr, int* dbl, unsigned long long* min_unc, cudaStream_t s) {
+    const DevAccess& L = apr->leaf;
+    const DevAccess& T = apr->tree;
+    if (T.n_particles == 0) return;
+    ensure_tree_links(apr, s);
+    FillArgs a = base_fill_args(apr);
+    a.links = apr->tree_links.as<Links>();
+    for (int lt = T.l_max; lt >= T.l_min; --lt) {
+        set_fill_level(a, L, T, lt);
+        if (a.n_work == 0) continue;
+        const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), apr->ctx->sm_count * 16);
+        k_partition_check<<<grid, 256, 0, s>>>(a, dbl, min_unc);
+        count_launch(apr->ctx);
+    }
+    APR_CUDA(cudaGetLastError());
+}
+
 // fp64 sums (vsum, wsum) of interior levels [lt_lo, lt_hi] (finest first),
 // restricted to parent rows whose cells lie in the finest-level pixel planes
 // [z_lo, z_hi) (z_hi < 0: every row).  Slab-decomposed callers run the levels
@@ -441,51 +556,16 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
         apr->vsum.ensure(sizeof(double) * T.n_particles);
         apr->wsum.ensure(sizeof(double) * T.n_particles);
     }
-    FillArgs a{};
-    a.leaf = L.view();
-    a.tree = T.view();
+    FillArgs a = base_fill_args(apr);
     a.leaf_v = leaf;
     a.vsum = apr->vsum.as<double>();
     a.wsum = apr->wsum.as<double>();
-    a.glm = L.l_max;
-    a.nz = apr->dims[0];
-    a.nx = apr->dims[1];
-    a.ny = apr->dims[2];
-    const bool build = !apr->tree_links.p;
-    if (build) {
-        if (L.n_particles >= (1ull << 30) || T.n_particles >= (1ull << 30))
-            fail(APRGPU_ERR_CAPABILITY, "fill_tree: child links need fewer than 2^30 particles per access");
-        apr->tree_links.ensure(sizeof(Links) * T.n_particles);
-    }
+    ensure_tree_links(apr, s);
     a.links = apr->tree_links.as<Links>();
-    // first use: the links of every level (no slab restriction: they serve every slab)
-    for (int lt = build ? T.l_max : -1; lt >= T.l_min; --lt) {
-        a.lt = lt;
-        a.c = lt + 1;
-        a.leaf_ok = (a.c >= L.l_min && a.c <= L.l_max) ? 1 : 0;
-        a.tree_ok = (a.c <= T.l_max) ? 1 : 0;
-        a.czd = grid_dim_dev(a.nz, a.glm, a.c);
-        a.cxd = grid_dim_dev(a.nx, a.glm, a.c);
-        a.pz_lo = 0;
-        a.pz_hi = 1 << 30;
-        a.work = T.work + T.work_off[lt];
-        a.n_work = T.work_off[lt + 1] - T.work_off[lt];
-        if (a.n_work == 0) continue;
-        const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), ctx->sm_count * 16);
-        k_fill_tree_level<true><<<grid, 256, 0, s>>>(a);
-        count_launch(ctx);
-    }
     for (int lt = std::min(lt_hi, T.l_max); lt >= std::max(lt_lo, T.l_min); --lt) {
-        a.lt = lt;
-        a.c = lt + 1;
-        a.leaf_ok = (a.c >= L.l_min && a.c <= L.l_max) ? 1 : 0;
-        a.tree_ok = (a.c <= T.l_max) ? 1 : 0;
-        a.czd = grid_dim_dev(a.nz, a.glm, a.c);
-        a.cxd = grid_dim_dev(a.nx, a.glm, a.c);
+        set_fill_level(a, L, T, lt);
         a.pz_lo = z_hi < 0 ? 0 : (z_lo >> (a.glm - lt));
         a.pz_hi = z_hi < 0 ? (1 << 30) : ((z_hi + (1 << (a.glm - lt)) - 1) >> (a.glm - lt));
-        a.work = T.work + T.work_off[lt];
-        a.n_work = T.work_off[lt + 1] - T.work_off[lt];
         if (a.n_work == 0) continue;
         const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), ctx->sm_count * 16);
         k_fill_tree_level<false><<<grid, 256, 0, s>>>(a);
