@@ -37,7 +37,10 @@ typedef enum {
     APRGPU_ERR_CUDA = 4,
     APRGPU_ERR_NCCL = 5,
     APRGPU_ERR_OOM = 6,
-    APRGPU_ERR_INVALID = 7 /* bad argument (null pointer, unknown enum, ...) */
+    APRGPU_ERR_INVALID = 7,    /* bad argument (null pointer, unknown enum, ...) */
+    APRGPU_ERR_IO = 8,         /* aprkit::IoError            (errors.hpp:26-30) */
+    APRGPU_ERR_BAD_FORMAT = 9, /* aprkit::BadFormatError     (errors.hpp:32-36) */
+    APRGPU_ERR_TRUNCATED = 10  /* aprkit::TruncatedFileError (errors.hpp:38-41) */
 } aprgpu_status;
 
 enum { APRGPU_HOST = 0, APRGPU_DEVICE = 1 };
@@ -112,6 +115,33 @@ int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, u
 /* fill_tree (tree.hpp:110-150): leaf[n_particles] -> tree[n_tree]; fp64
  * accumulation in the reference's per-parent order, bit-exact. */
 int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream);
+
+/* ---- .apr container (io.hpp:102-183, docs/FORMATS.md) ---------------------- */
+/* BuildParams (apr.hpp:16-33) as stored in an .apr file: sigma_mode 0 constant /
+ * 1 local range; gradient_mode 0 central difference / 1 Sobel. */
+typedef struct {
+    double rel_error;
+    int sigma_mode;
+    double sigma_value;
+    int sigma_window;
+    double sigma_floor;
+    int gradient_mode;
+    int smoothing_passes;
+} aprgpu_build_params;
+
+/* load_apr / read_apr (io.hpp:131-183): the file straight into a device handle
+ * -- leaf and interior structure as stored, leaf values on the device
+ * (aprgpu_apr_values), build parameters (aprgpu_apr_params) -- after the
+ * reader's checks (same order and messages) and validate on the device.
+ * Errors: IO (cannot open), BAD_FORMAT (malformed, or validate's violation
+ * as "invalid APR structure: ..."), TRUNCATED (early end of file). */
+int aprgpu_load_apr(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out);
+/* save_apr / write_apr (io.hpp:106-126, 171-176): values[n_particles] (host or
+ * device) with the handle's structure and parameters; byte-identical to the
+ * reference's writer.  Handles not loaded from a file carry BuildParams'
+ * defaults, or build_apr's (E, constant sigma = intensity range). */
+int aprgpu_save_apr(aprgpu_apr* apr, const char* path, const float* values, int ptr_kind);
+int aprgpu_apr_params(const aprgpu_apr* apr, aprgpu_build_params* out);
 
 /* validate (apr.hpp:61-134) of a leaf access and its image dims, on the device
  * in O(particles + rows) instead of the reference's O(pixels) cover map: *ok = 1,
@@ -225,7 +255,7 @@ int aprgpu_tile_values(aprgpu_apr* src, aprgpu_apr* big, int tz, int tx, int ty,
                        float* big_values);
 
 /* Copies the particle values sampled by aprgpu_build_apr (sample_particles,
- * build.hpp:252-284) into out[n_particles]. */
+ * build.hpp:252-284) or read by aprgpu_load_apr into out[n_particles]. */
 int aprgpu_apr_values(const aprgpu_apr* apr, float* out, int ptr_kind);
 
 /* Number of kernel launches this context issued since creation (bench.py's

@@ -50,6 +50,9 @@ namespace gpu {
         case APRGPU_ERR_CAPABILITY: throw CapabilityError(m);
         case APRGPU_ERR_INTEGRITY: throw IntegrityError(m);
         case APRGPU_ERR_OOM: throw std::bad_alloc();
+        case APRGPU_ERR_IO: throw IoError(m);
+        case APRGPU_ERR_BAD_FORMAT: throw BadFormatError(m);
+        case APRGPU_ERR_TRUNCATED: throw TruncatedFileError(m);
         default: throw std::runtime_error("aprgpu: " + m);
     }
 }
@@ -258,4 +261,7 @@ inline LinearAccess download(aprgpu_apr* h, int which) {
 #define APRKIT_GPU_RUNTIME_DONE 1
 #ifdef APRKIT_GPU_RECONSTRUCT_OVERLAY
 #include "aprkit_gpu_reconstruct.hpp"
+#endif
+#ifdef APRKIT_GPU_APR_OVERLAY
+#include "aprkit_gpu_apr.hpp"
 #endif

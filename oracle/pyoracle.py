@@ -351,6 +351,9 @@ class Ref:
         L.ref_convolve.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]
         L.ref_reconstruct_level.argtypes = [vp, vp, vp, C.c_int, vp]
         L.ref_reconstruct_full.argtypes = [vp, vp, vp]
+        L.ref_save_apr.argtypes = [vp, vp, C.c_char_p]
+        L.ref_load_apr.restype = C.c_int
+        L.ref_load_apr.argtypes = [C.c_char_p, C.POINTER(vp), vp, C.c_uint64]
         L.ref_validate_arrays.restype = C.c_int
         L.ref_validate_arrays.argtypes = [C.c_int, C.c_int, vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64, vp,
                                           C.c_int, C.c_int, C.c_int, vp, C.c_uint64]
@@ -481,6 +484,17 @@ class Ref:
         tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
         self._chk(self.L.ref_reconstruct_level(apr.h, _p(v), None if tv is None else _p(tv), l, out.ctypes.data))
         return out
+
+    def save_apr(self, apr: "RefApr", values, path: str):
+        v = np.ascontiguousarray(values, np.float32)
+        self._chk(self.L.ref_save_apr(apr.h, _p(v), path.encode()))
+
+    def load_apr(self, path: str):
+        """(kind, message, RefApr or None): kind 0 ok, 1 IoError, 2 BadFormatError, 3 TruncatedFileError."""
+        h = C.c_void_p()
+        buf = C.create_string_buffer(512)
+        kind = self.L.ref_load_apr(path.encode(), C.byref(h), buf, 512)
+        return kind, buf.value.decode(), (RefApr(self, h.value) if kind == 0 else None)
 
     def validate_arrays(self, leaf, dims):
         """validate (apr.hpp:61-134) of a leaf access: (ok, message)."""

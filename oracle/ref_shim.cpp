@@ -240,6 +240,43 @@ REF_API std::uint64_t ref_apr_values(void* hp, float* out) {
 // validate (apr.hpp:61-134); returns 1 if ok
 REF_API int ref_validate(void* hp) { return aprkit::validate(static_cast<RefApr*>(hp)->apr).ok ? 1 : 0; }
 
+// save_apr (io.hpp:171-176) of a handle with the given leaf values
+REF_API int ref_save_apr(void* hp, const float* values, const char* path) {
+    return guarded([&] {
+        auto* h = static_cast<RefApr*>(hp);
+        aprkit::ParticleValues v(values, values + h->apr.access.particle_count());
+        aprkit::save_apr(path, h->apr, v);
+    });
+}
+
+// load_apr (io.hpp:178-183): 0 and the handle, or the exception's kind
+// (1 IoError, 2 BadFormatError, 3 TruncatedFileError) and message
+REF_API int ref_load_apr(const char* path, void** out, char* msg, std::uint64_t cap) {
+    auto put = [&](const std::string& m) {
+        if (msg && cap) {
+            const std::size_t n = std::min<std::size_t>(cap - 1, m.size());
+            std::memcpy(msg, m.data(), n);
+            msg[n] = 0;
+        }
+    };
+    try {
+        auto h = std::make_unique<RefApr>();
+        h->apr = aprkit::load_apr(path, h->values);
+        *out = h.release();
+        put("");
+        return 0;
+    } catch (const aprkit::TruncatedFileError& e) {
+        put(e.what());
+        return 3;
+    } catch (const aprkit::BadFormatError& e) {
+        put(e.what());
+        return 2;
+    } catch (const aprkit::IoError& e) {
+        put(e.what());
+        return 1;
+    }
+}
+
 // validate (apr.hpp:61-134) of raw leaf arrays (no tree is built: malformed
 // structures are the point); returns ok, the report's message into msg
 REF_API int ref_validate_arrays(int l_min, int l_max, const int* zd, const int* xd, const int* yd,

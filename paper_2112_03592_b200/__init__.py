@@ -11,7 +11,7 @@ from .aprkit import (APR, ConvolveOptions, Context, DeviceApr, DevicePyramid, Li
                      explicit_pyramid, fill_tree, flip_stencil, gaussian_stencil, grid_dim, identity_stencil,
                      init_tree_structure, make_pyramid, nonempty_row_index, rescale_stencil, restrict_stencil,
                      rl_apr, sobel_stencil)
-from .errors import (CapabilityError, CudaError, DeviceOutOfMemory, IntegrityError, InvalidArgument,  # noqa: F401
-                     RangeError)
+from .errors import (BadFormatError, CapabilityError, CudaError, DeviceOutOfMemory, IntegrityError,  # noqa: F401
+                     InvalidArgument, IoError, RangeError, TruncatedFileError)
 
 __version__ = "0.1.0"

@@ -37,6 +37,12 @@ class AccessInfo(C.Structure):
 _lib = None
 _lock = threading.Lock()
 
+class BuildParamsC(C.Structure):  # aprgpu_build_params
+    _fields_ = [("rel_error", C.c_double), ("sigma_mode", C.c_int), ("sigma_value", C.c_double),
+                ("sigma_window", C.c_int), ("sigma_floor", C.c_double), ("gradient_mode", C.c_int),
+                ("smoothing_passes", C.c_int)]
+
+
 class PatchSpecC(C.Structure):  # aprgpu_patch_spec
     _fields_ = [(n, C.c_int) for n in ("level", "z_begin", "z_end", "x_begin", "x_end", "pad", "pad_mode")]
 
@@ -84,6 +90,9 @@ _SIGS = {
     "aprgpu_build_apr": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                          C.POINTER(C.c_void_p)],
     "aprgpu_apr_values": [C.c_void_p, C.c_void_p, C.c_int],
+    "aprgpu_load_apr": [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)],
+    "aprgpu_save_apr": [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int],
+    "aprgpu_apr_params": [C.c_void_p, C.c_void_p],
     "aprgpu_validate_access": [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int), C.c_char_p, C.c_size_t],
     "aprgpu_reconstruct_level": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p],
     "aprgpu_reconstruct_patch": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p],

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import math
 from dataclasses import dataclass, field
 from typing import List, NamedTuple, Optional, Sequence
@@ -142,6 +143,48 @@ class APR:
             if self.tree_access is None:
                 self.tree_access = h.download(L.TREE)
         return h
+
+
+@dataclass
+class BuildParams:                                        # apr.hpp:16-33 (SigmaPolicy flattened)
+    rel_error: float = 0.1
+    sigma_mode: int = 0          # 0 constant, 1 local range
+    sigma_value: float = 1.0
+    sigma_window: int = 2
+    sigma_floor: float = 0.0
+    gradient_mode: int = 0       # 0 central difference, 1 Sobel
+    smoothing_passes: int = 0
+
+
+def load_apr(path: str, ctx: Optional["Context"] = None):
+    """load_apr (io.hpp:178-183): (APR, leaf values).  The file is read straight
+    into a device handle (validated on the device) and the host APR mirrors it;
+    apr.params holds the stored BuildParams."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    L.check(L.lib().aprgpu_load_apr(ctx.handle, os.fsencode(path), C.byref(h)))
+    dims = np.zeros(3, np.int32)
+    L.check(L.lib().aprgpu_apr_dims(h, _ptr(dims)))
+    dev = DeviceApr(ctx, h, dims)
+    apr = APR(dev.download(L.LEAF), dev.download(L.TREE), tuple(int(v) for v in dims))
+    apr._dev[ctx.device] = dev
+    values = np.empty(dev.n_particles, np.float32)
+    if values.size:
+        L.check(L.lib().aprgpu_apr_values(h, _ptr(values), L.HOST))
+    p = L.BuildParamsC()
+    L.check(L.lib().aprgpu_apr_params(h, C.byref(p)))
+    apr.params = BuildParams(p.rel_error, p.sigma_mode, p.sigma_value, p.sigma_window, p.sigma_floor,
+                             p.gradient_mode, p.smoothing_passes)
+    return apr, values
+
+
+def save_apr(path: str, apr: APR, values) -> None:
+    """save_apr (io.hpp:171-176): byte-identical to the reference's writer."""
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    if values.size != apr.access.particle_count():
+        raise RangeError("write_apr: value count does not match particle count")
+    dev = apr.device()
+    L.check(L.lib().aprgpu_save_apr(dev.handle, os.fsencode(path), _ptr(values) if values.size else None, L.HOST))
 
 
 @dataclass

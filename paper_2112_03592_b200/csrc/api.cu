@@ -1,8 +1,8 @@
-#include <algorithm>
 // The C-ABI (include/aprgpu.h): contexts, structure upload/download, stencil
 // pyramids, and the host/device-pointer front doors of fill_tree, convolve_apr
 // and rl_apr.  Exceptions never cross this boundary; aprgpu::Error carries the
 // status code that the reference-side shim maps back to aprkit's exceptions.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -1010,10 +1010,45 @@ int aprgpu_tile_values(aprgpu_apr* src, aprgpu_apr* big, int tz, int tx, int ty,
     });
 }
 
+int aprgpu_load_apr(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out) {
+    return guard([&] {
+        need(ctx && path && out, "null argument");
+        DeviceGuard g(ctx->device);
+        std::string msg;
+        const int st = aprgpu::load_apr_host(ctx, path, out, msg);
+        if (st != APRGPU_OK) fail(st, msg);
+    });
+}
+
+int aprgpu_save_apr(aprgpu_apr* apr, const char* path, const float* values, int ptr_kind) {
+    return guard([&] {
+        need(apr && path && (values || apr->leaf.n_particles == 0), "null argument");
+        need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
+        DeviceGuard g(apr->ctx->device);
+        std::vector<float> host;
+        const float* v = values;
+        if (ptr_kind == APRGPU_DEVICE) {
+            host.resize(apr->leaf.n_particles);
+            APR_CUDA(cudaMemcpy(host.data(), values, 4 * host.size(), cudaMemcpyDeviceToHost));
+            v = host.data();
+        }
+        std::string msg;
+        const int st = aprgpu::save_apr_host(apr, path, v, msg);
+        if (st != APRGPU_OK) fail(st, msg);
+    });
+}
+
+int aprgpu_apr_params(const aprgpu_apr* apr, aprgpu_build_params* out) {
+    return guard([&] {
+        need(apr && out, "null argument");
+        *out = apr->params;
+    });
+}
+
 int aprgpu_apr_values(const aprgpu_apr* apr, float* out, int ptr_kind) {
     return guard([&] {
         need(apr && out, "null argument");
-        if (!apr->built_values.p) fail(APRGPU_ERR_INVALID, "this APR was not built by aprgpu_build_apr");
+        if (!apr->built_values.p) fail(APRGPU_ERR_INVALID, "this APR was neither built (aprgpu_build_apr) nor loaded");
         DeviceGuard g(apr->ctx->device);
         const uint64_t n = apr->leaf.n_particles;
         APR_CUDA(cudaMemcpy(out, apr->built_values.p, 4 * n,

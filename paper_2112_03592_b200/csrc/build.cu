@@ -363,6 +363,7 @@ void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny,
     const float range = mm[1] - mm[0];
     const double floor_value = 1e-3 * std::max(1e-30f, range);
     const double sigma = static_cast<double>(static_cast<float>(std::max(static_cast<double>(range), floor_value)));
+    apr->params = aprgpu_build_params{rel_error, 0, static_cast<double>(range), 2, 0.0, 0, 0};  // SigmaPolicy::constant(range)
     const double omega = static_cast<double>(1u << l_max);
 
     // dense per-level grids

@@ -107,7 +107,9 @@ struct aprgpu_apr {
     aprgpu::GpuBuf h_in, h_tree, h_out;    // staging for host-pointer calls
     aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
     aprgpu::GpuBuf tmp;                    // misc
-    aprgpu::GpuBuf built_values;           // leaf values sampled by aprgpu_build_apr
+    aprgpu::GpuBuf built_values;           // leaf values sampled by aprgpu_build_apr / read by aprgpu_load_apr
+    // BuildParams (apr.hpp:28-33): the reference's defaults unless built or loaded
+    aprgpu_build_params params{0.1, 0, 1.0, 2, 0.0, 0, 0};
 };
 
 struct aprgpu_pyramid {
@@ -148,6 +150,10 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
 void fill_tree_finalize(aprgpu_apr* apr, float* tree, cudaStream_t s);
 void ensure_tree_links(aprgpu_apr* apr, cudaStream_t s);
 void tree_partition_check(aprgpu_apr* apr, int* dbl, unsigned long long* min_unc, cudaStream_t s);
+
+// io.cpp: the .apr container (docs/FORMATS.md)
+int load_apr_host(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out, std::string& msg);
+int save_apr_host(const aprgpu_apr* apr, const char* path, const float* values, std::string& msg);
 
 // validate.cu: the per-row part of validate (apr.hpp:85-101) plus the cell
 // origins' domain check; first_y = min(particle << 1 | out-of-grid)

@@ -34,6 +34,18 @@ class InvalidArgument(ValueError):
     """Bad argument at the C-ABI (null pointer, unknown enum, ...)."""
 
 
+class IoError(RuntimeError):
+    """aprkit::IoError: a file that cannot be opened, read or written."""
+
+
+class BadFormatError(IoError):
+    """aprkit::BadFormatError: malformed file content."""
+
+
+class TruncatedFileError(IoError):
+    """aprkit::TruncatedFileError: the stream ends early."""
+
+
 _BY_STATUS = {
     1: RangeError,
     2: CapabilityError,
@@ -42,6 +54,9 @@ _BY_STATUS = {
     5: NcclError,
     6: DeviceOutOfMemory,
     7: InvalidArgument,
+    8: IoError,
+    9: BadFormatError,
+    10: TruncatedFileError,
 }
 
 
