@@ -259,6 +259,7 @@ def run_ours(args, rank, world):
     # reconstruct_full (reconstruct.hpp:87-90) of the same APR: the dense image,
     # bound by writing it (4 bytes per pixel); skipped when it would not fit easily
     recon = None
+    pixels_conv = None
     if 4 * n_pix <= 16e9:
         img = torch.empty(n_pix, dtype=torch.float32, device="cuda")
         lmax = int(dapr.info(L.LEAF).l_max)
@@ -270,11 +271,29 @@ def run_ours(args, rank, world):
             e1.record(stream)
             e1.synchronize()
             rt.append(e0.elapsed_time(e1) / 1e3)
-        del img
         tr = min(rt[1:])
         recon = {"ms": round(tr * 1e3, 4), "write_gbs": round(4 * n_pix / tr / 1e9, 1),
                  "frac_of_peak": round(4 * n_pix / tr / 1e9 / peaks()[0], 4),
                  "note": "reconstruct_full on the device (k_reconstruct), output bytes / time, best of 2 warm runs"}
+        # the pixel-space baseline on the same image (convolve_pixels, convolve.hpp:48-98;
+        # the paper's APR-vs-pixels comparison): same stencil, same accumulation mode
+        if 8 * n_pix <= 24e9:
+            pout = torch.empty_like(img)
+            pt = []
+            for i in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                P.convolve_pixels_ptr(ctx, img.data_ptr(), dapr.dims, w, 1, accum, pout.data_ptr(), s)
+                e1.record(stream)
+                e1.synchronize()
+                pt.append(e0.elapsed_time(e1) / 1e3)
+            del pout
+            tpx = min(pt[1:])
+            pixels_conv = {"ms": round(tpx * 1e3, 4), "gbs_pixel_equiv": round(4 * n_pix / tpx / 1e9, 1),
+                           "hbm_frac": round(8 * n_pix / tpx / 1e9 / peaks()[0], 4),
+                           "note": "convolve_pixels of the reconstructed image (k_convolve_pixels), best of 2 "
+                                   "warm runs; includes a stream sync for the weight buffer"}
+        del img
 
     def agg(x):
         t = float(np.mean(x))
@@ -329,6 +348,9 @@ def run_ours(args, rank, world):
     }
     if recon:
         res["reconstruct_full"] = recon
+    if pixels_conv:
+        pixels_conv["apr_speedup"] = round(pixels_conv["ms"] / (tc * 1e3), 2)
+        res["convolve_pixels"] = pixels_conv
     if rank == 0 and not args.no_cpu_baseline and apr is not None:
         res["cpu_baseline"] = cpu_baseline(apr, values, tv[:dapr.n_tree].cpu().numpy(), pyr, args)
     return res

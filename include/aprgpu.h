@@ -116,6 +116,14 @@ int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, u
  * accumulation in the reference's per-parent order, bit-exact. */
 int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream);
 
+/* ---- dense pixel convolution (convolve.hpp:48-98) --------------------------- */
+/* convolve_pixels: out = w * in over an nz x nx x ny volume ((z, x, y), y fastest),
+ * true-convolution convention, reflect / zero padding, taps in the reference's
+ * order skipping zero weights; EXACT accumulation is bit-identical.  w[kz*kx*ky]
+ * is always a host array.  CAPABILITY: an extent above 13; RANGE: even extents. */
+int aprgpu_convolve_pixels(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w, int kz, int kx,
+                           int ky, int pad_mode, int accum, float* out, int ptr_kind, void* stream);
+
 /* ---- .apr container (io.hpp:102-183, docs/FORMATS.md) ---------------------- */
 /* BuildParams (apr.hpp:16-33) as stored in an .apr file: sigma_mode 0 constant /
  * 1 local range; gradient_mode 0 central difference / 1 Sobel. */

@@ -7,18 +7,36 @@
 // B200 path through the C-ABI (include/aprgpu.h):
 //   convolve_apr        convolve.hpp:220-303  -> aprgpu_convolve
 //   nonempty_row_index  convolve.hpp:32-44    -> aprgpu_row_index
+//   convolve_pixels     convolve.hpp:48-98    -> aprgpu_convolve_pixels (the pixel baseline)
 // Signatures, argument meaning and exceptions are the reference's.
 #pragma once
 
 #define convolve_apr convolve_apr_reference_cpu_
 #define nonempty_row_index nonempty_row_index_reference_cpu_
+#define convolve_pixels convolve_pixels_reference_cpu_
 #include_next "aprkit/convolve.hpp"
 #undef convolve_apr
 #undef nonempty_row_index
+#undef convolve_pixels
 
 #include "aprkit_gpu.hpp"
 
 namespace aprkit {
+
+// Dense pixel convolution on the device (convolve.hpp:48-98); EXACT unless
+// $APRGPU_ACCUM=fast, like convolve_apr.  threads is accepted for API parity.
+inline PixelVolume convolve_pixels(const PixelVolume& v, const Stencil& w, PadMode pad, int threads = 0) {
+    (void)threads;
+    if (w.kz > kMaxStencilExtent || w.kx > kMaxStencilExtent || w.ky > kMaxStencilExtent)
+        throw CapabilityError("convolve_pixels: stencil extent exceeds the supported maximum");
+    PixelVolume out(v.nz, v.nx, v.ny);
+    if (out.size() == 0) return out;
+    gpu::Runtime& rt = gpu::Runtime::get();
+    gpu::check(aprgpu_convolve_pixels(rt.ctx(), v.values.data(), v.nz, v.nx, v.ny, w.weights.data(), w.kz, w.kx, w.ky,
+                                      pad == PadMode::Zero ? APRGPU_PAD_ZERO : APRGPU_PAD_REFLECT, rt.accum(),
+                                      out.values.data(), APRGPU_HOST, nullptr));
+    return out;
+}
 
 // Exact per-level row occupancy, computed on the device (convolve.hpp:32-44).
 inline std::vector<std::vector<RowSpan>> nonempty_row_index(const LinearAccess& a) {

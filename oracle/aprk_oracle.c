@@ -387,6 +387,50 @@ void orc_reconstruct_patch(const orc_access* leaf, const float* values, const or
     free(row);
 }
 
+void orc_convolve_pixels(const float* v, int nz, int nx, int ny, const float* w, int kz, int kx, int ky,
+                         int pad, float* out) {
+    /* convolve.hpp:48-98: pad (reflect_index or zeros) by the half-extents, then
+     * per output a double accumulator over (az, ax, ay), zero weights skipped */
+    const int hz = kz / 2, hx = kx / 2, hy = ky / 2;
+    const int pz = nz + 2 * hz, px = nx + 2 * hx, py = ny + 2 * hy;
+    float* padded = (float*)calloc((size_t)pz * px * py, sizeof(float));
+    for (int z = 0; z < pz; ++z) {
+        const int sz = z - hz, zo = sz < 0 || sz >= nz;
+        if (zo && pad == 0) continue;
+        const int zr = zo ? orc_reflect_index(sz, nz) : sz;
+        for (int x = 0; x < px; ++x) {
+            const int sx = x - hx, xo = sx < 0 || sx >= nx;
+            if (xo && pad == 0) continue;
+            const int xr = xo ? orc_reflect_index(sx, nx) : sx;
+            float* dst = padded + ((size_t)z * px + x) * py;
+            const float* src = v + ((size_t)zr * nx + xr) * ny;
+            memcpy(dst + hy, src, sizeof(float) * (size_t)ny);
+            if (pad == 1)
+                for (int p = 0; p < hy; ++p) {
+                    dst[p] = src[orc_reflect_index(p - hy, ny)];
+                    dst[hy + ny + p] = src[orc_reflect_index(ny + p, ny)];
+                }
+        }
+    }
+    double* acc = (double*)malloc(sizeof(double) * (size_t)(ny > 0 ? ny : 1));
+    for (int z = 0; z < nz; ++z)
+        for (int x = 0; x < nx; ++x) {
+            for (int y = 0; y < ny; ++y) acc[y] = 0.0;
+            for (int az = 0; az < kz; ++az)
+                for (int ax = 0; ax < kx; ++ax)
+                    for (int ay = 0; ay < ky; ++ay) {
+                        const float wv = w[((size_t)az * kx + ax) * ky + ay];
+                        if (wv == 0.0f) continue;
+                        const float* src = padded + ((size_t)(z + 2 * hz - az) * px + (x + 2 * hx - ax)) * py + (2 * hy - ay);
+                        for (int y = 0; y < ny; ++y) acc[y] += (double)wv * (double)src[y];
+                    }
+            float* dst = out + ((size_t)z * nx + x) * ny;
+            for (int y = 0; y < ny; ++y) dst[y] = (float)acc[y];
+        }
+    free(acc);
+    free(padded);
+}
+
 /* -------------------------------------------------------------- stencil ---- */
 
 static int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }

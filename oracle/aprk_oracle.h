@@ -80,6 +80,10 @@ void orc_reconstruct_level(const orc_access* leaf, const float* values, const or
 void orc_reconstruct_patch(const orc_access* leaf, const float* values, const orc_access* tree,
                            const float* tree_values, const int spec[7], float* out);
 
+/* convolve_pixels (convolve.hpp:48-98): out[nz*nx*ny]; pad 0 Zero, 1 Reflect */
+void orc_convolve_pixels(const float* v, int nz, int nx, int ny, const float* w, int kz, int kx, int ky,
+                         int pad, float* out);
+
 /* restrict_stencil (stencil.hpp:127-160).  out_k3 receives the extents; out may
  * be NULL to query them. */
 void orc_restrict_stencil(const float* w, int kz, int kx, int ky, int delta, int out_k3[3],

@@ -97,6 +97,7 @@ class Oracle:
         L.orc_fill_tree.argtypes = [vp, vp, vp, vp, vp]
         L.orc_reconstruct_level.argtypes = [vp, vp, vp, vp, C.c_int, vp]
         L.orc_reconstruct_patch.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.orc_convolve_pixels.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
         L.orc_validate.restype = C.c_int
         L.orc_validate.argtypes = [vp, vp, vp, C.c_size_t]
         L.orc_restrict_stencil.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
@@ -151,6 +152,15 @@ class Oracle:
         tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
         self.L.orc_reconstruct_level(C.byref(la), _p(v), C.byref(ta), None if tv is None else _p(tv), l,
                                      out.ctypes.data)
+        return out
+
+    def convolve_pixels(self, vol: np.ndarray, w: np.ndarray, k3, pad: int) -> np.ndarray:
+        v = np.ascontiguousarray(vol, np.float32)
+        ww = np.ascontiguousarray(w, np.float32).reshape(-1)
+        out = np.empty_like(v)
+        nz, nx, ny = v.shape
+        self.L.orc_convolve_pixels(v.ctypes.data, nz, nx, ny, ww.ctypes.data, int(k3[0]), int(k3[1]), int(k3[2]),
+                                   int(pad), out.ctypes.data)
         return out
 
     def validate(self, leaf, dims):
@@ -352,6 +362,7 @@ class Ref:
         L.ref_reconstruct_level.argtypes = [vp, vp, vp, C.c_int, vp]
         L.ref_reconstruct_full.argtypes = [vp, vp, vp]
         L.ref_save_apr.argtypes = [vp, vp, C.c_char_p]
+        L.ref_convolve_pixels.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
         L.ref_load_apr.restype = C.c_int
         L.ref_load_apr.argtypes = [C.c_char_p, C.POINTER(vp), vp, C.c_uint64]
         L.ref_validate_arrays.restype = C.c_int
@@ -483,6 +494,15 @@ class Ref:
         v = np.ascontiguousarray(values, np.float32)
         tv = None if tree_values is None else np.ascontiguousarray(tree_values, np.float32)
         self._chk(self.L.ref_reconstruct_level(apr.h, _p(v), None if tv is None else _p(tv), l, out.ctypes.data))
+        return out
+
+    def convolve_pixels(self, vol: np.ndarray, w: np.ndarray, k3, pad: int) -> np.ndarray:
+        v = np.ascontiguousarray(vol, np.float32)
+        ww = np.ascontiguousarray(w, np.float32).reshape(-1)
+        out = np.empty_like(v)
+        nz, nx, ny = v.shape
+        self._chk(self.L.ref_convolve_pixels(v.ctypes.data, nz, nx, ny, ww.ctypes.data, int(k3[0]), int(k3[1]),
+                                             int(k3[2]), int(pad), out.ctypes.data))
         return out
 
     def save_apr(self, apr: "RefApr", values, path: str):

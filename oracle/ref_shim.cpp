@@ -240,6 +240,19 @@ REF_API std::uint64_t ref_apr_values(void* hp, float* out) {
 // validate (apr.hpp:61-134); returns 1 if ok
 REF_API int ref_validate(void* hp) { return aprkit::validate(static_cast<RefApr*>(hp)->apr).ok ? 1 : 0; }
 
+// convolve_pixels (convolve.hpp:48-98); pad 0 Zero, 1 Reflect
+REF_API int ref_convolve_pixels(const float* v, int nz, int nx, int ny, const float* w, int kz, int kx, int ky,
+                                int pad, float* out) {
+    return guarded([&] {
+        aprkit::PixelVolume vol(nz, nx, ny);
+        std::memcpy(vol.values.data(), v, 4 * vol.size());
+        aprkit::Stencil st(kz, kx, ky);
+        std::memcpy(st.weights.data(), w, 4 * st.weights.size());
+        auto o = aprkit::convolve_pixels(vol, st, pad == 0 ? aprkit::PadMode::Zero : aprkit::PadMode::Reflect, 1);
+        std::memcpy(out, o.values.data(), 4 * o.size());
+    });
+}
+
 // save_apr (io.hpp:171-176) of a handle with the given leaf values
 REF_API int ref_save_apr(void* hp, const float* values, const char* path) {
     return guarded([&] {

@@ -90,6 +90,8 @@ _SIGS = {
     "aprgpu_build_apr": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                          C.POINTER(C.c_void_p)],
     "aprgpu_apr_values": [C.c_void_p, C.c_void_p, C.c_int],
+    "aprgpu_convolve_pixels": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                               C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p],
     "aprgpu_load_apr": [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)],
     "aprgpu_save_apr": [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int],
     "aprgpu_apr_params": [C.c_void_p, C.c_void_p],

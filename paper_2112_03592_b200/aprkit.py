@@ -605,6 +605,34 @@ def convolve_apr(apr: APR, values, tree_values, pyramid: StencilPyramid, pad: Pa
     return dev.convolve(values, tree_values, pyramid.device(dev.ctx), int(pad), _accum(opt.accum))
 
 
+def convolve_pixels(v: np.ndarray, w: Stencil, pad: PadMode = PadMode.Reflect, threads: int = 0,
+                    accum: str = "exact", ctx: Optional["Context"] = None) -> np.ndarray:
+    """convolve.hpp:48-98 on the device: v is (nz, nx, ny) float32, y fastest.
+    accum "exact" (default, bit-identical) or "fast" (fp32); threads is accepted
+    for API parity."""
+    del threads
+    if w.kz > kMaxStencilExtent or w.kx > kMaxStencilExtent or w.ky > kMaxStencilExtent:
+        raise CapabilityError("convolve_pixels: stencil extent exceeds the supported maximum")
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    if v.ndim != 3:
+        raise RangeError("convolve_pixels: expected a (nz, nx, ny) volume")
+    ctx = ctx or default_context()
+    out = np.empty_like(v)
+    wt = np.ascontiguousarray(w.weights, dtype=np.float32)
+    L.check(L.lib().aprgpu_convolve_pixels(ctx.handle, _ptr(v) if v.size else _ptr(wt), *v.shape, _ptr(wt), w.kz,
+                                           w.kx, w.ky, int(pad), _accum(accum), _ptr(out) if v.size else _ptr(wt),
+                                           L.HOST, None))
+    return out
+
+
+def convolve_pixels_ptr(ctx: "Context", in_ptr: int, dims, w: Stencil, pad: int, accum: int, out_ptr: int,
+                        stream: int = 0) -> None:
+    """Device-pointer convolve_pixels (stream-ordered)."""
+    wt = np.ascontiguousarray(w.weights, dtype=np.float32)
+    L.check(L.lib().aprgpu_convolve_pixels(ctx.handle, in_ptr, int(dims[0]), int(dims[1]), int(dims[2]), _ptr(wt),
+                                           w.kz, w.kx, w.ky, int(pad), accum, out_ptr, L.DEVICE, stream or None))
+
+
 @dataclass
 class PatchSpec:                                          # reconstruct.hpp:28-35
     level: int = 0

@@ -1010,6 +1010,38 @@ int aprgpu_tile_values(aprgpu_apr* src, aprgpu_apr* big, int tz, int tx, int ty,
     });
 }
 
+int aprgpu_convolve_pixels(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w, int kz, int kx,
+                           int ky, int pad_mode, int accum, float* out, int ptr_kind, void* stream) {
+    return guard([&] {
+        need(ctx && in && w && out, "null argument");
+        need(pad_mode == APRGPU_PAD_ZERO || pad_mode == APRGPU_PAD_REFLECT, "bad pad mode");
+        need(accum == APRGPU_ACCUM_EXACT || accum == APRGPU_ACCUM_FAST, "bad accumulation mode");
+        need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
+        need(nz >= 0 && nx >= 0 && ny >= 0, "negative volume dims");
+        const aprgpu::HostStencil hs = make_host_stencil(w, kz, kx, ky);
+        if (kz > 13 || kx > 13 || ky > 13)
+            fail(APRGPU_ERR_CAPABILITY, "convolve_pixels: stencil extent exceeds the supported maximum");
+        DeviceGuard g(ctx->device);
+        cudaStream_t s = aprgpu::pick_stream(ctx, stream);
+        const uint64_t n = static_cast<uint64_t>(nz) * nx * ny;
+        aprgpu::GpuBuf wd, vin, vout;
+        wd.ensure(4 * hs.w.size());
+        APR_CUDA(cudaMemcpyAsync(wd.p, hs.w.data(), 4 * hs.w.size(), cudaMemcpyHostToDevice, s));
+        const float* src = in;
+        float* dst = out;
+        if (ptr_kind == APRGPU_HOST) {
+            vin.ensure(4 * n + 4);
+            vout.ensure(4 * n + 4);
+            APR_CUDA(cudaMemcpyAsync(vin.p, in, 4 * n, cudaMemcpyHostToDevice, s));
+            src = vin.as<float>();
+            dst = vout.as<float>();
+        }
+        aprgpu::convolve_pixels_device(ctx, src, nz, nx, ny, wd.as<float>(), kz, kx, ky, pad_mode, accum, dst, s);
+        if (ptr_kind == APRGPU_HOST) APR_CUDA(cudaMemcpyAsync(out, dst, 4 * n, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));  // (the weights' buffer is released on return)
+    });
+}
+
 int aprgpu_load_apr(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out) {
     return guard([&] {
         need(ctx && path && out, "null argument");

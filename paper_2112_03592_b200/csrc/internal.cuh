@@ -151,6 +151,10 @@ void fill_tree_finalize(aprgpu_apr* apr, float* tree, cudaStream_t s);
 void ensure_tree_links(aprgpu_apr* apr, cudaStream_t s);
 void tree_partition_check(aprgpu_apr* apr, int* dbl, unsigned long long* min_unc, cudaStream_t s);
 
+// pixels.cu: convolve_pixels (convolve.hpp:48-98); w_dev = kz*kx*ky device floats
+void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w_dev, int kz,
+                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s);
+
 // io.cpp: the .apr container (docs/FORMATS.md)
 int load_apr_host(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out, std::string& msg);
 int save_apr_host(const aprgpu_apr* apr, const char* path, const float* values, std::string& msg);

@@ -1,0 +1,215 @@
+// Dense pixel convolution on the device: convolve_pixels (convolve.hpp:48-98),
+// the pixel-space baseline of the paper's APR-vs-pixels comparison
+// (SURVEY §8f row 4).
+//
+// o(p) = sum_r w(r) u(p - r), true-convolution convention, the volume padded by
+// reflect_index or zeros.  One CTA per 8 (z) x 8 (x) x kPy (y) output tile: the
+// tile's (8 + 2hz) x (8 + 2hx) x (kPy + 2hy) input box is staged in shared
+// memory (padding applied on load), then each thread evaluates 4 consecutive
+// y outputs of one (z, x) column, taps in the reference's order (az, ax, ay)
+// skipping zero weights (:86-88): EXACT = fp64 accumulation of exact products
+// (bit-identical), FAST = fp32 FMA.  Extents up to kMaxStencilExtent = 13.
+#include "common.cuh"
+
+namespace aprgpu {
+namespace {
+
+constexpr int kPz = 8, kPx = 8, kPy = 64, kPixThreads = 256, kPixMaxK = 13;
+
+struct PixArgs {
+    const float* in;
+    float* out;
+    int nz, nx, ny;
+    int kz, kx, ky;
+    int pad;
+    const float* w;  // kz * kx * ky
+};
+
+__device__ __forceinline__ int reflect_p(int i, int n) {  // reflect_index (reconstruct.hpp:16-25)
+    while (i < 0 || i >= n) i = i < 0 ? -i - 1 : 2 * n - 1 - i;
+    return i;
+}
+
+template <typename Acc>
+__global__ void __launch_bounds__(kPixThreads) k_convolve_pixels(PixArgs a, int tyd, int txd) {
+    extern __shared__ __align__(16) float box[];
+    __shared__ float W[kPixMaxK * kPixMaxK * kPixMaxK];
+    const int hz = a.kz / 2, hx = a.kx / 2, hy = a.ky / 2;
+    const int BZ = kPz + 2 * hz, BX = kPx + 2 * hx, BY = kPy + 2 * hy;
+    const int tid = threadIdx.x;
+    const int ty = blockIdx.x % tyd, t2 = blockIdx.x / tyd;
+    const int tx = t2 % txd, tz = t2 / txd;
+    const int z0 = tz * kPz, x0 = tx * kPx, y0 = ty * kPy;
+    const int KW = a.kz * a.kx * a.ky;
+    for (int i = tid; i < KW; i += kPixThreads) W[i] = a.w[i];
+    // stage the box: cell (bz, bx, by) is padded-volume (z0 + bz, x0 + bx, y0 + by),
+    // i.e. input (z0 + bz - hz, ...) reflected or zero
+    const int nb = BZ * BX * BY;
+    for (int i = tid; i < nb; i += kPixThreads) {
+        const int bz = i / (BX * BY), rem = i - bz * (BX * BY);
+        const int bx = rem / BY, by = rem - bx * BY;
+        int z = z0 + bz - hz, x = x0 + bx - hx, y = y0 + by - hy;
+        const bool out = z < 0 || z >= a.nz || x < 0 || x >= a.nx || y < 0 || y >= a.ny;
+        float v = 0.0f;
+        if (!out) {
+            v = __ldg(a.in + (static_cast<size_t>(z) * a.nx + x) * a.ny + y);
+        } else if (a.pad == APRGPU_PAD_REFLECT && z < a.nz + 2 * hz && x < a.nx + 2 * hx && y < a.ny + 2 * hy) {
+            z = reflect_p(z, a.nz);
+            x = reflect_p(x, a.nx);
+            y = reflect_p(y, a.ny);
+            v = __ldg(a.in + (static_cast<size_t>(z) * a.nx + x) * a.ny + y);
+        }
+        box[i] = v;
+    }
+    __syncthreads();
+    // 64 (z, x) columns x 16 groups of 4 y outputs
+    for (int job = tid; job < kPz * kPx * (kPy / 4); job += kPixThreads) {
+        const int col = job / (kPy / 4), g = job - col * (kPy / 4);
+        const int oz = col / kPx, ox = col - oz * kPx, oy = 4 * g;
+        if (z0 + oz >= a.nz || x0 + ox >= a.nx || y0 + oy >= a.ny) continue;
+        Acc acc[4] = {Acc(0), Acc(0), Acc(0), Acc(0)};
+        // output (oz, ox, oy + j) reads padded (z + 2hz - az, x + 2hx - ax, y + 2hy - ay)
+        for (int az = 0; az < a.kz; ++az)
+            for (int ax = 0; ax < a.kx; ++ax) {
+                const float* row = box + ((oz + 2 * hz - az) * BX + (ox + 2 * hx - ax)) * BY + oy + 2 * hy;
+                const float* wr = W + (az * a.kx + ax) * a.ky;
+                for (int ay = 0; ay < a.ky; ++ay) {
+                    const float wv = wr[ay];
+                    if (wv == 0.0f) continue;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        acc[j] = fma(static_cast<Acc>(wv), static_cast<Acc>(row[j - ay]), acc[j]);
+                }
+            }
+        float* dst = a.out + (static_cast<size_t>(z0 + oz) * a.nx + (x0 + ox)) * a.ny + y0 + oy;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (y0 + oy + j < a.ny) dst[j] = static_cast<float>(acc[j]);
+    }
+}
+
+// Isotropic K^3 (K = 3, 5): the same tile, staged row by row (a warp per box
+// row, lanes along y: coalesced loads, one reflection per row), weights in
+// registers, each thread one (z, x) column x 8 consecutive y outputs from a
+// sliding register window of 8 + K - 1 cells per (az, ax) row.
+constexpr int kIsoPy = 64;
+template <typename Acc, int K>
+__global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_iso(PixArgs a, int tyd, int txd) {
+    constexpr int kPy = kIsoPy;
+    constexpr int H = K / 2, BZ = kPz + 2 * H, BX = kPx + 2 * H, BY = kPy + 2 * H, RY = 8, NW = RY + K - 1;
+    extern __shared__ __align__(16) float box[];  // BZ * BX * BY
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ty = blockIdx.x % tyd, t2 = blockIdx.x / tyd;
+    const int tx = t2 % txd, tz = t2 / txd;
+    const int z0 = tz * kPz, x0 = tx * kPx, y0 = ty * kPy;
+    for (int r = warp; r < BZ * BX; r += kPixThreads / 32) {
+        const int bz = r / BX, bx = r - bz * BX;
+        int z = z0 + bz - H, x = x0 + bx - H;
+        const bool row_out = z < 0 || z >= a.nz || x < 0 || x >= a.nx;
+        float* dst = box + r * BY;
+        if (row_out && a.pad == APRGPU_PAD_ZERO) {
+            for (int by = lane; by < BY; by += 32) dst[by] = 0.0f;
+            continue;
+        }
+        z = reflect_p(z, a.nz);
+        x = reflect_p(x, a.nx);
+        const float* src = a.in + (static_cast<size_t>(z) * a.nx + x) * a.ny;
+
+        for (int by = lane; by < BY; by += 32) {
+            const int y = y0 + by - H;
+            float v = 0.0f;
+            if (y >= 0 && y < a.ny) v = __ldg(src + y);
+            else if (a.pad == APRGPU_PAD_REFLECT) v = __ldg(src + reflect_p(y, a.ny));
+            dst[by] = v;
+        }
+    }
+    float w[K * K * K];
+#pragma unroll
+    for (int i = 0; i < K * K * K; ++i) w[i] = __ldg(a.w + i);
+    __syncthreads();
+    for (int job = tid; job < kPz * kPx * (kPy / RY); job += kPixThreads) {
+        const int col = job / (kPy / RY), g = job - col * (kPy / RY);
+        const int oz = col / kPx, ox = col - oz * kPx, oy = RY * g;
+        if (z0 + oz >= a.nz || x0 + ox >= a.nx || y0 + oy >= a.ny) continue;
+        Acc acc[RY];
+#pragma unroll
+        for (int j = 0; j < RY; ++j) acc[j] = Acc(0);
+#pragma unroll
+        for (int az = 0; az < K; ++az)
+#pragma unroll
+            for (int ax = 0; ax < K; ++ax) {
+                // output oy + j reads box y index oy + j + 2H - ay
+                const float* row = box + ((oz + 2 * H - az) * BX + (ox + 2 * H - ax)) * BY + oy;
+                float win[NW];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) win[i] = row[i];
+#pragma unroll
+                for (int ay = 0; ay < K; ++ay) {
+                    const float wv = w[(az * K + ax) * K + ay];
+                    if (wv == 0.0f) continue;  // (convolve.hpp:86-88)
+#pragma unroll
+                    for (int j = 0; j < RY; ++j)
+                        acc[j] = fma(static_cast<Acc>(wv), static_cast<Acc>(win[j + 2 * H - ay]), acc[j]);
+                }
+            }
+        float* dst = a.out + (static_cast<size_t>(z0 + oz) * a.nx + (x0 + ox)) * a.ny + y0 + oy;
+#pragma unroll
+        for (int j = 0; j < RY; ++j)
+            if (y0 + oy + j < a.ny) dst[j] = static_cast<float>(acc[j]);
+    }
+}
+
+}  // namespace
+
+void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w_dev, int kz,
+                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s) {
+    if (kz > kPixMaxK || kx > kPixMaxK || ky > kPixMaxK)
+        fail(APRGPU_ERR_CAPABILITY, "convolve_pixels: stencil extent exceeds the supported maximum");
+    if (nz <= 0 || nx <= 0 || ny <= 0) return;
+    PixArgs a{in, out, nz, nx, ny, kz, kx, ky, pad, w_dev};
+    const int tzd = (nz + kPz - 1) / kPz, txd = (nx + kPx - 1) / kPx, tyd = (ny + kPy - 1) / kPy;
+    const uint64_t blocks = static_cast<uint64_t>(tzd) * txd * tyd;
+    if (blocks >= (1ull << 31)) fail(APRGPU_ERR_CAPABILITY, "convolve_pixels: volume too large");
+    if (kz == kx && kx == ky && (kz == 3 || kz == 5)) {
+        const bool ex = accum == APRGPU_ACCUM_EXACT;
+        const int ityd = (ny + kIsoPy - 1) / kIsoPy;
+        const unsigned g = static_cast<unsigned>(static_cast<uint64_t>(tzd) * txd * ityd);
+        const int h = kz / 2;
+        const int ib = (kPz + 2 * h) * (kPx + 2 * h) * (kIsoPy + 2 * h) * static_cast<int>(sizeof(float));
+        static const bool iattr = [] {
+            const int mx = (kPz + 4) * (kPx + 4) * (kIsoPy + 4) * static_cast<int>(sizeof(float));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<double, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<double, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<float, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            return true;
+        }();
+        (void)iattr;
+        if (kz == 3) {
+            if (ex) k_convolve_pixels_iso<double, 3><<<g, kPixThreads, ib, s>>>(a, ityd, txd);
+            else k_convolve_pixels_iso<float, 3><<<g, kPixThreads, ib, s>>>(a, ityd, txd);
+        } else {
+            if (ex) k_convolve_pixels_iso<double, 5><<<g, kPixThreads, ib, s>>>(a, ityd, txd);
+            else k_convolve_pixels_iso<float, 5><<<g, kPixThreads, ib, s>>>(a, ityd, txd);
+        }
+        count_launch(ctx);
+        APR_CUDA(cudaGetLastError());
+        return;
+    }
+    const int bytes = (kPz + 2 * (kz / 2)) * (kPx + 2 * (kx / 2)) * (kPy + 2 * (ky / 2)) * static_cast<int>(sizeof(float));
+    static const bool attr = [] {
+        const int mx = (kPz + kPixMaxK - 1) * (kPx + kPixMaxK - 1) * (kPy + kPixMaxK - 1) * static_cast<int>(sizeof(float));
+        APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        return true;
+    }();
+    (void)attr;
+    if (accum == APRGPU_ACCUM_EXACT)
+        k_convolve_pixels<double><<<static_cast<unsigned>(blocks), kPixThreads, bytes, s>>>(a, tyd, txd);
+    else
+        k_convolve_pixels<float><<<static_cast<unsigned>(blocks), kPixThreads, bytes, s>>>(a, tyd, txd);
+    count_launch(ctx);
+    APR_CUDA(cudaGetLastError());
+}
+
+}  // namespace aprgpu
