@@ -4,6 +4,7 @@
 // status code that the reference-side shim maps back to aprkit's exceptions.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -846,25 +847,59 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
         const double eps = epsilon > 0.0 ? epsilon : 1e-6 * std::max(mean, 1e-30);  // rl_epsilon, deconv.hpp:36-38
         float* ratio = apr->rl_ratio.as<float>();
         float* tv = apr->rl_tv.as<float>();
+        auto iteration = [&] {
+            aprgpu::fill_tree_device(apr, est, tv, s);
+            aprgpu::EpiArgs e1;
+            e1.mode = aprgpu::EPI_RL_RATIO;
+            e1.u = u;
+            e1.eps = eps;
+            aprgpu::convolve_device(apr, est, tv, pw, APRGPU_PAD_REFLECT, accum, ratio, e1, s);
+            aprgpu::fill_tree_device(apr, ratio, tv, s);
+            aprgpu::EpiArgs e2;
+            e2.mode = aprgpu::EPI_RL_MULT;
+            e2.est = est;
+            aprgpu::convolve_device(apr, ratio, tv, pwt, APRGPU_PAD_REFLECT, accum, nullptr, e2, s);
+        };
+        // The first iteration runs eagerly (it builds the lazily cached maps,
+        // links and attributes); the rest replay it as one CUDA graph (~24
+        // kernels per iteration, no launch gaps).  APRGPU_RL_GRAPH=0: eager.
+        const char* ge = std::getenv("APRGPU_RL_GRAPH");
+        const bool use_graph = !(ge && ge[0] == '0') && s != nullptr;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t graph_kernels = 0;  // our kernels per replay
         try {
             for (int k = 1; k <= iterations; ++k) {
-                aprgpu::fill_tree_device(apr, est, tv, s);
-                aprgpu::EpiArgs e1;
-                e1.mode = aprgpu::EPI_RL_RATIO;
-                e1.u = u;
-                e1.eps = eps;
-                aprgpu::convolve_device(apr, est, tv, pw, APRGPU_PAD_REFLECT, accum, ratio, e1, s);
-                aprgpu::fill_tree_device(apr, ratio, tv, s);
-                aprgpu::EpiArgs e2;
-                e2.mode = aprgpu::EPI_RL_MULT;
-                e2.est = est;
-                aprgpu::convolve_device(apr, ratio, tv, pwt, APRGPU_PAD_REFLECT, accum, nullptr, e2, s);
+                if (k == 1 || !use_graph) {
+                    iteration();
+                    continue;
+                }
+                if (!exec) {
+                    const uint64_t l0 = ctx->launches.load();
+                    APR_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                    try {
+                        iteration();
+                    } catch (...) {
+                        cudaStreamEndCapture(s, &graph);
+                        throw;
+                    }
+                    APR_CUDA(cudaStreamEndCapture(s, &graph));
+                    APR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+                    graph_kernels = ctx->launches.load() - l0;  // captured, not run: counted per replay
+                    ctx->launches.fetch_sub(graph_kernels);
+                }
+                APR_CUDA(cudaGraphLaunch(exec, s));
+                aprgpu::count_launch(ctx, graph_kernels);
             }
         } catch (...) {
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
             aprgpu_pyramid_free(pw);
             aprgpu_pyramid_free(pwt);
             throw;
         }
+        if (exec) APR_CUDA(cudaGraphExecDestroy(exec));
+        if (graph) APR_CUDA(cudaGraphDestroy(graph));
         if (ptr_kind == APRGPU_HOST) APR_CUDA(cudaMemcpyAsync(out, est, 4 * np, cudaMemcpyDeviceToHost, s));
         APR_CUDA(cudaStreamSynchronize(s));
         aprgpu_pyramid_free(pw);
