@@ -151,6 +151,8 @@ __global__ void k_verify_links(AccessView child, AccessView tree, int c, uint64_
 __device__ __forceinline__ double footprint_dev(int l, int iz, int ix, int iy, int glm, int nz, int nx, int ny) {
     // cell_footprint_volume (tree.hpp:15-22)
     const int s = 1 << (glm - l);
+    if ((iz + 1) * s <= nz && (ix + 1) * s <= nx && (iy + 1) * s <= ny)  // unclipped: s^3, exactly (< 2^53)
+        return static_cast<double>(s) * static_cast<double>(s) * static_cast<double>(s);
     const double dz = min((iz + 1) * s, nz) - iz * s;
     const double dx = min((ix + 1) * s, nx) - ix * s;
     const double dy = min((iy + 1) * s, ny) - iy * s;
@@ -200,8 +202,9 @@ __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
         if (pz < a.pz_lo || pz >= a.pz_hi) continue;  // another slab's rows
         const uint32_t pb = a.tree.rb[prow], pe = a.tree.rb[prow + 1];
         // child row ranges (4 leaf + 4 interior), held by lanes 0..7 and broadcast
+        // (the BUILD pass only: the fill reads the links)
         uint32_t cb = 0, ce = 0;
-        if (lane < 8) {
+        if (BUILD && lane < 8) {
             const int k = lane & 3;
             const int cz = 2 * pz + (k >> 1), cx = 2 * px + (k & 1);
             if (cz < a.czd && cx < a.cxd) {
@@ -219,10 +222,12 @@ __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
             }
         }
         uint32_t rbk[8], rek[8];
+        if (BUILD) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            rbk[k] = __shfl_sync(kFull, cb, k);
-            rek[k] = __shfl_sync(kFull, ce, k);
+            for (int k = 0; k < 8; ++k) {
+                rbk[k] = __shfl_sync(kFull, cb, k);
+                rek[k] = __shfl_sync(kFull, ce, k);
+            }
         }
         for (uint32_t j = pb + lane; j < pe; j += 32) {
             const int py = a.tree.y[j];
