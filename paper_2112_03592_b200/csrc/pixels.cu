@@ -9,6 +9,8 @@
 // y outputs of one (z, x) column, taps in the reference's order (az, ax, ay)
 // skipping zero weights (:86-88): EXACT = fp64 accumulation of exact products
 // (bit-identical), FAST = fp32 FMA.  Extents up to kMaxStencilExtent = 13.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace aprgpu {
@@ -159,6 +161,130 @@ __global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_iso(PixArgs a, 
     }
 }
 
+__device__ __forceinline__ void cp_async_4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+// Isotropic K^3 (K = 3, 5), streamed along z (2.5-D blocking): a CTA owns a
+// 16 (x) x 64 (y) column of outputs over kZc planes and keeps a ring of K + 2
+// input planes -- the K the current output plane reads and the next two,
+// prefetched with cp.async while the current plane is evaluated (padding
+// applied on load).  Every input plane is read from HBM about once (x / y halo
+// 1.16x, z halo 2H / kZc).  Each thread computes 4 consecutive y outputs of
+// one x from a register window (converted to the accumulator type once per row).
+constexpr int kSx = 16, kSy = 64, kZc = 32;
+template <typename Acc, int K>
+__global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_stream(PixArgs a, int txd, int tyd) {
+    constexpr int D = 2;  // prefetch distance (planes)
+    // a plane row: 4 - H unused floats, H left halo, the 64-float interior at a
+    // 16-byte boundary (16-byte copies), H right halo, padded to 16 bytes
+    constexpr int H = K / 2, PX = kSx + 2 * H, OFF = 4 - H, PY = kSy + 8, PLANE = PX * PY, RY = 4, NW = RY + K - 1,
+                  NS = K + D;
+    static_assert(kSx * (kSy / RY) == kPixThreads, "one output run per thread");
+    extern __shared__ __align__(16) float ring[];  // NS planes
+    __shared__ float W[K * K * K];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ty = blockIdx.x % tyd, t2 = blockIdx.x / tyd;
+    const int tx = t2 % txd, tzc = t2 / txd;
+    const int x0 = tx * kSx, y0 = ty * kSy, zc0 = tzc * kZc, zc1 = min(zc0 + kZc, a.nz);
+    for (int i = tid; i < K * K * K; i += kPixThreads) W[i] = a.w[i];
+    auto slot = [&](int z) { return ring + (((z % NS) + NS) % NS) * PLANE; };
+    const bool vec = (a.ny & 3) == 0;  // rows 16-byte aligned
+    // input plane z into its slot (reflected / zero outside the volume), asynchronously
+    auto load = [&](int z) {
+        float* pl = slot(z);
+        const bool zout = z < 0 || z >= a.nz;
+        const int zr = reflect_p(z, a.nz);
+        for (int r = warp; r < PX; r += kPixThreads / 32) {
+            const int x = x0 + r - H;
+            float* dst = pl + r * PY + OFF;  // dst[c]: y = y0 + c - H
+            if ((zout || x < 0 || x >= a.nx) && a.pad == APRGPU_PAD_ZERO) {
+                for (int c = lane; c < kSy + 2 * H; c += 32) dst[c] = 0.0f;
+                continue;
+            }
+            const float* src = a.in + (static_cast<size_t>(zr) * a.nx + reflect_p(x, a.nx)) * a.ny;
+            if (lane < kSy / 4 && vec && y0 + kSy <= a.ny) {  // the interior: 16-byte copies
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 static_cast<unsigned>(__cvta_generic_to_shared(dst + H + 4 * lane))),
+                             "l"(src + y0 + 4 * lane)
+                             : "memory");
+            } else if (lane < kSy / 4) {  // (ragged or unaligned rows)
+                for (int c = H + 4 * lane; c < H + 4 * lane + 4; ++c) {
+                    const int y = y0 + c - H;
+                    if (y < a.ny) cp_async_4(dst + c, src + y);
+                    else if (a.pad == APRGPU_PAD_REFLECT) cp_async_4(dst + c, src + reflect_p(y, a.ny));
+                    else dst[c] = 0.0f;
+                }
+            } else if (lane < kSy / 4 + 2 * H) {  // the halos
+                const int c = lane - kSy / 4 < H ? lane - kSy / 4 : kSy + (lane - kSy / 4);
+                const int y = y0 + c - H;
+                if (y >= 0 && y < a.ny) cp_async_4(dst + c, src + y);
+                else if (a.pad == APRGPU_PAD_REFLECT) cp_async_4(dst + c, src + reflect_p(y, a.ny));
+                else dst[c] = 0.0f;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int ox = tid / (kSy / RY), oy = (tid % (kSy / RY)) * RY;  // this thread's outputs
+    // planes zc0 - H .. zc0 + H + D - 1 in flight; then one group per plane
+    for (int z = zc0 - H; z < zc0 + H + D; ++z) {
+        if (z < zc1 + H) load(z);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int z = zc0 + H; z < zc1 + H; ++z) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(D) : "memory");  // all but the D newest groups
+        __syncthreads();  // planes o - H .. o + H resident; the slot of o - H - 1 is free
+        if (z + D < zc1 + H) load(z + D);  // prefetch D planes ahead
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        const int o = z - H;
+        if (x0 + ox < a.nx && y0 + oy < a.ny) {
+            Acc acc[RY];
+#pragma unroll
+            for (int j = 0; j < RY; ++j) acc[j] = Acc(0);
+#pragma unroll
+            for (int az = 0; az < K; ++az) {
+                const float* plz = slot(o + H - az);  // input plane read with weight plane az
+#pragma unroll
+                for (int ax = 0; ax < K; ++ax) {
+                    const float* row = plz + (ox + 2 * H - ax) * PY + OFF + oy;
+                    // pairs from the even index at or below the window (8-byte loads)
+                    constexpr int SH = OFF & 1, NL = (NW + SH + 1) & ~1;
+                    Acc win[NL];  // (converted once per row, not per tap)
+#pragma unroll
+                    for (int i = 0; i < NL; i += 2) {
+                        const float2 t = *reinterpret_cast<const float2*>(row - SH + i);
+                        win[i] = static_cast<Acc>(t.x);
+                        win[i + 1] = static_cast<Acc>(t.y);
+                    }
+#pragma unroll
+                    for (int ay = 0; ay < K; ++ay) {
+                        const float wv = W[(az * K + ax) * K + ay];
+                        if (wv == 0.0f) continue;  // (convolve.hpp:86-88)
+                        const Acc wa = static_cast<Acc>(wv);
+#pragma unroll
+                        for (int j = 0; j < RY; ++j) acc[j] = fma(wa, win[SH + j + 2 * H - ay], acc[j]);
+                    }
+                }
+            }
+            float* dst = a.out + (static_cast<size_t>(o) * a.nx + (x0 + ox)) * a.ny + y0 + oy;
+            if (y0 + oy + RY <= a.ny && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                for (int j = 0; j < RY; j += 4)
+                    __stcs(reinterpret_cast<float4*>(dst + j),
+                           make_float4(static_cast<float>(acc[j]), static_cast<float>(acc[j + 1]),
+                                       static_cast<float>(acc[j + 2]), static_cast<float>(acc[j + 3])));
+            } else {
+#pragma unroll
+                for (int j = 0; j < RY; ++j)
+                    if (y0 + oy + j < a.ny) dst[j] = static_cast<float>(acc[j]);
+            }
+        }
+        __syncthreads();  // (the next prefetch overwrites this iteration's oldest plane)
+    }
+}
+
 }  // namespace
 
 void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w_dev, int kz,
@@ -170,6 +296,32 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
     const int tzd = (nz + kPz - 1) / kPz, txd = (nx + kPx - 1) / kPx, tyd = (ny + kPy - 1) / kPy;
     const uint64_t blocks = static_cast<uint64_t>(tzd) * txd * tyd;
     if (blocks >= (1ull << 31)) fail(APRGPU_ERR_CAPABILITY, "convolve_pixels: volume too large");
+    if (kz == kx && kx == ky && (kz == 3 || kz == 5) && !std::getenv("APRGPU_PIXELS_TILED")) {
+        const bool ex = accum == APRGPU_ACCUM_EXACT;
+        const int sxd = (nx + kSx - 1) / kSx, syd = (ny + kSy - 1) / kSy, szd = (nz + kZc - 1) / kZc;
+        const unsigned g = static_cast<unsigned>(static_cast<uint64_t>(szd) * sxd * syd);
+        const int h = kz / 2;
+        const int rb = (kz + 2) * (kSx + 2 * h) * (kSy + 8) * static_cast<int>(sizeof(float));
+        static const bool sattr = [] {
+            const int mx = 7 * (kSx + 4) * (kSy + 8) * static_cast<int>(sizeof(float));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<double, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<double, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<float, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            return true;
+        }();
+        (void)sattr;
+        if (kz == 3) {
+            if (ex) k_convolve_pixels_stream<double, 3><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
+            else k_convolve_pixels_stream<float, 3><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
+        } else {
+            if (ex) k_convolve_pixels_stream<double, 5><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
+            else k_convolve_pixels_stream<float, 5><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
+        }
+        count_launch(ctx);
+        APR_CUDA(cudaGetLastError());
+        return;
+    }
     if (kz == kx && kx == ky && (kz == 3 || kz == 5)) {
         const bool ex = accum == APRGPU_ACCUM_EXACT;
         const int ityd = (ny + kIsoPy - 1) / kIsoPy;
