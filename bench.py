@@ -53,21 +53,30 @@ class ClockSampler:
         self.gpu, self.samples, self._stop = gpu, [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self.max_mhz = None
-
-    def _run(self):
-        try:
+        self._nvml = None
+        try:  # NVML is set up before the timed region, so short regions still get samples
             import pynvml as N
             N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            h = N.nvmlDeviceGetHandleByIndex(gpu)
             self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
             get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 N.nvmlDeviceGetCurrentClocksThrottleReasons
-            while not self._stop.is_set():
-                self.samples.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), get_reasons(h)))
-                self._stop.wait(0.005)
-            return
+            self._nvml = lambda: (N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), get_reasons(h))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        try:
+            self.samples.append(self._nvml())
         except Exception:
             pass
+
+    def _run(self):
+        if self._nvml is not None:
+            while not self._stop.is_set():
+                self._sample()
+                self._stop.wait(0.005)
+            return
         q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
         while not self._stop.is_set():
             try:
@@ -81,10 +90,14 @@ class ClockSampler:
             self._stop.wait(0.05)
 
     def __enter__(self):
+        if self._nvml is not None:
+            self._sample()
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        if self._nvml is not None:
+            self._sample()  # (still at load clocks)
         self._stop.set()
         self._t.join(timeout=10)
 
@@ -592,14 +605,17 @@ def main():
             return
         print(json.dumps(run_reference(args, rank, world)), flush=True)
         return
-    if world > 1:
+    # APRGPU_BENCH_SLAB=1 runs the N > 1 path (NCCL, z-slabs) with whatever world
+    # size torchrun gives, 1 included: how the slab path is exercised on one GPU
+    slab = world > 1 or os.environ.get("APRGPU_BENCH_SLAB") == "1"
+    if slab:
         import torch
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         torch.distributed.init_process_group("nccl")
-    res = run_slab(args, rank, world) if world > 1 else run_ours(args, rank, world)
+    res = run_slab(args, rank, world) if slab else run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(res), flush=True)
-    if world > 1:
+    if slab:
         import torch
         torch.distributed.destroy_process_group()
 
