@@ -126,12 +126,11 @@ template <int H>
 struct MapBox {
     static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * H;
     static constexpr int NC = BZ * BX * BY;
-    // codes in 128-cell chunks, lane-transposed: word pair 32k + i of chunk k
-    // holds cells 128k + i + 32j (j = 0..3), so a warp's reads of F for one j
-    // are consecutive cells (consecutive / repeated sources: no bank conflicts)
-    static constexpr int NCH = (NC + 127) / 128, NCP = NCH * 128;
-    static constexpr int CW = NCP / 2;                  // code words
+    // codes in cell order, two per word: the apply reads a cell pair (c, c+1),
+    // c even, with one 32-bit load
+    static constexpr int CW = NC / 2;                   // code words
     static constexpr int REC = CW + 2 * kTZ * kTX + 4;  // 32-bit words per record (+ nleaf, pad)
+    static_assert((CW * 4) % 16 == 0 && (REC * 4) % 16 == 0, "16-byte bulk copies");
     static constexpr uint32_t ZERO = 0;
     static constexpr int NF = kFlat0 + ((NC + 3) & ~3);  // F entries
 };
@@ -465,12 +464,14 @@ template <> struct Vec<double> {
 // the reference's (az, ax, ay) order (convolve.hpp:154-169).  The
 // neighbourhood's y window (box index 2qy + PADY - H .. +N) is loaded as
 // aligned pairs from the even index at or below it.
-template <typename Acc, int H, int BX, int BY, int PADY>
-__device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz, int qx, int qy, Acc (&acc)[8]) {
+// pair(c): the values of box cells c, c + 1 (c even) -- from the box itself
+// (k_conv_tile) or through the cells' codes (k_conv_map)
+template <typename Acc, int H, int BX, int BY, int PADY, typename Pair>
+__device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int qz, int qx, int qy, Acc (&acc)[8]) {
     constexpr int K = 2 * H + 1, N = 2 + 2 * H;
     constexpr int Y0 = PADY - H;
     constexpr int YA = Y0 & ~1, SH = Y0 - YA, NP = (SH + N + 1) / 2;
-    const float* base = S + ((2 * qz) * BX + 2 * qx) * BY + 2 * qy + YA;
+    const int base = ((2 * qz) * BX + 2 * qx) * BY + 2 * qy + YA;
     if constexpr (sizeof(Acc) == 4) {
         // FAST: the block's two y-outputs share every tap's weight -> packed
         // fp32x2 FMA (same per-element rounding as two FFMAs)
@@ -485,7 +486,7 @@ __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz
                 float r[2 * NP];
 #pragma unroll
                 for (int pp = 0; pp < NP; ++pp) {
-                    const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * BX + nx) * BY + 2 * pp);
+                    const float2 t2 = pair(base + (nz * BX + nx) * BY + 2 * pp);
                     r[2 * pp] = t2.x;
                     r[2 * pp + 1] = t2.y;
                 }
@@ -525,7 +526,7 @@ __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz
                 Acc r[2 * NP];
 #pragma unroll
                 for (int pp = 0; pp < NP; ++pp) {  // exact: every float is a double
-                    const float2 t2 = *reinterpret_cast<const float2*>(base + (nz * BX + nx) * BY + 2 * pp);
+                    const float2 t2 = pair(base + (nz * BX + nx) * BY + 2 * pp);
                     r[2 * pp] = static_cast<Acc>(t2.x);
                     r[2 * pp + 1] = static_cast<Acc>(t2.y);
                 }
@@ -552,6 +553,12 @@ __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz
             }
         }
     }
+}
+
+template <typename Acc, int H, int BX, int BY, int PADY>
+__device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz, int qx, int qy, Acc (&acc)[8]) {
+    apply_block_pairs<Acc, H, BX, BY, PADY>(
+        [S](int c) { return *reinterpret_cast<const float2*>(S + c); }, W, qz, qx, qy, acc);
 }
 
 // Output i of the launch's epilogue (EpiArgs, internal.cuh).
@@ -888,15 +895,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
         if (tid == 0 && roff[nruns] > M::NC) atomicOr(a.map_overflow, 1);
         auto code = [&](int c) -> uint32_t {
-            if (c >= M::NC) return M::ZERO;
             const int r = c / M::BY;
             return __float_as_uint(S[r * B::BY + (c - r * M::BY) + (kPadY - H)]);
         };
-        for (int u = tid; u < M::NCH * 32; u += kTileThreads) {
-            const int c = (u >> 5) * 128 + (u & 31);
-            rec[2 * u] = code(c) | code(c + 32) << 16;
-            rec[2 * u + 1] = code(c + 64) | code(c + 96) << 16;
-        }
+        for (int u = tid; u < M::CW; u += kTileThreads) rec[u] = code(2 * u) | code(2 * u + 1) << 16;
         if (tid < kTZ * kTX) {  // per inner row: output mask over y0 .. y0+31 and the first output's index
             uint32_t m = 0;
             int first = -1;
@@ -960,10 +962,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     k_conv_map(const __grid_constant__ TileLaunch a) {
     using M = MapBox<H>;
     constexpr int K = 2 * H + 1, KW = K * K * K;
-    // dynamic: the box, the tile's map record, the zero + its flattened source values
+    // dynamic: the tile's map record, then the zero + its flattened source values
     extern __shared__ __align__(16) unsigned char map_smem[];
-    float* S = reinterpret_cast<float*>(map_smem);
-    uint32_t* Mb = reinterpret_cast<uint32_t*>(S + M::NCP);
+    uint32_t* Mb = reinterpret_cast<uint32_t*>(map_smem);
     float* F = reinterpret_cast<float*>(Mb + M::REC);
     __shared__ __align__(8) uint64_t mbar;
     __shared__ Acc W[KW];
@@ -1004,20 +1005,6 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     }
     cp_async_wait_all();
     __syncthreads();
-    // the box, from F (shared memory only)
-    {
-        const uint2* c2 = reinterpret_cast<const uint2*>(Mb);
-        const int lane = tid & 31;
-        for (int u = tid; u < M::NCH * 32; u += kTileThreads) {
-            const uint2 c = c2[u];
-            float* dst = S + (u >> 5) * 128 + lane;
-            dst[0] = F[c.x & 0xffffu];
-            dst[32] = F[c.x >> 16];
-            dst[64] = F[c.y & 0xffffu];
-            dst[96] = F[c.y >> 16];
-        }
-    }
-    __syncthreads();
     const uint32_t* omask = Mb + M::CW;
     const uint32_t* ofirst = omask + kTZ * kTX;
     const int nb = compact_blocks(
@@ -1033,7 +1020,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
         Acc acc[8];
-        apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+        // box cells straight from their codes: no box is materialised
+        apply_block_pairs<Acc, H, M::BX, M::BY, H>(
+            [Mb, F](int c) {
+                const uint32_t w = Mb[c >> 1];
+                return make_float2(F[w & 0xffffu], F[w >> 16]);
+            },
+            W, qz, qx, qy, acc);
 #pragma unroll
         for (int oz = 0; oz < 2; ++oz)
 #pragma unroll
@@ -1227,7 +1220,7 @@ void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t
 
 template <typename Acc, int H>
 void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
-    constexpr int bytes = (MapBox<H>::NCP + MapBox<H>::REC + MapBox<H>::NF) * 4;
+    constexpr int bytes = (MapBox<H>::REC + MapBox<H>::NF) * 4;
     static const bool attr = [] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         return true;
