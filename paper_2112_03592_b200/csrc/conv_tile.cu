@@ -958,7 +958,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
 // each code's value, then the same block-compacted apply as k_conv_tile.
 // Results are bit-identical to k_conv_tile's (same box contents, same taps).
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 6))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 10))
     k_conv_map(const __grid_constant__ TileLaunch a) {
     using M = MapBox<H>;
     constexpr int K = 2 * H + 1, KW = K * K * K;
@@ -1005,6 +1005,21 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     }
     cp_async_wait_all();
     __syncthreads();
+    // 5^3 (H = 2): each box cell is read by ~3x more taps than at 3^3, so the
+    // box is expanded once (8 cells per thread) and the apply reads it; 3^3
+    // reads cells straight through their codes
+    constexpr bool kBox = H == 2;
+    float* S = F + M::NF;  // (kBox: NC floats after the source values)
+    if constexpr (kBox) {
+        const uint4* c4 = reinterpret_cast<const uint4*>(Mb);
+        float4* S4 = reinterpret_cast<float4*>(S);
+        for (int i = tid; i < M::NC / 8; i += kTileThreads) {
+            const uint4 c = c4[i];
+            S4[2 * i] = make_float4(F[c.x & 0xffffu], F[c.x >> 16], F[c.y & 0xffffu], F[c.y >> 16]);
+            S4[2 * i + 1] = make_float4(F[c.z & 0xffffu], F[c.z >> 16], F[c.w & 0xffffu], F[c.w >> 16]);
+        }
+        __syncthreads();
+    }
     const uint32_t* omask = Mb + M::CW;
     const uint32_t* ofirst = omask + kTZ * kTX;
     const int nb = compact_blocks(
@@ -1020,13 +1035,16 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
         Acc acc[8];
-        // box cells straight from their codes: no box is materialised
-        apply_block_pairs<Acc, H, M::BX, M::BY, H>(
-            [Mb, F](int c) {
-                const uint32_t w = Mb[c >> 1];
-                return make_float2(F[w & 0xffffu], F[w >> 16]);
-            },
-            W, qz, qx, qy, acc);
+        if constexpr (kBox) {
+            apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+        } else {  // box cells straight from their codes: no box is materialised
+            apply_block_pairs<Acc, H, M::BX, M::BY, H>(
+                [Mb, F](int c) {
+                    const uint32_t w = Mb[c >> 1];
+                    return make_float2(F[w & 0xffffu], F[w >> 16]);
+                },
+                W, qz, qx, qy, acc);
+        }
 #pragma unroll
         for (int oz = 0; oz < 2; ++oz)
 #pragma unroll
@@ -1220,7 +1238,7 @@ void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t
 
 template <typename Acc, int H>
 void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
-    constexpr int bytes = (MapBox<H>::REC + MapBox<H>::NF) * 4;
+    constexpr int bytes = (MapBox<H>::REC + MapBox<H>::NF + (H == 2 ? MapBox<H>::NC : 0)) * 4;
     static const bool attr = [] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         return true;
