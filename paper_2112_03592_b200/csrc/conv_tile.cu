@@ -129,7 +129,13 @@ struct MapBox {
     // codes in cell order, two per word: the apply reads a cell pair (c, c+1),
     // c even, with one 32-bit load
     static constexpr int CW = NC / 2;                   // code words
-    static constexpr int REC = CW + 2 * kTZ * kTX + 4;  // 32-bit words per record (+ nleaf, pad)
+    // + per inner row mask and first index, nleaf, the active-block count, pad,
+    // and the active blocks' order (bytes; see k_conv_tile's map mode)
+    static constexpr int W_NLEAF = CW + 2 * kTZ * kTX, W_NBLK = W_NLEAF + 1, W_BLK = W_NLEAF + 4;
+    static constexpr int REC = W_BLK + kBlocks / 4;     // 32-bit words per record
+    // bank key of an apply block: its first pair's word (H = 1: code words,
+    // 32 banks; H = 2: float2 box pairs, 16 double banks) modulo the bank count
+    static constexpr int NK = H == 1 ? 32 : 16;
     static_assert((CW * 4) % 16 == 0 && (REC * 4) % 16 == 0, "16-byte bulk copies");
     static constexpr uint32_t ZERO = 0;
     static constexpr int NF = kFlat0 + ((NC + 3) & ~3);  // F entries
@@ -914,8 +920,41 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         if (tid == 0) {  // runs are in row-slot order: interior rows come last
             int j = 0;
             while (j < nruns && !((rinfo[j] >> 5) & 1u)) ++j;
-            rec[M::CW + 2 * kTZ * kTX] = static_cast<uint32_t>(roff[j]);
-            rec[M::CW + 2 * kTZ * kTX + 1] = rec[M::CW + 2 * kTZ * kTX + 2] = rec[M::CW + 2 * kTZ * kTX + 3] = 0u;
+            rec[M::W_NLEAF] = static_cast<uint32_t>(roff[j]);
+            // the active 2x2x2 blocks, dealt round-robin over their bank keys so
+            // that a warp's 32 blocks start on as many distinct banks as possible
+            // (every tap load of the apply shifts all lanes alike)
+            uint8_t keyed[kBlocks], bkey[kBlocks];  // active blocks and their keys, then sorted by key
+            int nbk[M::NK] = {}, start[M::NK];
+            int total = 0;
+            for (int b = 0; b < kBlocks; ++b) {
+                const int qz = b / (kBlocks / 4), qx = (b / (kTY / 2)) & 3, qy = b & (kTY / 2 - 1);
+                const uint8_t* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
+                const unsigned m = *reinterpret_cast<const uint16_t*>(o) & *reinterpret_cast<const uint16_t*>(o + kTY) &
+                                   *reinterpret_cast<const uint16_t*>(o + kTX * kTY) &
+                                   *reinterpret_cast<const uint16_t*>(o + kTX * kTY + kTY);
+                if (m == 0xffffu) continue;
+                const int key = (((2 * qz) * M::BX + 2 * qx) * (M::BY / 2) + qy) % M::NK;
+                keyed[total] = static_cast<uint8_t>(b);
+                bkey[total++] = static_cast<uint8_t>(key);
+                ++nbk[key];
+            }
+            for (int k = 0, acc = 0; k < M::NK; ++k) {
+                start[k] = acc;
+                acc += nbk[k];
+            }
+            uint8_t sorted[kBlocks];
+            int fill[M::NK];
+            for (int k = 0; k < M::NK; ++k) fill[k] = start[k];
+            for (int i = 0; i < total; ++i) sorted[fill[bkey[i]]++] = keyed[i];
+            uint8_t* lst = reinterpret_cast<uint8_t*>(rec + M::W_BLK);
+            int n = 0;
+            for (int r = 0; n < total; ++r)
+                for (int k = 0; k < M::NK; ++k)
+                    if (r < nbk[k]) lst[n++] = sorted[start[k] + r];
+            for (int i = n; i < kBlocks; ++i) lst[i] = 0;
+            rec[M::W_NBLK] = static_cast<uint32_t>(total);
+            rec[M::W_NBLK + 1] = rec[M::W_NBLK + 2] = 0u;
         }
         return;
     }
@@ -968,8 +1007,6 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     float* F = reinterpret_cast<float*>(Mb + M::REC);
     __shared__ __align__(8) uint64_t mbar;
     __shared__ Acc W[KW];
-    __shared__ uint8_t blist[kBlocks];
-    __shared__ int wcnt[2 * kTileThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
     const int l = a.lvl[s];
@@ -998,7 +1035,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     // read and overwritten by the same thread); a warp's entries are mostly
     // consecutive particles
     {
-        const uint32_t nleaf = Mb[M::CW + 2 * kTZ * kTX];
+        const uint32_t nleaf = Mb[M::W_NLEAF];
         uint32_t q = tid;
         for (; q < nleaf; q += kTileThreads) cp_async4(Fi + q, a.val + Fi[q]);
         for (; q < nflat; q += kTileThreads) cp_async4(Fi + q, a.tval + Fi[q]);
@@ -1022,15 +1059,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     }
     const uint32_t* omask = Mb + M::CW;
     const uint32_t* ofirst = omask + kTZ * kTX;
-    const int nb = compact_blocks(
-        [&](int b) {
-            const int qz = b / (kBlocks / 4), qx = (b / (kTY / 2)) & 3, qy = b & (kTY / 2 - 1);
-            const int r = 2 * qz * kTX + 2 * qx;
-            const uint32_t m = omask[r] | omask[r + 1] | omask[r + kTX] | omask[r + kTX + 1];
-            return ((m >> (2 * qy)) & 3u) != 0;
-        },
-        blist, wcnt);
-    __syncthreads();
+    // the active blocks in their bank-interleaved order (map build)
+    const int nb = static_cast<int>(Mb[M::W_NBLK]);
+    const uint8_t* blist = reinterpret_cast<const uint8_t*>(Mb + M::W_BLK);
     for (int q = tid; q < nb; q += kTileThreads) {
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);

@@ -55,3 +55,12 @@ def pyramid_levels(d: dict, name: str):
 
 def bits(a: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def as_oracle(a):
+    """An oracle Access from a product LinearAccess."""
+    from pyoracle import Access
+    return Access(l_min=a.l_min, l_max=a.l_max, z_dim=np.asarray(a.z_dim, np.int32),
+                  x_dim=np.asarray(a.x_dim, np.int32), y_dim=np.asarray(a.y_dim, np.int32),
+                  y_idx=np.asarray(a.y_idx, np.uint16), xz_end=np.asarray(a.xz_end, np.uint64),
+                  level_offset=np.asarray(a.level_offset, np.uint64))

@@ -130,6 +130,43 @@ def test_map_and_reconstruction_paths_bit_identical(name, monkeypatch):
                 assert np.array_equal(G.bits(out["1"]), G.bits(out["0"])), (k, pad, accum)
 
 
+def _dense_apr(nz, nx, ny):
+    """Every pixel a finest-level particle (CR = 1): full tiles, all 256 output
+    blocks active (the acceptance criterion 4 degeneracy, at tile scale)."""
+    l_max = max(int(np.ceil(np.log2(max(nz, nx, ny)))), 1)
+    dims = [[-(-d // (1 << (l_max - l))) for d in (nz, nx, ny)] for l in range(l_max + 1)]
+    l_min = 1
+    rows = sum(dims[l][0] * dims[l][1] for l in range(l_min, l_max + 1))
+    level_offset = np.zeros(l_max + 1, np.uint64)
+    off = 0
+    for l in range(l_min, l_max + 1):
+        level_offset[l] = off
+        off += dims[l][0] * dims[l][1]
+    counts = np.zeros(rows, np.int64)
+    counts[int(level_offset[l_max]):] = ny
+    xz_end = np.cumsum(counts).astype(np.uint64)
+    y = np.tile(np.arange(ny, dtype=np.uint16), nz * nx)
+    z_dim, x_dim, y_dim = (np.array([d[i] for d in dims], np.int32) for i in range(3))
+    return P.APR(P.LinearAccess(l_min, l_max, z_dim, x_dim, y_dim, y, xz_end, level_offset), None, (nz, nx, ny))
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (40, 24, 70)])
+def test_dense_apr_all_blocks_active(shape, tile_path):
+    apr = _dense_apr(*shape)
+    assert P.validate(apr).ok
+    rng = np.random.default_rng(4)
+    v = rng.uniform(0, 100, apr.access.particle_count()).astype(np.float32)
+    tv = P.fill_tree(apr, v)
+    leaf, tree = G.as_oracle(apr.access), G.as_oracle(apr.tree_access)
+    for k in (3, 5):
+        pyr = P.make_pyramid(P.gaussian_stencil(1.0, k), apr.access.l_min, apr.access.l_max, P.PyramidMode.Restricted)
+        levels = [((s.kz, s.kx, s.ky), s.weights) for s in pyr.stencils]
+        for pad in (P.PadMode.Zero, P.PadMode.Reflect):
+            got = P.convolve_apr(apr, v, tv, pyr, pad)
+            exp = ORC.convolve(leaf, tree, v, tv, levels, apr.access.l_min, int(pad))
+            assert np.array_equal(G.bits(got), G.bits(exp)), (shape, k, pad)
+
+
 @pytest.mark.parametrize("name", ["rl_spheres64"])
 def test_rl_apr_bit_exact(name):
     d = G.load(name)
