@@ -371,8 +371,9 @@ def run_ours(args, rank, world):
 
 # ------------------------------------------------------- multi-GPU z-slabs ---
 def run_slab(args, rank, world):
-    """N > 1: ONE volume (strong scaling) cut into z-slabs, one per GPU
-    (paper_2112_03592_b200.slab).  A conv-only step is the halo
+    """N > 1: one volume cut into z-slabs, one per GPU (paper_2112_03592_b200.slab,
+    DESIGN.md §6) -- for C3, the C3 APR tiled N times along z (weak scaling:
+    each GPU holds a C3-sized slab); other configs: the one volume (strong).  A conv-only step is the halo
     exchange of leaf and tree values over NCCL plus each rank's slab
     convolution; the paper step adds the slab tree fill with its cut-level
     all-gather.  Time = max over ranks of the CUDA-event step time."""
@@ -387,15 +388,41 @@ def run_slab(args, rank, world):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = P.default_context(dev_id)
-    apr, values, desc = workload(args.config)
-    dapr = apr.device(ctx)
+    vdev = None
+    tz = int(os.environ.get("APRGPU_BENCH_TILEZ", world))  # (a test hook: the tiling at any world size)
+    if args.config == "c3" and tz > 1:
+        # weak scaling: the C3 APR tiled N times along z on the device -- one
+        # C3-sized z-slab per GPU, neighbours exchanging halos
+        from paper_2112_03592_b200 import synth
+        apr3, values3, _ = workload("c3")
+        d3 = apr3.device(ctx)
+        dapr = synth.tile_apr(d3, tz, 1, 1)
+        v3 = torch.from_numpy(np.ascontiguousarray(values3, np.float32)).cuda()
+        vdev = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")
+        synth.tile_values(d3, dapr, tz, 1, 1, v3.data_ptr(), vdev.data_ptr())
+        torch.cuda.synchronize()
+        del v3, d3
+        apr = P.APR(dapr.download(L.LEAF), dapr.download(L.TREE), tuple(int(d) for d in dapr.dims))
+        apr._dev[ctx.device] = dapr
+        values = vdev.cpu().numpy()
+        desc = {"workload": f"C3 tiled {tz}(z) x 1 x 1 -> {1024 * tz} x 1024 x 1024 pixel-equivalent "
+                            "(device tiler): one C3-sized z-slab per GPU (weak scaling)"}
+        scaling = "weak"
+    else:
+        apr, values, desc = workload(args.config)
+        dapr = apr.device(ctx)
+        scaling = "strong"
     k = args.stencil
     pyr = P.make_pyramid(P.gaussian_stencil(1.0, k), apr.access.l_min, apr.access.l_max, P.PyramidMode.Restricted)
     dpyr = pyr.device(ctx)
     accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
     plan = SlabPlan.make(apr.access, apr.tree_access, apr.source_dims, world, rank, halo=max(k // 2, 1))
     st = GpuRankState(plan, dapr, dev_id, stream)
-    st.values.copy_(torch.from_numpy(np.ascontiguousarray(values, np.float32)).to(st.device))
+    if vdev is not None:
+        st.values.copy_(vdev)
+        del vdev
+    else:
+        st.values.copy_(torch.from_numpy(np.ascontiguousarray(values, np.float32)).to(st.device))
     comm = TorchComm()
     sc = SlabConvolver([st], comm)
     sc.fill_tree()
@@ -475,7 +502,7 @@ def run_slab(args, rank, world):
         "warmup": args.warmup,
         "ms_per_step": round(tc * 1e3, 4),
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f32 values, " + ("f64 accumulate (bit-exact)" if accum == L.ACCUM_EXACT else "f32 accumulate"),
         "data": "synthetic",

@@ -51,3 +51,17 @@ def test_bench_slab_path_over_nccl():
     for k in KEYS:
         assert k in d, k
     assert d["scaling"] == "strong" and d["gpu_launches"] > 0 and "z-slabs" in d["config"]["parallelism"]
+
+
+@pytest.mark.gpu
+def test_bench_weak_scaling_slab_workload():
+    # the N > 1 workload (C3 tiled N times along z, one slab per GPU), at N = 2 on one rank
+    env = dict(os.environ, APRGPU_BENCH_SLAB="1", APRGPU_BENCH_TILEZ="2")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "1",
+                        "--steps", "3", "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _line(r.stdout)
+    assert d["scaling"] == "weak" and "2048 x 1024 x 1024" in d["config"]["workload"]
+    assert d["config"]["particles"] > 30_000_000
