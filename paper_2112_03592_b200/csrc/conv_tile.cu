@@ -567,6 +567,51 @@ __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz
         [S](int c) { return *reinterpret_cast<const float2*>(S + c); }, W, qz, qx, qy, acc);
 }
 
+// The block's (up to 8) outputs through the epilogue, batched: all indices
+// first, then the epilogue's own loads, then the stores -- so RL's fp64
+// divisions (and their operand loads) overlap instead of running one output
+// at a time.  Output (oz, ox, oy) of block (qz, qx, qy) is inner row
+// r = (2qz + oz) * 8 + 2qx + ox at y = 2qy + oy; its particle is
+// ofirst[r] + popc(omask[r] below y).
+template <typename Acc>
+__device__ __forceinline__ void store_block(const TileLaunch& a, const uint32_t* omask, const uint32_t* ofirst, int qz,
+                                            int qx, int qy, const Acc (&acc)[8]) {
+    uint32_t idx[8];
+    bool ok[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int oz = j >> 2, ox = (j >> 1) & 1, oy = j & 1;
+        const int r = (2 * qz + oz) * kTX + 2 * qx + ox, y = 2 * qy + oy;
+        const uint32_t m = omask[r];
+        ok[j] = (m >> y) & 1u;
+        idx[j] = ofirst[r] + __popc(m & ((1u << y) - 1u));
+    }
+    if (a.epi.mode == EPI_STORE) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (ok[j]) a.out[idx[j]] = to_f(acc[j]);
+    } else if (a.epi.mode == EPI_RL_RATIO) {
+        float u[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = ok[j] ? __ldg(a.epi.u + idx[j]) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (!ok[j]) continue;
+            // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
+            const double bd = static_cast<double>(to_f(acc[j]));
+            const double den = bd < a.epi.eps ? a.epi.eps : bd;
+            a.out[idx[j]] = __double2float_rn(__ddiv_rn(static_cast<double>(u[j]), den));
+        }
+    } else {
+        float e[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = ok[j] ? a.epi.est[idx[j]] : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (ok[j]) a.epi.est[idx[j]] = __fmul_rn(e[j], to_f(acc[j]));  // deconv.hpp:102
+    }
+}
+
 // Output i of the launch's epilogue (EpiArgs, internal.cuh).
 __device__ __forceinline__ void store_out(const TileLaunch& a, uint32_t i, float r) {
     if (a.epi.mode == EPI_STORE) {
@@ -1076,19 +1121,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                 },
                 W, qz, qx, qy, acc);
         }
-#pragma unroll
-        for (int oz = 0; oz < 2; ++oz)
-#pragma unroll
-            for (int ox = 0; ox < 2; ++ox) {
-                const int r = (2 * qz + oz) * kTX + 2 * qx + ox;
-                const uint32_t m = omask[r];
-#pragma unroll
-                for (int oy = 0; oy < 2; ++oy) {
-                    const int y = 2 * qy + oy;
-                    if (!((m >> y) & 1u)) continue;
-                    store_out(a, ofirst[r] + __popc(m & ((1u << y) - 1u)), to_f(acc[(oz * 2 + ox) * 2 + oy]));
-                }
-            }
+        store_block(a, omask, ofirst, qz, qx, qy, acc);
     }
 }
 
