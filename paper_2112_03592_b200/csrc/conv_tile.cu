@@ -110,9 +110,10 @@ struct Box {
 
 // Gather-map record of a tile (k_conv_map): the box as (8+2H) x (8+2H) rows
 // of kTY + 2H cells (y origin y0 - H: exactly the cells the stencil reads),
-// one 16-bit code per cell -- kFlat0 + the index of its source particle in the
-// tile's flattened source list (the concatenation of its source runs,
-// k_tile_runs), ZERO for a zero cell -- then per inner row an output mask over
+// one 16-bit code per cell -- the byte offset in F (the staged values) of its
+// source, 4 * (kFlat0 + its index in the tile's flattened source list, the
+// concatenation of its source runs, k_tile_runs), ZERO = F[0] = 0 for a zero
+// cell; byte offsets spare the apply an address multiply -- then per inner row an output mask over
 // y0 .. y0+kTY-1 and the index of its first output particle, then the number
 // of leaf sources (the list holds the leaf runs' particles, then the interior
 // runs' nodes, so each part copies from one base pointer).  The flattened
@@ -818,7 +819,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         float v;
         if constexpr (MAP) {
             if (p < MapBox<H>::NC) a.flat[flat0 + p] = gi;
-            v = __uint_as_float(static_cast<uint32_t>(kFlat0 + p));
+            v = __uint_as_float(static_cast<uint32_t>(4 * (kFlat0 + p)));  // byte offset into F
         } else {
             v = __ldg((is_tree ? a.tval : a.val) + gi);
         }
@@ -1097,8 +1098,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         float4* S4 = reinterpret_cast<float4*>(S);
         for (int i = tid; i < M::NC / 8; i += kTileThreads) {
             const uint4 c = c4[i];
-            S4[2 * i] = make_float4(F[c.x & 0xffffu], F[c.x >> 16], F[c.y & 0xffffu], F[c.y >> 16]);
-            S4[2 * i + 1] = make_float4(F[c.z & 0xffffu], F[c.z >> 16], F[c.w & 0xffffu], F[c.w >> 16]);
+            const char* Fb = reinterpret_cast<const char*>(F);
+            auto at = [Fb](uint32_t off) { return *reinterpret_cast<const float*>(Fb + off); };
+            S4[2 * i] = make_float4(at(c.x & 0xffffu), at(c.x >> 16), at(c.y & 0xffffu), at(c.y >> 16));
+            S4[2 * i + 1] = make_float4(at(c.z & 0xffffu), at(c.z >> 16), at(c.w & 0xffffu), at(c.w >> 16));
         }
         __syncthreads();
     }
@@ -1115,9 +1118,11 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
             apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
         } else {  // box cells straight from their codes: no box is materialised
             apply_block_pairs<Acc, H, M::BX, M::BY, H>(
-                [Mb, F](int c) {
+                [Mb](int c) {  // codes are byte offsets into F, which sits at a fixed offset
                     const uint32_t w = Mb[c >> 1];
-                    return make_float2(F[w & 0xffffu], F[w >> 16]);
+                    const char* Fb = reinterpret_cast<const char*>(Mb + M::REC);
+                    return make_float2(*reinterpret_cast<const float*>(Fb + (w & 0xffffu)),
+                                       *reinterpret_cast<const float*>(Fb + (w >> 16)));
                 },
                 W, qz, qx, qy, acc);
         }
