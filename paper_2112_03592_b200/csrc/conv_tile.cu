@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
 // each code's value, then the same block-compacted apply as k_conv_tile.
 // Results are bit-identical to k_conv_tile's (same box contents, same taps).
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 10))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 8))
     k_conv_map(const __grid_constant__ TileLaunch a) {
     using M = MapBox<H>;
     constexpr int K = 2 * H + 1, KW = K * K * K;
