@@ -697,7 +697,7 @@ __device__ __forceinline__ int compact_blocks(Pred active, uint8_t* blist, int* 
 // j -> 2^31 | j, 0 = zero) in place of values, so the map reproduces every
 // fill rule -- overlap order, holes, reflect / zero pad -- by construction.
 template <typename Acc, int H, bool MAP = false>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 8))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 6) : (H == 2 ? 5 : 8))
     k_conv_tile(const __grid_constant__ TileLaunch a) {
     using B = Box<H>;
     using VT = Vec<float>;  // the box holds the particle values themselves (floats) in both modes
@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
 // each code's value, then the same block-compacted apply as k_conv_tile.
 // Results are bit-identical to k_conv_tile's (same box contents, same taps).
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 5) : (H == 2 ? 4 : 8))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 6) : (H == 2 ? 5 : 8))
     k_conv_map(const __grid_constant__ TileLaunch a) {
     using M = MapBox<H>;
     constexpr int K = 2 * H + 1, KW = K * K * K;
