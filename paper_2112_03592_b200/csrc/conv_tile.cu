@@ -1063,13 +1063,18 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         if ((z0 + kTZ) << sh <= a.slab_zlo || z0 << sh >= a.slab_zhi) return;
     }
     const uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
-    // the record and the flattened source list stream in by two bulk copies
-    const uint32_t f0 = __ldg(a.flat_off + tix), nflat = __ldg(a.flat_off + tix + 1) - f0;
+    // the record and the flattened source list stream in by two bulk copies; the
+    // record's is issued before the list's extent is known (its bytes are
+    // expected without an arrival; the one arrival comes with the list's)
     uint32_t* Fi = reinterpret_cast<uint32_t*>(F + kFlat0);
     if (tid == 0) {
         mbar_init(&mbar, 1);
-        mbar_expect(&mbar, (M::REC + nflat) * 4);
+        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(M::REC * 4) : "memory");
         bulk_copy(Mb, rec, M::REC * 4, &mbar);
+    }
+    const uint32_t f0 = __ldg(a.flat_off + tix), nflat = __ldg(a.flat_off + tix + 1) - f0;
+    if (tid == 0) {
+        mbar_expect(&mbar, nflat * 4);  // (arrive.expect_tx)
         if (nflat) bulk_copy(Fi, a.flat + f0, nflat * 4, &mbar);
     }
     if (tid < kFlat0) F[tid] = 0.0f;
