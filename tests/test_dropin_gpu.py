@@ -4,7 +4,8 @@ tests/cpp/Makefile builds proj/tests/test_*.cpp (with the doctest shim in
 tests/cpp/doctest.h) and proj/tests/acceptance.cpp from /root/reference with
 include/aprkit_gpu/ ahead of the reference's include directory, so every
 convolve_apr / nonempty_row_index / fill_tree / init_tree_structure / rl_apr
-call in them runs on the GPU through libaprgpu.so.  The binaries are built in
+call in them (and validate, reconstruct_*, convolve_pixels) runs on the GPU
+through libaprgpu.so: all 10 acceptance criteria.  The binaries are built in
 the container that has the reference and travel to the GPU box.
 """
 import os
@@ -30,7 +31,18 @@ def test_reference_unit_tests_pass_on_the_dropin():
     assert "failed: 0 | assertions" in out, out[-2000:]
 
 
-@pytest.mark.parametrize("criterion", [1, 2, 3, 4, 5, 8, 9])
+@pytest.mark.parametrize("criterion", [1, 2, 3, 4, 5, 6, 7, 8, 9])
 def test_reference_acceptance_criterion_on_the_dropin(criterion, tmp_path):
     rc, out = _run([os.path.join(BUILD, "acceptance"), str(tmp_path), str(criterion)], 1800)
+    assert rc == 0 and "PASS" in out, out[-3000:]
+
+
+def test_reference_acceptance_serialization_on_the_dropin(tmp_path):
+    # criterion 10: 200 write/read/re-write round trips (read_apr validates
+    # through the drop-in's device validate), then the reference's own fixtures
+    # written and read back
+    exe = os.path.join(BUILD, "acceptance")
+    rc, out = _run([exe, str(tmp_path), "--write-fixtures", "10"], 900)
+    assert rc == 0 and "PASS" in out, out[-3000:]
+    rc, out = _run([exe, str(tmp_path), "10"], 900)
     assert rc == 0 and "PASS" in out, out[-3000:]
