@@ -1,5 +1,6 @@
-"""Parity at BASELINE.json's full size (C3: 1024^3 spheres -> 17.1 M particles,
-built on the device): the whole C3 output against the C oracle bit for bit,
+"""Parity at BASELINE.json's full sizes (C3: 1024^3 spheres -> 17.1 M particles,
+built on the device; C4: C3 tiled 4 x 4 x 2): the whole C3 output against the
+C oracle bit for bit,
 and size-independent properties -- the device validator on the built
 structure, constant fields through fill_tree and convolve_apr, linearity, and
 the two independent tile paths (resident gather maps vs per-call
@@ -84,3 +85,34 @@ def test_c3_exact_convolution_equals_the_oracle(c3):
     assert np.array_equal(G.bits(tv), G.bits(orc.fill_tree(leaf, tree, tuple(apr.source_dims), values)))
     exp = orc.convolve(leaf, tree, values, tv, levels, apr.access.l_min, 1)
     assert np.array_equal(G.bits(out), G.bits(exp))
+
+
+def test_c4_paths_agree(c3, monkeypatch):
+    """C4 (the C3 APR tiled 4 x 4 x 2 on the device, 548 M particles): the
+    map and reconstruction paths agree bit for bit over the whole output."""
+    import torch
+    import paper_2112_03592_b200 as P
+    from paper_2112_03592_b200 import _lib as L
+    from paper_2112_03592_b200 import synth
+    apr, values = c3
+    ctx = P.default_context()
+    d3 = apr.device(ctx)
+    big = synth.tile_apr(d3, 4, 4, 2)
+    assert big.n_particles == 32 * values.size
+    v3 = torch.from_numpy(values).cuda()
+    v = torch.empty(big.n_particles, dtype=torch.float32, device="cuda")
+    synth.tile_values(d3, big, 4, 4, 2, v3.data_ptr(), v.data_ptr())
+    tv = torch.empty(max(big.n_tree, 1), dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    big.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
+    li = big.info(L.LEAF)
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, 3), int(li.l_min), int(li.l_max), P.PyramidMode.Restricted)
+    dpyr = pyr.device(ctx)
+    outs = []
+    for path in ("1", "0"):
+        monkeypatch.setenv("APRGPU_TILE_MAP", path)
+        o = torch.empty_like(v)
+        big.convolve_ptr(v.data_ptr(), tv.data_ptr(), dpyr, 1, L.ACCUM_FAST, o.data_ptr(), s)
+        torch.cuda.synchronize()
+        outs.append(o)
+    assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
