@@ -7,8 +7,9 @@
 // covering it, ..., the level l_min leaves, then (when tree values are given)
 // the level-l interior nodes -- with a warp barrier between passes, so a cell
 // covered twice (a malformed APR) keeps the reference's last writer.  Leaves at
-// most 2 levels coarser are written one particle per lane (<= 4 cells each);
-// coarser ones one particle at a time, the warp across its 2^d cells.  Writes
+// most 2 levels coarser are written one particle per lane (<= 4 cells, one
+// vector store); 3-4 levels coarser a lane per cell, several particles per
+// warp step; coarser ones one particle at a time, the warp across its 2^d cells.  Writes
 // are row-contiguous; the zero pass and the fill of a row merge in L2, so the
 // output is written to HBM about once: the kernel is bound by the output's
 // size (4 bytes per cell).
@@ -49,24 +50,55 @@ __device__ void fill_row_warp(const ReconArgs& a, int z, int x, float* dst, int 
             re = __ldg(a.leaf.rb + row + 1);
         }
     }
-    for (int y = lane; y < yd; y += 32) dst[y] = 0.0f;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {  // 16-byte zero stores where aligned
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        for (int y = lane; y < (yd >> 2); y += 32) d4[y] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        for (int y = (yd & ~3) + lane; y < yd; y += 32) dst[y] = 0.0f;
+    } else {
+        for (int y = lane; y < yd; y += 32) dst[y] = 0.0f;
+    }
     __syncwarp();
     for (int d = 0; d <= l - a.leaf.l_min; ++d) {
         const uint32_t b = __shfl_sync(0xffffffffu, rb, d), e = __shfl_sync(0xffffffffu, re, d);
         if (e <= b) continue;
-        if (d <= 2) {
+        const bool al = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+        if (d <= 2) {  // one particle per lane, its 1 / 2 / 4 cells as one (aligned) store
             for (uint32_t i = b + lane; i < e; i += 32) {
                 const int y0 = static_cast<int>(__ldg(a.leaf.y + i)) << d;
                 const float v = __ldg(a.values + i);
                 const int y1 = min(y0 + (1 << d), yd);
-                for (int y = y0; y < y1; ++y) dst[y] = v;
+                if (al && d == 2 && y1 - y0 == 4) {
+                    *reinterpret_cast<float4*>(dst + y0) = make_float4(v, v, v, v);
+                } else if (al && d == 1 && y1 - y0 == 2) {
+                    *reinterpret_cast<float2*>(dst + y0) = make_float2(v, v);
+                } else {
+                    for (int y = y0; y < y1; ++y) dst[y] = v;
+                }
             }
-        } else {
-            for (uint32_t i = b; i < e; ++i) {
-                const int y0 = static_cast<int>(__ldg(a.leaf.y + i)) << d;
-                const float v = __ldg(a.values + i);
-                const int y1 = min(y0 + (1 << d), yd);
-                for (int y = y0 + lane; y < y1; y += 32) dst[y] = v;
+        } else if (d <= 4) {  // 4 (d = 3) or 2 (d = 4) particles per warp step, a lane per cell
+            const int c = 1 << d, per = 32 / c, k = lane / c, j = lane % c;
+            for (uint32_t i0 = b; i0 < e; i0 += per) {
+                const uint32_t i = i0 + k;
+                if (i < e) {
+                    const int y = (static_cast<int>(__ldg(a.leaf.y + i)) << d) + j;
+                    if (y < yd) dst[y] = __ldg(a.values + i);
+                }
+            }
+        } else {  // 32 particles' (y, value) loaded at once, then broadcast one by one
+            for (uint32_t i0 = b; i0 < e; i0 += 32) {
+                const int n = static_cast<int>(min(32u, e - i0));
+                int yl = 0;
+                float vl = 0.0f;
+                if (lane < n) {
+                    yl = __ldg(a.leaf.y + i0 + lane);
+                    vl = __ldg(a.values + i0 + lane);
+                }
+                for (int k = 0; k < n; ++k) {
+                    const int y0 = __shfl_sync(0xffffffffu, yl, k) << d;
+                    const float v = __shfl_sync(0xffffffffu, vl, k);
+                    const int y1 = min(y0 + (1 << d), yd);
+                    for (int y = y0 + lane; y < y1; y += 32) dst[y] = v;
+                }
             }
         }
         __syncwarp();
