@@ -104,4 +104,15 @@ __host__ __device__ __forceinline__ int grid_dim_dev(int n, int l_max, int l) {
     return (n + s - 1) / s;
 }
 
+// deconv.hpp:98-99: float(u / std::max<double>(blurred, eps)), blurred a float.
+// When the denominator is the float itself, the fp64 quotient of two floats
+// rounded to float equals their correctly rounded float quotient (double
+// rounding is innocuous: 53 >= 2 * 24 + 2 bits), so the IEEE float division
+// gives the reference's bits; the eps branch keeps the fp64 division.
+__device__ __forceinline__ float rl_ratio(float u, float blurred, double eps) {
+    const double bd = static_cast<double>(blurred);
+    if (bd < eps) return __double2float_rn(__ddiv_rn(static_cast<double>(u), eps));
+    return __fdiv_rn(u, blurred);
+}
+
 }  // namespace aprgpu

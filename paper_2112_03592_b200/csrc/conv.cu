@@ -237,10 +237,7 @@ __global__ void __launch_bounds__(256) k_conv(ConvArgs a) {
                 if (a.epi.mode == EPI_STORE) {
                     a.out[i] = o;
                 } else if (a.epi.mode == EPI_RL_RATIO) {
-                    // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
-                    const double bd = static_cast<double>(o);
-                    const double den = bd < a.epi.eps ? a.epi.eps : bd;
-                    a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
+                    a.out[i] = rl_ratio(__ldg(a.epi.u + i), o, a.epi.eps);  // deconv.hpp:98-99
                 } else {
                     // deconv.hpp:102: estimate *= corr
                     a.epi.est[i] = __fmul_rn(a.epi.est[i], o);

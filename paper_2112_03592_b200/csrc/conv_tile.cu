@@ -596,13 +596,8 @@ __device__ __forceinline__ void store_block(const TileLaunch& a, const uint32_t*
 #pragma unroll
         for (int j = 0; j < 8; ++j) u[j] = ok[j] ? __ldg(a.epi.u + idx[j]) : 0.0f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (!ok[j]) continue;
-            // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
-            const double bd = static_cast<double>(to_f(acc[j]));
-            const double den = bd < a.epi.eps ? a.epi.eps : bd;
-            a.out[idx[j]] = __double2float_rn(__ddiv_rn(static_cast<double>(u[j]), den));
-        }
+        for (int j = 0; j < 8; ++j)
+            if (ok[j]) a.out[idx[j]] = rl_ratio(u[j], to_f(acc[j]), a.epi.eps);
     } else {
         float e[8];
 #pragma unroll
@@ -618,10 +613,7 @@ __device__ __forceinline__ void store_out(const TileLaunch& a, uint32_t i, float
     if (a.epi.mode == EPI_STORE) {
         a.out[i] = r;
     } else if (a.epi.mode == EPI_RL_RATIO) {
-        // deconv.hpp:98-99: float(u / std::max<double>(blurred, eps))
-        const double bd = static_cast<double>(r);
-        const double den = bd < a.epi.eps ? a.epi.eps : bd;
-        a.out[i] = __double2float_rn(__ddiv_rn(static_cast<double>(__ldg(a.epi.u + i)), den));
+        a.out[i] = rl_ratio(__ldg(a.epi.u + i), r, a.epi.eps);
     } else {
         a.epi.est[i] = __fmul_rn(a.epi.est[i], r);  // deconv.hpp:102
     }
