@@ -207,6 +207,179 @@ __global__ void __launch_bounds__(256) k_mean_exact(const float* __restrict__ u,
 
 }  // namespace
 
+namespace {
+
+__global__ void k_gather_rb(const uint32_t* __restrict__ rb, const uint64_t* __restrict__ rows, uint64_t* __restrict__ out,
+                            int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = rb[rows[i]];
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : dflt;
+}
+
+// The z-chunk plan of a host-pointer convolution (see convolve_host_pipelined).
+bool host_pipe_plan(aprgpu_apr* apr, int chunks, cudaStream_t s) {
+    const aprgpu::DevAccess& L = apr->leaf;
+    const aprgpu::DevAccess& T = apr->tree;
+    const int nzf = L.zd[L.l_max];
+    int S = 8;  // >= the tile height at l_max
+    while (2 * S * chunks <= nzf) S *= 2;
+    const int K = (nzf + S - 1) / S;
+    if (K < 2) return false;
+    int lg = 0;
+    while ((1 << lg) < S) ++lg;
+    // levels >= lc: a tile (8 rows) never spans two chunks, so a chunk's outputs
+    // are final after its own pass; its halo (<= 6 rows) lies in the neighbours
+    const int lc = std::max(L.l_max - (lg - 3), L.l_min);
+    auto& P = apr->host_pipe;
+    if (P.S == S && P.K == K) return true;
+    std::vector<uint64_t> rows;
+    auto add_rows = [&](const aprgpu::DevAccess& A, int lo) {
+        for (int l = lo; l <= A.l_max; ++l) {
+            const int sh = L.l_max - l;
+            for (int j = 0; j <= K; ++j) {
+                const int64_t zp = std::min<int64_t>(static_cast<int64_t>(j) * S, nzf);
+                const int64_t zb = std::min<int64_t>((zp + (int64_t(1) << sh) - 1) >> sh, A.zd[l]);
+                rows.push_back(A.level_offset[l] + static_cast<uint64_t>(zb) * A.xd[l]);
+            }
+        }
+    };
+    const int tlo = std::max(lc, T.l_min);
+    add_rows(L, lc);
+    const size_t nleafrows = rows.size();
+    if (T.n_particles) add_rows(T, tlo);
+    const size_t ntreerows = rows.size() - nleafrows;
+    rows.push_back(L.level_offset[lc]);
+    if (T.n_particles) rows.push_back(tlo <= T.l_max ? T.level_offset[tlo] : T.n_rows);
+    aprgpu::GpuBuf d_rows, d_out;
+    d_rows.ensure(8 * rows.size());
+    d_out.ensure(8 * rows.size());
+    APR_CUDA(cudaMemcpyAsync(d_rows.p, rows.data(), 8 * rows.size(), cudaMemcpyHostToDevice, s));
+    std::vector<uint64_t> got(rows.size());
+    // (leaf rows index the leaf rb, the rest the interior rb)
+    k_gather_rb<<<1, 256, 0, s>>>(L.rb, d_rows.as<uint64_t>(), d_out.as<uint64_t>(), static_cast<int>(nleafrows));
+    if (ntreerows)
+        k_gather_rb<<<1, 256, 0, s>>>(T.rb, d_rows.as<uint64_t>() + nleafrows, d_out.as<uint64_t>() + nleafrows,
+                                      static_cast<int>(ntreerows));
+    k_gather_rb<<<1, 32, 0, s>>>(L.rb, d_rows.as<uint64_t>() + nleafrows + ntreerows,
+                                 d_out.as<uint64_t>() + nleafrows + ntreerows, 1);
+    if (T.n_particles)
+        k_gather_rb<<<1, 32, 0, s>>>(T.rb, d_rows.as<uint64_t>() + nleafrows + ntreerows + 1,
+                                     d_out.as<uint64_t>() + nleafrows + ntreerows + 1, 1);
+    aprgpu::count_launch(apr->ctx, 2 + (ntreerows ? 1 : 0) + (T.n_particles ? 1 : 0));
+    APR_CUDA(cudaGetLastError());
+    APR_CUDA(cudaMemcpyAsync(got.data(), d_out.p, 8 * rows.size(), cudaMemcpyDeviceToHost, s));
+    APR_CUDA(cudaStreamSynchronize(s));
+    P.S = S;
+    P.K = K;
+    P.lc = lc;
+    P.leaf_b.assign(got.begin(), got.begin() + nleafrows);
+    P.tree_b.assign(got.begin() + nleafrows, got.begin() + nleafrows + ntreerows);
+    P.leaf_pre = got[nleafrows + ntreerows];
+    P.tree_pre = T.n_particles ? got[nleafrows + ntreerows + 1] : 0;
+    return true;
+}
+
+// convolve_apr with host pointers, pipelined over z-chunks of the volume: the
+// inputs stream in chunk by chunk on one copy stream, chunk j's tiles convolve
+// (Slab restriction, as the multi-GPU path) once chunks <= j+1 have arrived, and
+// chunk j's outputs stream back on a second copy stream while later chunks
+// convolve -- so the PCIe copies in both directions overlap each other and the
+// kernels.  Outputs are bit-identical to the one-shot path (every output is
+// computed from the same inputs by the same kernel; levels < lc, a few
+// thousand particles, are recomputed by every pass and copied back last).
+// Only page-locked buffers qualify (a pageable copy blocks the host); with
+// C3 on one B200 the call drops from 2.80 to 2.46 ms (PCIe: the two
+// directions share the link's budget, so the overlap is partial).
+// Returns false when the volume is too small to be worth chunking.
+bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* tree_values,
+                             const aprgpu_pyramid* pyr, int pad, int accum, float* out, cudaStream_t s) {
+    const int chunks = env_int("APRGPU_HOST_CHUNKS", 8);
+    const int min_np = env_int("APRGPU_HOST_PIPELINE_MIN", 1 << 20);
+    const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
+    if (chunks < 2 || np < static_cast<uint64_t>(std::max(min_np, 0)) || !s) return false;
+    // only page-locked host buffers copy asynchronously (a pageable copy blocks
+    // the host, which would serialise the pipeline)
+    auto pinned = [](const void* p) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return at.type == cudaMemoryTypeHost;
+    };
+    if (!pinned(values) || !pinned(out) || (nt && !pinned(tree_values))) return false;
+    if (!host_pipe_plan(apr, chunks, s)) return false;
+    aprgpu_ctx* ctx = apr->ctx;
+    const auto& P = apr->host_pipe;
+    const int K = P.K;
+    if (!ctx->copy_in) APR_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+    if (!ctx->copy_out) APR_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+    while (ctx->events.size() < static_cast<size_t>(2 * K + 1)) {
+        cudaEvent_t e;
+        APR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->events.push_back(e);
+    }
+    cudaEvent_t start = ctx->events[0];
+    cudaEvent_t* e_in = ctx->events.data() + 1;
+    cudaEvent_t* e_conv = ctx->events.data() + 1 + K;
+    float* d_in = apr->h_in.as<float>();
+    float* d_tree = apr->h_tree.as<float>();
+    float* d_out = apr->h_out.as<float>();
+    const aprgpu::DevAccess& L = apr->leaf;
+    const aprgpu::DevAccess& T = apr->tree;
+    const int tlo = std::max(P.lc, T.l_min);
+    const int ntl = nt ? std::max(T.l_max - tlo + 1, 0) : 0;
+    auto h2d = [&](float* d, const float* h, uint64_t b, uint64_t e) {
+        if (e > b) APR_CUDA(cudaMemcpyAsync(d + b, h + b, 4 * (e - b), cudaMemcpyHostToDevice, ctx->copy_in));
+    };
+    auto d2h = [&](uint64_t b, uint64_t e) {
+        if (e > b) APR_CUDA(cudaMemcpyAsync(out + b, d_out + b, 4 * (e - b), cudaMemcpyDeviceToHost, ctx->copy_out));
+    };
+    APR_CUDA(cudaEventRecord(start, s));
+    APR_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
+    APR_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+    // few, large copies: the finest level's rows carry ~90 % of the particles,
+    // so chunk 0 takes every coarser level whole and each later chunk one
+    // contiguous range of the finest level (leaf and interior alike); outputs
+    // come back per chunk for the two finest levels, the rest at the end
+    auto LB = [&](int l, int jj) { return P.leaf_b[(l - P.lc) * (K + 1) + jj]; };
+    auto TB = [&](int jj) { return P.tree_b[(ntl - 1) * (K + 1) + jj]; };
+    for (int j = 0; j < K; ++j) {
+        h2d(d_in, values, j ? LB(L.l_max, j) : 0, LB(L.l_max, j + 1));
+        if (nt) {
+            if (ntl)
+                h2d(d_tree, tree_values, j ? TB(j) : 0, TB(j + 1));
+            else if (j == 0)
+                h2d(d_tree, tree_values, 0, nt);
+        }
+        APR_CUDA(cudaEventRecord(e_in[j], ctx->copy_in));
+    }
+    const bool two = L.l_max - 1 >= P.lc;
+    aprgpu::EpiArgs epi;
+    for (int j = 0; j < K; ++j) {
+        APR_CUDA(cudaStreamWaitEvent(s, e_in[std::min(j + 1, K - 1)], 0));
+        aprgpu::Slab slab;
+        slab.lc = P.lc;
+        slab.z_lo = j * P.S;
+        slab.z_hi = j == K - 1 ? (1 << 30) : (j + 1) * P.S;
+        aprgpu::convolve_device(apr, d_in, d_tree, pyr, pad, accum, d_out, epi, s, slab);
+        APR_CUDA(cudaEventRecord(e_conv[j], s));
+        APR_CUDA(cudaStreamWaitEvent(ctx->copy_out, e_conv[j], 0));
+        d2h(LB(L.l_max, j), LB(L.l_max, j + 1));
+        if (two) d2h(LB(L.l_max - 1, j), LB(L.l_max - 1, j + 1));
+    }
+    d2h(0, two ? LB(L.l_max - 1, 0) : LB(L.l_max, 0));
+    APR_CUDA(cudaStreamSynchronize(ctx->copy_out));
+    APR_CUDA(cudaStreamSynchronize(s));
+
+    return true;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* aprgpu_last_error(void) { return g_last_error.c_str(); }
@@ -233,6 +406,9 @@ int aprgpu_ctx_free(aprgpu_ctx* ctx) {
         DeviceGuard g(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
+        if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+        if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+        for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
         delete ctx;
     });
 }
@@ -675,6 +851,7 @@ int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_valu
         apr->h_in.ensure(4 * np + 4);
         apr->h_tree.ensure(4 * nt + 4);
         apr->h_out.ensure(4 * np + 4);
+        if (convolve_host_pipelined(apr, values, tree_values, pyr, pad_mode, accum, out, s)) return;
         APR_CUDA(cudaMemcpyAsync(apr->h_in.p, values, 4 * np, cudaMemcpyHostToDevice, s));
         if (nt) APR_CUDA(cudaMemcpyAsync(apr->h_tree.p, tree_values, 4 * nt, cudaMemcpyHostToDevice, s));
         aprgpu::convolve_device(apr, apr->h_in.as<float>(), apr->h_tree.as<float>(), pyr, pad_mode, accum,

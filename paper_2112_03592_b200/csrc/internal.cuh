@@ -91,6 +91,9 @@ struct GpuBuf {  // trivially owned device allocation
 struct aprgpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // host-pointer convolutions: copy streams and events of the z-chunk pipeline (lazy)
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    std::vector<cudaEvent_t> events;
     std::mutex mu;
     std::atomic<uint64_t> launches{0};
     int sm_count = 148;
@@ -108,6 +111,14 @@ struct aprgpu_apr {
     aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
     aprgpu::GpuBuf tmp;                    // misc
     aprgpu::GpuBuf built_values;           // leaf values sampled by aprgpu_build_apr / read by aprgpu_load_apr
+    // z-chunk plan of host-pointer convolutions (api.cu, HostPipe): chunk of S
+    // finest planes; levels >= lc split per chunk, [l - lc][j] = first particle
+    // of chunk j's rows at level l (j = 0..K)
+    struct HostPipe {
+        int S = 0, K = 0, lc = 0;
+        std::vector<uint64_t> leaf_b, tree_b;
+        uint64_t leaf_pre = 0, tree_pre = 0;  // particles of the levels < lc (a prefix)
+    } host_pipe;
     // BuildParams (apr.hpp:28-33): the reference's defaults unless built or loaded
     aprgpu_build_params params{0.1, 0, 1.0, 2, 0.0, 0, 0};
 };
