@@ -350,7 +350,9 @@ def run_ours(args, rank, world):
                              + (f" ({traffic_src})" if traffic_src else " (no committed capture)")},
         "e2e": {"value": round(world * 4 * n_pix / te / 1e9, 3), "unit": "GB/s (pixel-equivalent)",
                 "ms_per_step": round(te * 1e3, 4),
-                "h2d_bytes_per_step": int(4 * n_p + 4 * dapr.n_tree), "d2h_bytes_per_step": int(4 * n_p)},
+                "h2d_bytes_per_step": int(4 * n_p + 4 * dapr.n_tree), "d2h_bytes_per_step": int(4 * n_p),
+                "note": "aprgpu_convolve with pinned HOST buffers (the drop-in call): copies pipelined over "
+                        "z-chunks against the per-chunk passes (APRGPU_HOST_CHUNKS, default 8)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 2),
