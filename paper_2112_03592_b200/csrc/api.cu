@@ -311,8 +311,9 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
         return at.type == cudaMemoryTypeHost;
     };
     if (!pinned(values) || !pinned(out) || (nt && !pinned(tree_values))) return false;
-    if (!host_pipe_plan(apr, chunks, s)) return false;
     aprgpu_ctx* ctx = apr->ctx;
+    std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+    if (!host_pipe_plan(apr, chunks, s)) return false;
     const auto& P = apr->host_pipe;
     const int K = P.K;
     if (!ctx->copy_in) APR_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));

@@ -94,6 +94,7 @@ struct aprgpu_ctx {
     // host-pointer convolutions: copy streams and events of the z-chunk pipeline (lazy)
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> events;
+    std::mutex pipe_mu;  // one pipelined call at a time per context (shares the streams and events)
     std::mutex mu;
     std::atomic<uint64_t> launches{0};
     int sm_count = 148;
@@ -157,7 +158,8 @@ void reconstruct_patch_device(aprgpu_apr* apr, const float* values, const float*
 void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s);
-void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi, cudaStream_t s);
+void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi, cudaStream_t s,
+                    float* tree_out = nullptr);
 void fill_tree_finalize(aprgpu_apr* apr, float* tree, cudaStream_t s);
 void ensure_tree_links(aprgpu_apr* apr, cudaStream_t s);
 void tree_partition_check(aprgpu_apr* apr, int* dbl, unsigned long long* min_unc, cudaStream_t s);

@@ -1,5 +1,5 @@
-"""Warm timings on C3 (CUDA events): fill_tree alone, and the env variants given
-as arguments (KEY=VALUE pairs are set before each run in a subprocess).
+"""Warm timings on C3 (CUDA events): fill_tree alone, then once per KEY=VALUE
+argument with that variable set (the library reads it at call time).
 
     python tools/time_tree.py
 """
@@ -19,15 +19,28 @@ tv = torch.empty(dev.n_tree, dtype=torch.float32, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 for _ in range(3):
     dev.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
-torch.cuda.synchronize()
-ts = []
-for _ in range(20):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    dev.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
-    e1.record()
-    e1.synchronize()
-    ts.append(e0.elapsed_time(e1))
-ts.sort()
-print(f"fill_tree C3: median {ts[len(ts) // 2] * 1e3:.1f} us, min {ts[0] * 1e3:.1f} us "
-      f"({dev.n_particles} leaves, {dev.n_tree} interior nodes)")
+
+
+def run(tag):
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(20):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dev.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    print(f"fill_tree C3{tag}: median {ts[len(ts) // 2] * 1e3:.1f} us, min {ts[0] * 1e3:.1f} us "
+          f"({dev.n_particles} leaves, {dev.n_tree} interior nodes)")
+
+
+run("")
+for kv in sys.argv[1:]:
+    k, val = kv.split("=", 1)
+    os.environ[k] = val
+    for _ in range(3):
+        dev.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
+    run(f" [{kv}]")
+    del os.environ[k]
