@@ -284,6 +284,48 @@ __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
     }
 }
 
+// The fill of a level whose child cells are never clipped by the image edge
+// (every dim a multiple of the child cell size -- C3, C4): every leaf child
+// weighs s^3, so a node needs only its links -- one thread per node over the
+// level's contiguous node range, no row walk.  Same per-node order and
+// operations as k_fill_tree_level (bit-identical).
+__global__ void __launch_bounds__(256) k_fill_tree_flat(FillArgs a, uint32_t n0, uint32_t n1, double w) {
+    for (uint32_t j = n0 + blockIdx.x * blockDim.x + threadIdx.x; j < n1; j += gridDim.x * blockDim.x) {
+        const Links lk = a.links[j];
+        const uint32_t wl[4] = {lk.leaf.x, lk.leaf.y, lk.leaf.z, lk.leaf.w};
+        const uint32_t wt[4] = {lk.tree.x, lk.tree.y, lk.tree.z, lk.tree.w};
+        double vs = 0.0, ws = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            {
+                const uint32_t b = wl[k] & 0x3fffffffu, f0 = (wl[k] >> 30) & 1u, f1 = wl[k] >> 31;
+                if (f0) {
+                    vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b])));
+                    ws = __dadd_rn(ws, w);
+                }
+                if (f1) {
+                    vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b + f0])));
+                    ws = __dadd_rn(ws, w);
+                }
+            }
+            {
+                const uint32_t b = wt[k] & 0x3fffffffu, f0 = (wt[k] >> 30) & 1u, f1 = wt[k] >> 31;
+                if (f0) {
+                    vs = __dadd_rn(vs, a.vsum[b]);
+                    ws = __dadd_rn(ws, a.wsum[b]);
+                }
+                if (f1) {
+                    vs = __dadd_rn(vs, a.vsum[b + f0]);
+                    ws = __dadd_rn(ws, a.wsum[b + f0]);
+                }
+            }
+        }
+        a.vsum[j] = vs;
+        a.wsum[j] = ws;
+        if (a.tree_out) a.tree_out[j] = ws > 0.0 ? __double2float_rn(__ddiv_rn(vs, ws)) : 0.0f;  // tree.hpp:146-148
+    }
+}
+
 __global__ void k_tree_finalize(const double* __restrict__ vsum, const double* __restrict__ wsum, uint64_t n,
                                 float* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -571,13 +613,35 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
     ensure_tree_links(apr, s);
     a.links = apr->tree_links.as<Links>();
     a.tree_out = tree_out;
+    if (apr->tree_level_first.empty()) {  // first node of each interior level, + the total (once per APR)
+        std::vector<uint32_t> f(T.l_max + 2);
+        for (int l = 0; l <= T.l_max + 1; ++l) {
+            const uint64_t row = l <= T.l_max ? T.level_offset[l] : T.n_rows;
+            APR_CUDA(cudaMemcpyAsync(&f[l], T.rb + row, 4, cudaMemcpyDeviceToHost, s));
+        }
+        APR_CUDA(cudaStreamSynchronize(s));
+        apr->tree_level_first.assign(f.begin(), f.end());
+    }
     for (int lt = std::min(lt_hi, T.l_max); lt >= std::max(lt_lo, T.l_min); --lt) {
         set_fill_level(a, L, T, lt);
         a.pz_lo = z_hi < 0 ? 0 : (z_lo >> (a.glm - lt));
         a.pz_hi = z_hi < 0 ? (1 << 30) : ((z_hi + (1 << (a.glm - lt)) - 1) >> (a.glm - lt));
         if (a.n_work == 0) continue;
-        const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), ctx->sm_count * 16);
-        k_fill_tree_level<false><<<grid, 256, 0, s>>>(a);
+        const int64_t cs = int64_t(1) << (a.glm - a.c);  // child cell size
+        static const bool flat_ok = [] {  // APRGPU_FILL_FLAT=0: always the row kernel
+            const char* e = std::getenv("APRGPU_FILL_FLAT");
+            return !(e && e[0] == '0');
+        }();
+        if (flat_ok && z_hi < 0 && a.nz % cs == 0 && a.nx % cs == 0 && a.ny % cs == 0) {
+            const uint32_t n0 = static_cast<uint32_t>(apr->tree_level_first[lt]);
+            const uint32_t n1 = static_cast<uint32_t>(apr->tree_level_first[lt + 1]);
+            const double w = static_cast<double>(cs) * static_cast<double>(cs) * static_cast<double>(cs);
+            const unsigned grid = std::min<unsigned>(blocks_for(n1 - n0, 256), ctx->sm_count * 16);
+            k_fill_tree_flat<<<grid, 256, 0, s>>>(a, n0, n1, w);
+        } else {
+            const unsigned grid = std::min<unsigned>(blocks_for(a.n_work, 8), ctx->sm_count * 16);
+            k_fill_tree_level<false><<<grid, 256, 0, s>>>(a);
+        }
         count_launch(ctx);
     }
     APR_CUDA(cudaGetLastError());
