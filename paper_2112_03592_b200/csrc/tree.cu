@@ -289,40 +289,57 @@ __global__ void __launch_bounds__(256) k_fill_tree_level(FillArgs a) {
 // weighs s^3, so a node needs only its links -- one thread per node over the
 // level's contiguous node range, no row walk.  Same per-node order and
 // operations as k_fill_tree_level (bit-identical).
-__global__ void __launch_bounds__(256) k_fill_tree_flat(FillArgs a, uint32_t n0, uint32_t n1, double w) {
-    for (uint32_t j = n0 + blockIdx.x * blockDim.x + threadIdx.x; j < n1; j += gridDim.x * blockDim.x) {
-        const Links lk = a.links[j];
-        const uint32_t wl[4] = {lk.leaf.x, lk.leaf.y, lk.leaf.z, lk.leaf.w};
-        const uint32_t wt[4] = {lk.tree.x, lk.tree.y, lk.tree.z, lk.tree.w};
-        double vs = 0.0, ws = 0.0;
+__device__ __forceinline__ void fill_node_flat(const FillArgs& a, uint32_t j, double w) {
+    const Links lk = a.links[j];
+    const uint32_t wl[4] = {lk.leaf.x, lk.leaf.y, lk.leaf.z, lk.leaf.w};
+    const uint32_t wt[4] = {lk.tree.x, lk.tree.y, lk.tree.z, lk.tree.w};
+    double vs = 0.0, ws = 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            {
-                const uint32_t b = wl[k] & 0x3fffffffu, f0 = (wl[k] >> 30) & 1u, f1 = wl[k] >> 31;
-                if (f0) {
-                    vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b])));
-                    ws = __dadd_rn(ws, w);
-                }
-                if (f1) {
-                    vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b + f0])));
-                    ws = __dadd_rn(ws, w);
-                }
+    for (int k = 0; k < 4; ++k) {
+        {
+            const uint32_t b = wl[k] & 0x3fffffffu, f0 = (wl[k] >> 30) & 1u, f1 = wl[k] >> 31;
+            if (f0) {
+                vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b])));
+                ws = __dadd_rn(ws, w);
             }
-            {
-                const uint32_t b = wt[k] & 0x3fffffffu, f0 = (wt[k] >> 30) & 1u, f1 = wt[k] >> 31;
-                if (f0) {
-                    vs = __dadd_rn(vs, a.vsum[b]);
-                    ws = __dadd_rn(ws, a.wsum[b]);
-                }
-                if (f1) {
-                    vs = __dadd_rn(vs, a.vsum[b + f0]);
-                    ws = __dadd_rn(ws, a.wsum[b + f0]);
-                }
+            if (f1) {
+                vs = __dadd_rn(vs, __dmul_rn(w, static_cast<double>(a.leaf_v[b + f0])));
+                ws = __dadd_rn(ws, w);
             }
         }
-        a.vsum[j] = vs;
-        a.wsum[j] = ws;
-        if (a.tree_out) a.tree_out[j] = ws > 0.0 ? __double2float_rn(__ddiv_rn(vs, ws)) : 0.0f;  // tree.hpp:146-148
+        {
+            const uint32_t b = wt[k] & 0x3fffffffu, f0 = (wt[k] >> 30) & 1u, f1 = wt[k] >> 31;
+            if (f0) {
+                vs = __dadd_rn(vs, a.vsum[b]);
+                ws = __dadd_rn(ws, a.wsum[b]);
+            }
+            if (f1) {
+                vs = __dadd_rn(vs, a.vsum[b + f0]);
+                ws = __dadd_rn(ws, a.wsum[b + f0]);
+            }
+        }
+    }
+    a.vsum[j] = vs;
+    a.wsum[j] = ws;
+    if (a.tree_out) a.tree_out[j] = ws > 0.0 ? __double2float_rn(__ddiv_rn(vs, ws)) : 0.0f;  // tree.hpp:146-148
+}
+
+__global__ void __launch_bounds__(256) k_fill_tree_flat(FillArgs a, uint32_t n0, uint32_t n1, double w) {
+    for (uint32_t j = n0 + blockIdx.x * blockDim.x + threadIdx.x; j < n1; j += gridDim.x * blockDim.x)
+        fill_node_flat(a, j, w);
+}
+
+// The small coarse levels (flat-eligible) in ONE block, level after level with
+// a block barrier between them, instead of a launch each.
+struct CoarseLevels {
+    int n;
+    uint32_t n0[kMaxLevels], n1[kMaxLevels];
+    double w[kMaxLevels];
+};
+__global__ void __launch_bounds__(1024) k_fill_tree_coarse(FillArgs a, CoarseLevels c) {
+    for (int i = 0; i < c.n; ++i) {
+        for (uint32_t j = c.n0[i] + threadIdx.x; j < c.n1[i]; j += blockDim.x) fill_node_flat(a, j, c.w[i]);
+        __syncthreads();
     }
 }
 
@@ -632,7 +649,28 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
             const char* e = std::getenv("APRGPU_FILL_FLAT");
             return !(e && e[0] == '0');
         }();
-        if (flat_ok && z_hi < 0 && a.nz % cs == 0 && a.nx % cs == 0 && a.ny % cs == 0) {
+        auto flat_level = [&](int l) {  // child cells of interior level l never clipped
+            const int64_t c = int64_t(1) << (a.glm - l - 1);
+            return flat_ok && z_hi < 0 && a.nz % c == 0 && a.nx % c == 0 && a.ny % c == 0;
+        };
+        const int lo = std::max(lt_lo, T.l_min);
+        if (apr->tree_level_first[lt + 1] - apr->tree_level_first[lt] <= 8192) {
+            bool all = true;  // this level and every coarser one: one fused launch
+            for (int l = lt; l >= lo && all; --l) all = flat_level(l);
+            if (all) {
+                CoarseLevels c{};
+                for (int l = lt; l >= lo; --l, ++c.n) {
+                    const double cl = static_cast<double>(int64_t(1) << (a.glm - l - 1));
+                    c.n0[c.n] = static_cast<uint32_t>(apr->tree_level_first[l]);
+                    c.n1[c.n] = static_cast<uint32_t>(apr->tree_level_first[l + 1]);
+                    c.w[c.n] = cl * cl * cl;
+                }
+                k_fill_tree_coarse<<<1, 1024, 0, s>>>(a, c);
+                count_launch(ctx);
+                break;
+            }
+        }
+        if (flat_level(lt)) {
             const uint32_t n0 = static_cast<uint32_t>(apr->tree_level_first[lt]);
             const uint32_t n1 = static_cast<uint32_t>(apr->tree_level_first[lt + 1]);
             const double w = static_cast<double>(cs) * static_cast<double>(cs) * static_cast<double>(cs);
