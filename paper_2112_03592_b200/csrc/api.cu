@@ -1182,6 +1182,7 @@ int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int n
             need(ptr_kind == APRGPU_DEVICE, "bad pointer kind");
         }
         aprgpu::build_apr_device(ctx, vol, nz, nx, ny, rel_error, apr, apr->built_values, ctx->stream);
+        APR_CUDA(cudaStreamSynchronize(ctx->stream));  // (the staged volume is freed on return)
         apr->geom_l_max = std::max(apr->leaf.l_max, host_compute_l_max(nz, nx, ny));
         *out = apr;
     });

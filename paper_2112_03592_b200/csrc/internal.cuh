@@ -78,9 +78,17 @@ struct DevAccess {
     void release();
 };
 
-struct GpuBuf {  // trivially owned device allocation
+struct GpuBuf {  // owned device allocation (freed on release() or destruction; move-only)
     void* p = nullptr;
     size_t bytes = 0;
+    GpuBuf() = default;
+    GpuBuf(const GpuBuf&) = delete;
+    GpuBuf& operator=(const GpuBuf&) = delete;
+    GpuBuf(GpuBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    ~GpuBuf() { release(); }
     void ensure(size_t n);
     void release();
     template <class T> T* as() const { return static_cast<T*>(p); }
