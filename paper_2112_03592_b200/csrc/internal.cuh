@@ -117,6 +117,7 @@ struct aprgpu_apr {
     aprgpu::GpuBuf vsum, wsum;             // fill_tree fp64 sums [n_tree]
     aprgpu::GpuBuf tree_links;             // per interior node, its children (tree.cu); lazy
     std::vector<uint64_t> tree_level_first;  // first node of each interior level + the total (tree.cu); lazy
+    std::mutex init_mu;                      // guards the lazy per-APR caches above (links, level starts)
     aprgpu::GpuBuf h_in, h_tree, h_out;    // staging for host-pointer calls
     aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
     aprgpu::GpuBuf tmp;                    // misc

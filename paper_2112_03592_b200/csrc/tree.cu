@@ -570,6 +570,7 @@ __global__ void __launch_bounds__(256) k_partition_check(FillArgs a, int* dbl, u
 
 // Child links of every interior node (structure only; built on first use).
 void ensure_tree_links(aprgpu_apr* apr, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(apr->init_mu);
     if (apr->tree_links.p) return;
     const DevAccess& L = apr->leaf;
     const DevAccess& T = apr->tree;
@@ -630,6 +631,7 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
     ensure_tree_links(apr, s);
     a.links = apr->tree_links.as<Links>();
     a.tree_out = tree_out;
+    std::unique_lock<std::mutex> lk(apr->init_mu);
     if (apr->tree_level_first.empty()) {  // first node of each interior level, + the total (once per APR)
         std::vector<uint32_t> f(T.l_max + 2);
         for (int l = 0; l <= T.l_max + 1; ++l) {
@@ -639,6 +641,7 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
         APR_CUDA(cudaStreamSynchronize(s));
         apr->tree_level_first.assign(f.begin(), f.end());
     }
+    lk.unlock();
     for (int lt = std::min(lt_hi, T.l_max); lt >= std::max(lt_lo, T.l_min); --lt) {
         set_fill_level(a, L, T, lt);
         a.pz_lo = z_hi < 0 ? 0 : (z_lo >> (a.glm - lt));
