@@ -89,12 +89,31 @@ void upload_one(aprgpu_ctx* ctx, const aprgpu_access_desc* d, aprgpu::DevAccess&
 }
 
 void free_apr(aprgpu_apr* apr) {
+    if (apr->scratch_ev) cudaEventDestroy(apr->scratch_ev);
+    apr->scratch_ev = nullptr;
     apr->leaf.release();
     apr->tree.release();
     for (aprgpu::GpuBuf* b : {&apr->vsum, &apr->wsum, &apr->tree_links, &apr->h_in, &apr->h_tree, &apr->h_out, &apr->rl_u,
                               &apr->rl_ratio, &apr->rl_tv, &apr->tmp, &apr->built_values})
         b->release();
 }
+
+// One user of an APR's scratch at a time (fill_tree's fp64 sums, the staging
+// buffers of host-pointer calls, RL state): the lock serialises the callers on
+// the host, the event orders their work across their streams (a device-pointer
+// fill on one stream completes before the next caller's kernels touch the sums).
+struct ScratchGuard {
+    std::lock_guard<std::mutex> lk;
+    aprgpu_apr* apr;
+    cudaStream_t s;
+    ScratchGuard(aprgpu_apr* a, cudaStream_t st) : lk(a->exec_mu), apr(a), s(st) {
+        if (!a->scratch_ev)
+            APR_CUDA(cudaEventCreateWithFlags(&a->scratch_ev, cudaEventDisableTiming));
+        else
+            APR_CUDA(cudaStreamWaitEvent(s, a->scratch_ev, 0));
+    }
+    ~ScratchGuard() { cudaEventRecord(apr->scratch_ev, s); }
+};
 
 aprgpu::HostStencil make_host_stencil(const float* w, int kz, int kx, int ky) {
     if (kz < 1 || kx < 1 || ky < 1 || kz % 2 == 0 || kx % 2 == 0 || ky % 2 == 0)
@@ -691,6 +710,7 @@ int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_ki
         DeviceGuard g(apr->ctx->device);
         cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
         const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
+        ScratchGuard sg(apr, s);
         if (ptr_kind == APRGPU_DEVICE) {
             aprgpu::fill_tree_device(apr, leaf, tree, s);
             return;
@@ -849,6 +869,7 @@ int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_valu
             return;
         }
         need(ptr_kind == APRGPU_HOST, "bad pointer kind");
+        ScratchGuard sg(apr, s);
         apr->h_in.ensure(4 * np + 4);
         apr->h_tree.ensure(4 * nt + 4);
         apr->h_out.ensure(4 * np + 4);
@@ -879,6 +900,7 @@ void reconstruct_call(aprgpu_apr* apr, const float* values, const float* tree_va
         return;
     }
     const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
+    ScratchGuard sg(apr, s);
     apr->h_in.ensure(4 * np + 4);
     APR_CUDA(cudaMemcpyAsync(apr->h_in.p, values, 4 * np, cudaMemcpyHostToDevice, s));
     const float* tv = nullptr;
@@ -947,6 +969,7 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
         DeviceGuard g(apr->ctx->device);
         aprgpu_ctx* ctx = apr->ctx;
         cudaStream_t s = aprgpu::pick_stream(ctx, stream);
+        ScratchGuard sg(apr, s);
         // normalized_psf (deconv.hpp:26-34)
         aprgpu::HostStencil w = make_host_stencil(psf, kz, kx, ky);
         for (float v : w.w)

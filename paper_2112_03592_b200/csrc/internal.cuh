@@ -118,6 +118,10 @@ struct aprgpu_apr {
     aprgpu::GpuBuf tree_links;             // per interior node, its children (tree.cu); lazy
     std::vector<uint64_t> tree_level_first;  // first node of each interior level + the total (tree.cu); lazy
     std::mutex init_mu;                      // guards the lazy per-APR caches above (links, level starts)
+    // per-APR scratch (fill_tree's fp64 sums, host-call staging, RL state): one
+    // call at a time, and stream-ordered across callers' streams (api.cu ScratchGuard)
+    std::mutex exec_mu;
+    cudaEvent_t scratch_ev = nullptr;
     aprgpu::GpuBuf h_in, h_tree, h_out;    // staging for host-pointer calls
     aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
     aprgpu::GpuBuf tmp;                    // misc

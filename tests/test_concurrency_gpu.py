@@ -1,0 +1,85 @@
+"""Concurrent calls (inputs immutable, safe for concurrent reads):
+several host threads calling fill_tree / convolve_apr on ONE fresh APR (so the
+lazy per-APR caches -- child links, level starts, gather maps -- are built
+under contention), and pipelined host-pointer calls sharing one context.
+Every result must equal the serial one bit for bit."""
+import threading
+
+import numpy as np
+import pytest
+
+import goldens as G
+import paper_2112_03592_b200 as P
+from paper_2112_03592_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_threads(fn, n):
+    out, errs = [None] * n, []
+
+    def work(i):
+        try:
+            out[i] = fn(i)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("name", ["spheres64", "c1_256"])
+def test_concurrent_fill_and_convolve_on_one_apr(name):
+    d = G.load(name)
+    rng = np.random.default_rng(3)
+    serial_apr = G.product_apr(d)
+    values = rng.uniform(0, 100, serial_apr.access.particle_count()).astype(np.float32)
+    tv0 = P.fill_tree(serial_apr, values)
+    a = serial_apr.access
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, 3), a.l_min, a.l_max, P.PyramidMode.Restricted)
+    out0 = P.convolve_apr(serial_apr, values, tv0, pyr)
+    fresh = G.product_apr(d)  # uploaded, nothing else cached: the threads race to build the lazy caches
+    fresh.device()
+    pyr.device()
+
+    def job(i):
+        tv = P.fill_tree(fresh, values)
+        return tv, P.convolve_apr(fresh, values, tv, pyr)
+
+    for tv, out in _run_threads(job, 6):
+        assert np.array_equal(G.bits(tv), G.bits(tv0))
+        assert np.array_equal(G.bits(out), G.bits(out0))
+
+
+def test_concurrent_pipelined_host_calls(monkeypatch):
+    import torch
+    monkeypatch.setenv("APRGPU_HOST_PIPELINE_MIN", "0")
+    d = G.load("c1_256")
+    apr = G.product_apr(d)
+    dev = apr.device()
+    a = apr.access
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, 3), a.l_min, a.l_max, P.PyramidMode.Restricted)
+    pyr.device(dev.ctx)
+    rng = np.random.default_rng(5)
+    vals = [rng.uniform(0, 10, a.particle_count()).astype(np.float32) for _ in range(4)]
+    trees = [P.fill_tree(apr, v) for v in vals]
+    exp = [P.convolve_apr(apr, v, t, pyr) for v, t in zip(vals, trees)]
+    # one APR handle per thread (the staging buffers are per APR), one shared context
+    devs = [G.product_apr(d).device(dev.ctx) for _ in range(4)]
+
+    def job(i):
+        hv = torch.from_numpy(vals[i]).pin_memory()
+        ht = torch.from_numpy(trees[i]).pin_memory()
+        ho = torch.empty(a.particle_count(), dtype=torch.float32).pin_memory()
+        dp = pyr.device(devs[i].ctx)
+        L.check(L.lib().aprgpu_convolve(devs[i].handle, hv.data_ptr(), ht.data_ptr(), dp.handle, 1, L.ACCUM_EXACT,
+                                        ho.data_ptr(), L.HOST, None))
+        return ho.numpy().copy()
+
+    for i, got in enumerate(_run_threads(job, 4)):
+        assert np.array_equal(G.bits(got), G.bits(exp[i])), i
