@@ -138,7 +138,10 @@ public:
     // Device handle of an APR (uploaded on first use).  With an empty
     // tree_access the interior structure is built on the device
     // (init_tree_structure semantics).
-    aprgpu_apr* upload(const APR& apr) {
+    // Handles are shared: a call holds its APR for its duration, so an eviction
+    // by another thread frees it only after the last holder is done.
+    using Ref = std::shared_ptr<aprgpu_apr>;
+    Ref upload(const APR& apr) {
         Fingerprint f;
         f.access(apr.access);
         const bool tree = well_formed(apr.tree_access);
@@ -155,7 +158,7 @@ public:
     }
 
     // Device handle of a bare access structure (leaf only; dims = its finest grid).
-    aprgpu_apr* upload(const LinearAccess& a, const std::array<int, 3>& dims) {
+    Ref upload(const LinearAccess& a, const std::array<int, 3>& dims) {
         Fingerprint f;
         f.access(a);
         f.bytes(dims.data(), sizeof(int) * 3);
@@ -169,7 +172,7 @@ public:
     }
 
     ~Runtime() {
-        for (auto& e : cache_) aprgpu_apr_free(e.second);
+        cache_.clear();  // (the handles free themselves)
         if (ctx_) aprgpu_ctx_free(ctx_);
     }
 
@@ -182,7 +185,7 @@ private:
     }
 
     template <class Upload>
-    aprgpu_apr* lookup(std::uint64_t key, Upload&& up) {
+    Ref lookup(std::uint64_t key, Upload&& up) {
         std::lock_guard<std::mutex> lk(mu_);
         for (auto it = cache_.begin(); it != cache_.end(); ++it)
             if (it->first == key) {
@@ -191,19 +194,16 @@ private:
             }
         aprgpu_apr* h = nullptr;
         check(up(&h));
-        cache_.emplace_front(key, h);
-        while (cache_.size() > kCacheSize) {
-            aprgpu_apr_free(cache_.back().second);
-            cache_.pop_back();
-        }
-        return h;
+        cache_.emplace_front(key, Ref(h, [](aprgpu_apr* p) { aprgpu_apr_free(p); }));
+        while (cache_.size() > kCacheSize) cache_.pop_back();  // freed when its last holder lets go
+        return cache_.front().second;
     }
 
     static constexpr std::size_t kCacheSize = 8;
     aprgpu_ctx* ctx_ = nullptr;
     int accum_ = APRGPU_ACCUM_EXACT;
     std::mutex mu_;
-    std::list<std::pair<std::uint64_t, aprgpu_apr*>> cache_;
+    std::list<std::pair<std::uint64_t, Ref>> cache_;
 };
 
 // A StencilPyramid held on the device for one call.

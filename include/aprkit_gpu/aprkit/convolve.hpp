@@ -42,7 +42,8 @@ inline PixelVolume convolve_pixels(const PixelVolume& v, const Stencil& w, PadMo
 inline std::vector<std::vector<RowSpan>> nonempty_row_index(const LinearAccess& a) {
     if (!gpu::well_formed(a)) return {};
     const std::array<int, 3> dims{a.z_dim[a.l_max], a.x_dim[a.l_max], a.y_dim[a.l_max]};
-    aprgpu_apr* h = gpu::Runtime::get().upload(a, dims);
+    const auto href_ = gpu::Runtime::get().upload(a, dims);
+    aprgpu_apr* h = href_.get();
     std::vector<std::vector<RowSpan>> index(a.level_count());
     for (int l = a.l_min; l <= a.l_max; ++l) {
         std::uint64_t n = 0;
@@ -78,7 +79,8 @@ inline ParticleValues convolve_apr(const APR& apr, const ParticleValues& values,
     }
     if (values.size() != a.particle_count()) throw RangeError("convolve_apr: value count does not match the APR");
     gpu::Runtime& rt = gpu::Runtime::get();
-    aprgpu_apr* h = rt.upload(apr);
+    const auto href_ = rt.upload(apr);
+    aprgpu_apr* h = href_.get();
     const std::uint64_t nt = gpu::count(h, APRGPU_TREE);
     ParticleValues tree_filled;
     const ParticleValues* tv = &tree_values;

@@ -22,7 +22,8 @@ inline ParticleValues rl_apr(const APR& apr, const ParticleValues& observed, con
     if (observed.size() != apr.access.particle_count())
         throw RangeError("rl_apr: observation count does not match the APR");
     gpu::Runtime& rt = gpu::Runtime::get();
-    aprgpu_apr* h = rt.upload(apr);
+    const auto href_ = rt.upload(apr);
+    aprgpu_apr* h = href_.get();
     ParticleValues est(observed.size(), 0.0f);
     if (est.empty()) return est;
     const Stencil& w = cfg.psf;

@@ -20,7 +20,8 @@ namespace aprkit {
 
 // Interior-node structure (tree.hpp:26-82), built on the device; bit-identical.
 inline LinearAccess init_tree_structure(const LinearAccess& apr_access, const std::array<int, 3>& source_dims) {
-    aprgpu_apr* h = gpu::Runtime::get().upload(apr_access, source_dims);
+    const auto href_ = gpu::Runtime::get().upload(apr_access, source_dims);
+    aprgpu_apr* h = href_.get();
     return gpu::download(h, APRGPU_TREE);
 }
 
@@ -30,7 +31,8 @@ inline ParticleValues fill_tree(const APR& apr, const ParticleValues& leaf_value
     (void)threads;
     if (leaf_values.size() != apr.access.particle_count())
         throw RangeError("fill_tree: leaf value count does not match the APR");
-    aprgpu_apr* h = gpu::Runtime::get().upload(apr);
+    const auto href_ = gpu::Runtime::get().upload(apr);
+    aprgpu_apr* h = href_.get();
     ParticleValues out(gpu::count(h, APRGPU_TREE), 0.0f);
     if (out.empty() || leaf_values.empty()) return out;
     gpu::check(aprgpu_fill_tree(h, leaf_values.data(), out.data(), APRGPU_HOST, nullptr));

@@ -13,7 +13,8 @@ inline PixelVolume reconstruct_level(const APR& apr, const ParticleValues& value
     if (l < apr.access.l_min || l > apr.access.l_max) throw RangeError("reconstruct_level: level out of range");
     if (values.size() != apr.access.particle_count())
         throw RangeError("reconstruct_level: value count does not match the APR");
-    aprgpu_apr* h = gpu::Runtime::get().upload(apr);
+    const auto href_ = gpu::Runtime::get().upload(apr);
+    aprgpu_apr* h = href_.get();
     const bool tree = !tree_values.empty();
     if (tree && tree_values.size() != gpu::count(h, APRGPU_TREE))
         throw RangeError("reconstruct_level: tree value count does not match the APR");
@@ -40,7 +41,8 @@ inline PixelVolume reconstruct_patch(const APR& apr, const ParticleValues& value
         spec.z_begin > spec.z_end || spec.x_begin > spec.x_end || spec.pad < 0)
         throw RangeError("reconstruct_patch: spec outside the level grid");
     if (values.size() != a.particle_count()) throw RangeError("reconstruct_patch: value count does not match the APR");
-    aprgpu_apr* h = gpu::Runtime::get().upload(apr);
+    const auto href_ = gpu::Runtime::get().upload(apr);
+    aprgpu_apr* h = href_.get();
     const bool tree = !tree_values.empty();
     if (tree && tree_values.size() != gpu::count(h, APRGPU_TREE))
         throw RangeError("reconstruct_patch: tree value count does not match the APR");
