@@ -131,13 +131,18 @@ struct MapBox {
     // c even, with one 32-bit load
     static constexpr int CW = NC / 2;                   // code words
     // + per inner row mask and first index, nleaf, the active-block count, pad,
-    // and the active blocks' order (bytes; see k_conv_tile's map mode)
-    static constexpr int W_NLEAF = CW + 2 * kTZ * kTX, W_NBLK = W_NLEAF + 1, W_BLK = W_NLEAF + 4;
-    static constexpr int REC = W_BLK + kBlocks / 4;     // 32-bit words per record
+    // and the active blocks' order (bytes; see k_conv_tile's map mode).  H = 1:
+    // codes first; H = 2: this header first, then the codes (the 5^3 box is
+    // expanded in place over the codes, so the header must lie before them)
+    static constexpr int HDR = 2 * kTZ * kTX + 4 + kBlocks / 4;  // header words
+    static constexpr int CODE0 = H == 2 ? HDR : 0;               // first code word
+    static constexpr int MASK0 = H == 2 ? 0 : CW;                // masks, then first indices
+    static constexpr int W_NLEAF = MASK0 + 2 * kTZ * kTX, W_NBLK = W_NLEAF + 1, W_BLK = W_NLEAF + 4;
+    static constexpr int REC = CW + HDR;                // 32-bit words per record
     // bank key of an apply block: its first pair's word (H = 1: code words,
     // 32 banks; H = 2: float2 box pairs, 16 double banks) modulo the bank count
     static constexpr int NK = H == 1 ? 32 : 16;
-    static_assert((CW * 4) % 16 == 0 && (REC * 4) % 16 == 0, "16-byte bulk copies");
+    static_assert((CW * 4) % 16 == 0 && (REC * 4) % 16 == 0 && (HDR * 4) % 16 == 0, "16-byte bulk copies");
     static constexpr uint32_t ZERO = 0;
     static constexpr int NF = kFlat0 + ((NC + 3) & ~3);  // F entries
 };
@@ -942,7 +947,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
             const int r = c / M::BY;
             return __float_as_uint(S[r * B::BY + (c - r * M::BY) + (kPadY - H)]);
         };
-        for (int u = tid; u < M::CW; u += kTileThreads) rec[u] = code(2 * u) | code(2 * u + 1) << 16;
+        for (int u = tid; u < M::CW; u += kTileThreads) rec[M::CODE0 + u] = code(2 * u) | code(2 * u + 1) << 16;
         if (tid < kTZ * kTX) {  // per inner row: output mask over y0 .. y0+31 and the first output's index
             uint32_t m = 0;
             int first = -1;
@@ -952,8 +957,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                 m |= 1u << y;
                 if (first < 0) first = o;
             }
-            rec[M::CW + tid] = m;
-            rec[M::CW + kTZ * kTX + tid] = m ? orow[tid] + first : 0u;
+            rec[M::MASK0 + tid] = m;
+            rec[M::MASK0 + kTZ * kTX + tid] = m ? orow[tid] + first : 0u;
         }
         if (tid == 0) {  // runs are in row-slot order: interior rows come last
             int j = 0;
@@ -1042,7 +1047,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     // dynamic: the tile's map record, then the zero + its flattened source values
     extern __shared__ __align__(16) unsigned char map_smem[];
     uint32_t* Mb = reinterpret_cast<uint32_t*>(map_smem);
-    float* F = reinterpret_cast<float*>(Mb + M::REC);
+    // F: the staged source values.  FAST 5^3 keeps the box S between the
+    // header and F (the codes arrive at S's start and are expanded over in
+    // place: shared memory bounds its occupancy); EXACT 5^3 (register-bound)
+    // puts S after F and expands in one pass
+    constexpr bool kInPlace = H == 2 && sizeof(Acc) == 4;
+    float* F = reinterpret_cast<float*>(Mb + (kInPlace ? M::HDR + M::NC : M::REC));
     __shared__ __align__(8) uint64_t mbar;
     __shared__ Acc W[KW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1087,22 +1097,48 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __syncthreads();
     // 5^3 (H = 2): each box cell is read by ~3x more taps than at 3^3, so the
     // box is expanded once (8 cells per thread) and the apply reads it; 3^3
-    // reads cells straight through their codes
+    // reads cells straight through their codes.  The expansion writes S over
+    // the codes it reads (S[c] lands on code word c, which holds cells 2c and
+    // 2c+1): descending chunks of one 8-cell group per thread, each chunk's
+    // codes and values read before its writes, never clobber a code still to
+    // be read -- so the box needs no storage of its own beyond the codes'.
     constexpr bool kBox = H == 2;
-    float* S = F + M::NF;  // (kBox: NC floats after the source values)
+    float* S = kInPlace ? reinterpret_cast<float*>(Mb + M::HDR) : F + M::NF;  // (kBox: NC floats)
     if constexpr (kBox) {
-        const uint4* c4 = reinterpret_cast<const uint4*>(Mb);
+        const uint4* C4 = reinterpret_cast<const uint4*>(Mb + M::CODE0);
         float4* S4 = reinterpret_cast<float4*>(S);
-        for (int i = tid; i < M::NC / 8; i += kTileThreads) {
-            const uint4 c = c4[i];
-            const char* Fb = reinterpret_cast<const char*>(F);
-            auto at = [Fb](uint32_t off) { return *reinterpret_cast<const float*>(Fb + off); };
-            S4[2 * i] = make_float4(at(c.x & 0xffffu), at(c.x >> 16), at(c.y & 0xffffu), at(c.y >> 16));
-            S4[2 * i + 1] = make_float4(at(c.z & 0xffffu), at(c.z >> 16), at(c.w & 0xffffu), at(c.w >> 16));
+        const char* Fb = reinterpret_cast<const char*>(F);
+        auto at = [Fb](uint32_t off) { return *reinterpret_cast<const float*>(Fb + off); };
+        constexpr int NG = M::NC / 8;
+        static_assert(M::NC % 8 == 0, "8-cell groups");
+        auto group = [&](int g, float4& v0, float4& v1) {
+            const uint4 c = C4[g];
+            v0 = make_float4(at(c.x & 0xffffu), at(c.x >> 16), at(c.y & 0xffffu), at(c.y >> 16));
+            v1 = make_float4(at(c.z & 0xffffu), at(c.z >> 16), at(c.w & 0xffffu), at(c.w >> 16));
+        };
+        if constexpr (kInPlace) {
+#pragma unroll 1
+            for (int j = (NG - 1) / kTileThreads; j >= 0; --j) {
+                const int g = j * kTileThreads + tid;
+                float4 v0, v1;
+                if (g < NG) group(g, v0, v1);
+                __syncthreads();
+                if (g < NG) {
+                    S4[2 * g] = v0;
+                    S4[2 * g + 1] = v1;
+                }
+            }
+        } else {
+            for (int g = tid; g < NG; g += kTileThreads) {
+                float4 v0, v1;
+                group(g, v0, v1);
+                S4[2 * g] = v0;
+                S4[2 * g + 1] = v1;
+            }
         }
         __syncthreads();
     }
-    const uint32_t* omask = Mb + M::CW;
+    const uint32_t* omask = Mb + M::MASK0;
     const uint32_t* ofirst = omask + kTZ * kTX;
     // the active blocks in their bank-interleaved order (map build)
     const int nb = static_cast<int>(Mb[M::W_NBLK]);
@@ -1304,7 +1340,8 @@ void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t
 
 template <typename Acc, int H>
 void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
-    constexpr int bytes = (MapBox<H>::REC + MapBox<H>::NF + (H == 2 ? MapBox<H>::NC : 0)) * 4;
+    constexpr int bytes = (H == 2 && sizeof(Acc) == 4 ? MapBox<H>::HDR + MapBox<H>::NC + MapBox<H>::NF
+                                                       : MapBox<H>::REC + MapBox<H>::NF + (H == 2 ? MapBox<H>::NC : 0)) * 4;
     static const bool attr = [] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         return true;
