@@ -8,7 +8,8 @@
 //             device instead of an O(pixels) cover map (load_apr / read_apr,
 //             io.hpp:165, use it through this header).
 // Structures the device cannot hold (more than 20 levels, y beyond 65536)
-// are answered by the reference's own validate.
+// raise CapabilityError; the reference's validate (renamed below) is never
+// called -- there is no CPU path.
 #pragma once
 
 #define validate validate_reference_cpu_
