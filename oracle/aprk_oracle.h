@@ -111,6 +111,17 @@ int orc_rl_apr(const orc_access* leaf, const orc_access* tree, const int dims[3]
                const float* observed, const orc_pyramid* pyr_w, const orc_pyramid* pyr_wt,
                int iterations, double eps, float* out);
 
+/* generate_spheres (synthetic.hpp:74-111, no noise) into v[nz*nx*ny] and
+ * build_apr (build.hpp:290-312; constant sigma = intensity range, central
+ * differences, no smoothing) -> leaf access (malloc'd; orc_free_access) and
+ * sampled values (orc_free_values).  Multi-threaded over z planes, bit-identical
+ * to the reference (build_oracle.c).  Return 0, or -1 on bad input / no memory. */
+int orc_generate_spheres(int nz, int nx, int ny, int count, double min_r, double max_r, double background,
+                         double min_i, double max_i, double blur, uint64_t seed, int threads, float* v);
+int orc_build_apr(const float* v, int nz, int nx, int ny, double rel_error, int threads, orc_owned_access* out,
+                  float** values_out);
+void orc_free_values(float* v);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,10 @@ class Oracle:
         L.orc_restrict_stencil.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
         L.orc_convolve.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp]
         L.orc_rl_apr.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, C.c_double, vp]
+        L.orc_generate_spheres.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                           C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int, vp]
+        L.orc_build_apr.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, vp, vp]
+        L.orc_free_values.argtypes = [vp]
 
     def reflect_index(self, i: int, n: int) -> int:
         return self.L.orc_reflect_index(i, n)
@@ -122,6 +126,47 @@ class Oracle:
                      np.ctypeslib.as_array(out.level_offset, (n,)).copy())
         self.L.orc_free_access(C.byref(out))
         return res
+
+    def generate_spheres(self, dims, count, rmin, rmax, blur=2.0, seed=42, background=100.0, imin=500.0,
+                         imax=2000.0, threads=0) -> np.ndarray:
+        """generate_spheres (synthetic.hpp:74-111, no noise), multi-threaded C."""
+        threads = threads or os.cpu_count() or 1
+        out = np.empty(tuple(int(d) for d in dims), np.float32)
+        if self.L.orc_generate_spheres(int(dims[0]), int(dims[1]), int(dims[2]), int(count), C.c_double(rmin),
+                                       C.c_double(rmax), C.c_double(background), C.c_double(imin),
+                                       C.c_double(imax), C.c_double(blur), C.c_uint64(seed), int(threads),
+                                       out.ctypes.data):
+            raise MemoryError("orc_generate_spheres failed")
+        return out
+
+    def build_apr(self, vol: np.ndarray, rel_error=0.1, threads=0):
+        """build_apr (build.hpp:290-312), spheres recipe: (leaf Access, values)."""
+        threads = threads or os.cpu_count() or 1
+        v = np.ascontiguousarray(vol, np.float32)
+        out = _OrcOwned()
+        vals = C.POINTER(C.c_float)()
+        if self.L.orc_build_apr(v.ctypes.data, v.shape[0], v.shape[1], v.shape[2], C.c_double(rel_error),
+                                int(threads), C.byref(out), C.byref(vals)):
+            raise MemoryError("orc_build_apr failed")
+        n = out.l_max + 1
+        res = Access(out.l_min, out.l_max,
+                     np.ctypeslib.as_array(out.z_dim, (n,)).copy(), np.ctypeslib.as_array(out.x_dim, (n,)).copy(),
+                     np.ctypeslib.as_array(out.y_dim, (n,)).copy(),
+                     np.ctypeslib.as_array(out.y_idx, (max(out.n_particles, 1),))[:out.n_particles].copy(),
+                     np.ctypeslib.as_array(out.xz_end, (max(out.n_rows, 1),))[:out.n_rows].copy(),
+                     np.ctypeslib.as_array(out.level_offset, (n,)).copy())
+        values = np.ctypeslib.as_array(vals, (max(out.n_particles, 1),))[:out.n_particles].copy()
+        self.L.orc_free_access(C.byref(out))
+        self.L.orc_free_values(vals)
+        return res, values
+
+    def build_spheres(self, n, count, rmin, rmax, blur=2.0, seed=42, rel_error=0.1, threads=0):
+        """generate_spheres + build_apr of an n^3 (or (nz, nx, ny)) sphere scene."""
+        dims = (n, n, n) if np.isscalar(n) else tuple(n)
+        vol = self.generate_spheres(dims, count, rmin, rmax, blur, seed, threads=threads)
+        acc, values = self.build_apr(vol, rel_error, threads)
+        del vol
+        return acc, values
 
     def fill_tree(self, leaf, tree, dims, values) -> np.ndarray:
         keep = []

@@ -404,6 +404,11 @@ class DevicePyramid:
                                                        C.byref(h)))
         self.handle = h
         self.l_min, self.l_max = pyr.l_min, pyr.l_max
+        self.k3 = {pyr.l_min + i: (s.kz, s.kx, s.ky) for i, s in enumerate(pyr.stencils)}
+
+    def half_width(self, l_lo: int, l_hi: int) -> int:
+        """Largest stencil half-width over levels [l_lo, l_hi] (any axis)."""
+        return max([max(k) // 2 for l, k in self.k3.items() if l_lo <= l <= l_hi] or [0])
 
     def __del__(self):
         try:
@@ -492,11 +497,19 @@ class DeviceApr:
                                         int(pad), accum, _ptr(out), L.HOST, None))
         return out
 
-    def rl(self, observed: np.ndarray, psf: Stencil, iterations: int, epsilon: float, accum: int) -> np.ndarray:
+    def rl(self, observed: np.ndarray, psf: Stencil, iterations: int, epsilon: float, accum: int,
+           estimate=None) -> np.ndarray:
+        """aprgpu_rl, or aprgpu_rl_resume from a running estimate (host arrays)."""
         observed = np.ascontiguousarray(observed, dtype=np.float32)
         out = np.empty(self.n_particles, np.float32)
-        L.check(L.lib().aprgpu_rl(self.handle, _ptr(observed), _ptr(psf.weights), psf.kz, psf.kx, psf.ky,
-                                  int(iterations), float(epsilon), accum, _ptr(out), L.HOST, None))
+        if estimate is None:
+            L.check(L.lib().aprgpu_rl(self.handle, _ptr(observed), _ptr(psf.weights), psf.kz, psf.kx, psf.ky,
+                                      int(iterations), float(epsilon), accum, _ptr(out), L.HOST, None))
+        else:
+            est = np.ascontiguousarray(estimate, dtype=np.float32)
+            L.check(L.lib().aprgpu_rl_resume(self.handle, _ptr(observed), _ptr(est), _ptr(psf.weights), psf.kz,
+                                             psf.kx, psf.ky, int(iterations), float(epsilon), accum, _ptr(out),
+                                             L.HOST, None))
         return out
 
     def reconstruct_level(self, values: np.ndarray, tree_values, level: int) -> np.ndarray:
@@ -677,6 +690,16 @@ def rl_apr(apr: APR, observed, cfg: RLConfig, observer=None) -> np.ndarray:
     the observer between blocks, as the reference does)."""
     dev = apr.device()
     acc = _accum(cfg.accum)
-    if observer is None or cfg.record_metrics_every <= 0:
+    if observer is None or cfg.record_metrics_every <= 0 or cfg.iterations <= 0:
         return dev.rl(observed, cfg.psf, cfg.iterations, cfg.epsilon, acc)
-    raise NotImplementedError("rl_apr observer callbacks are not supported on the device path yet")
+    # the reference's state between iterations is (u, eps, estimate): resuming
+    # the device iteration every record_metrics_every iterations is bit-identical
+    # to one uninterrupted run (aprgpu_rl_resume; deconv.hpp:103-104)
+    every, done, est = cfg.record_metrics_every, 0, None
+    while done < cfg.iterations:
+        n = min(every, cfg.iterations - done)
+        est = dev.rl(observed, cfg.psf, n, cfg.epsilon, acc, estimate=est)
+        done += n
+        if done % every == 0:
+            observer(done, est)
+    return est

@@ -143,12 +143,15 @@ void push_level(aprgpu_pyramid* p, const aprgpu::HostStencil& s) {
     p->w_host.insert(p->w_host.end(), s.w.begin(), s.w.end());
 }
 
-__global__ void k_clamp_copy(const float* __restrict__ in, float* __restrict__ u, float* __restrict__ est, uint64_t n) {
+// u = max(in, 0) (deconv.hpp:89), and the same into est unless est is null
+// (a resumed run keeps its running estimate).  in may alias est: every
+// element is read before it is written, by the same thread.
+__global__ void k_clamp_copy(const float* in, float* __restrict__ u, float* est, uint64_t n) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const float v = in[i];
         const float c = v < 0.0f ? 0.0f : v;  // std::max(v, 0.0f), deconv.hpp:89
         u[i] = c;
-        est[i] = c;
+        if (est) est[i] = c;
     }
 }
 
@@ -1008,11 +1011,13 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
         }
         float* est = ptr_kind == APRGPU_DEVICE ? out : apr->h_out.as<float>();
         float* u = apr->rl_u.as<float>();
-        k_clamp_copy<<<std::min<unsigned>(aprgpu::blocks_for(np, 256), ctx->sm_count * 8), 256, 0, s>>>(obs_dev, u, est,
-                                                                                                       np);
+        // resume: the running estimate replaces the clamped observation, so the
+        // clamp writes u only (estimate_in may be out itself: an in-place resume)
+        k_clamp_copy<<<std::min<unsigned>(aprgpu::blocks_for(np, 256), ctx->sm_count * 8), 256, 0, s>>>(
+            obs_dev, u, estimate_in ? nullptr : est, np);
         aprgpu::count_launch(ctx);
         APR_CUDA(cudaGetLastError());
-        if (estimate_in && estimate_in != est)  // resume: the running estimate replaces the clamped observation
+        if (estimate_in && estimate_in != est)
             APR_CUDA(cudaMemcpyAsync(est, estimate_in, 4 * np,
                                      ptr_kind == APRGPU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
         // mean of the clamped observations in the reference's sequential order

@@ -262,11 +262,10 @@ void launch_conv(aprgpu_ctx* ctx, ConvArgs& a, cudaStream_t s) {
     while (nw > 1 && wbytes + per_warp * nw > budget) --nw;
     const size_t smem = wbytes + per_warp * nw;
     if (smem > 227 * 1024) fail(APRGPU_ERR_CAPABILITY, "stencil too large for the shared-memory tile");
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
+    static OncePerDevice attr;  // per instantiation and device
+    attr([] {
         APR_CUDA(cudaFuncSetAttribute(k_conv<Acc, KZ, KX, KY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
+    });
     const uint64_t blocks64 = (a.n_work + nw - 1) / nw;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(blocks64, 1u << 30));
     k_conv<Acc, KZ, KX, KY><<<grid, nw * 32, smem, s>>>(a);

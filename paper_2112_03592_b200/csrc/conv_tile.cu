@@ -579,16 +579,29 @@ __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz
 // at a time.  Output (oz, ox, oy) of block (qz, qx, qy) is inner row
 // r = (2qz + oz) * 8 + 2qx + ox at y = 2qy + oy; its particle is
 // ofirst[r] + popc(omask[r] below y).
+// Tile-local output rows [lo, hi) a slab-restricted launch may write (a tile
+// can straddle two slabs: its other rows belong to the neighbour, whose inputs
+// were never exchanged); every row otherwise.
+struct RowRange {
+    int lo, hi;
+};
+__device__ __forceinline__ RowRange slab_rows(const TileLaunch& a, int l, int z0) {
+    if (l < a.slab_lc) return RowRange{0, kTZ};
+    const int sh = a.leaf.l_max - l;
+    const int zlo = a.slab_zlo >> sh, zhi = (a.slab_zhi + (1 << sh) - 1) >> sh;
+    return RowRange{max(zlo - z0, 0), min(zhi - z0, kTZ)};
+}
+
 template <typename Acc>
 __device__ __forceinline__ void store_block(const TileLaunch& a, const uint32_t* omask, const uint32_t* ofirst, int qz,
-                                            int qx, int qy, const Acc (&acc)[8]) {
+                                            int qx, int qy, const Acc (&acc)[8], RowRange rr) {
     uint32_t idx[8];
     bool ok[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int oz = j >> 2, ox = (j >> 1) & 1, oy = j & 1;
         const int r = (2 * qz + oz) * kTX + 2 * qx + ox, y = 2 * qy + oy;
-        const uint32_t m = omask[r];
+        const uint32_t m = (2 * qz + oz >= rr.lo && 2 * qz + oz < rr.hi) ? omask[r] : 0u;
         ok[j] = (m >> y) & 1u;
         idx[j] = ofirst[r] + __popc(m & ((1u << y) - 1u));
     }
@@ -1016,6 +1029,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __syncthreads();
 
     // ---- apply: one thread per active block, 8 outputs
+    const RowRange rr = slab_rows(a, l, G.z0);
     for (int q = tid; q < nb; q += kTileThreads) {
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
@@ -1029,7 +1043,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
 #pragma unroll
                 for (int oy = 0; oy < 2; ++oy) {
                     const int off = o[(oz * kTX + ox) * kTY + oy];
-                    if (off == 0xff) continue;
+                    if (off == 0xff || 2 * qz + oz < rr.lo || 2 * qz + oz >= rr.hi) continue;
                     store_out(a, orow[(2 * qz + oz) * kTX + 2 * qx + ox] + off, to_f(acc[(oz * 2 + ox) * 2 + oy]));
                 }
     }
@@ -1059,11 +1073,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
     const int l = a.lvl[s];
     const uint32_t tix = a.tile_base + blockIdx.x;
-    if (l >= a.slab_lc) {  // slab decomposition: only tiles touching this slab's planes
-        const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
-        const int sh = a.leaf.l_max - l;
-        if ((z0 + kTZ) << sh <= a.slab_zlo || z0 << sh >= a.slab_zhi) return;
-    }
+    const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
+    const RowRange rr = slab_rows(a, l, z0);
+    if (rr.lo >= rr.hi) return;  // slab decomposition: no row of this tile is in the slab
     const uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
     // the record and the flattened source list stream in by two bulk copies; the
     // record's is issued before the list's extent is known (its bytes are
@@ -1159,7 +1171,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                 },
                 W, qz, qx, qy, acc);
         }
-        store_block(a, omask, ofirst, qz, qx, qy, acc);
+        store_block(a, omask, ofirst, qz, qx, qy, acc, rr);
     }
 }
 
@@ -1202,7 +1214,7 @@ void set_level(TileLaunch& a, const DevAccess& L, int l, uint32_t end) {
 // First use of an APR by the tile path: probe every tile once.
 void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
     DevAccess& L = apr->leaf;
-    if (L.tile_meta || !L.tiles) return;
+    if (acquire_ptr(L.tile_meta) || !L.tiles) return;
     std::lock_guard<std::mutex> lk(apr->ctx->mu);
     if (L.tile_meta) return;
     const uint64_t n = L.tile_off[L.l_max + 1];
@@ -1225,14 +1237,14 @@ void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
         APR_CUDA(cudaGetLastError());
         APR_CUDA(cudaStreamSynchronize(s));
     }
-    L.tile_meta = meta;
+    publish_ptr(L.tile_meta, meta);
 }
 
 // First use of an APR with stencil half-width H: the per-tile source runs.
 template <int H>
 void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
     DevAccess& L = apr->leaf;
-    if (L.tile_runs[H - 1] || !L.tiles) return;
+    if (acquire_ptr(L.tile_runs[H - 1]) || !L.tiles) return;
     std::lock_guard<std::mutex> lk(apr->ctx->mu);
     if (L.tile_runs[H - 1]) return;
     const uint64_t n = L.tile_off[L.l_max + 1];
@@ -1277,7 +1289,7 @@ void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
         APR_CUDA(cudaMalloc(&runs, 8));
     }
     L.tile_run_off[H - 1] = off;
-    L.tile_runs[H - 1] = runs;
+    publish_ptr(L.tile_runs[H - 1], runs);  // (tile_run_off is read only after tile_runs)
 }
 
 // per tile: its flattened source count (sum of its run lengths), padded to 4
@@ -1328,11 +1340,10 @@ void ensure_tile_flat(aprgpu_apr* apr, cudaStream_t s) {
 template <typename Acc, int H, bool MAP = false>
 void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
     constexpr int bytes = Box<H>::NC * static_cast<int>(sizeof(float));
-    static const bool attr = [] {
+    static OncePerDevice attr;
+    attr([] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_tile<Acc, H, MAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        return true;
-    }();
-    (void)attr;
+    });
     k_conv_tile<Acc, H, MAP><<<n, kTileThreads, bytes, s>>>(a);
     count_launch(ctx);
     APR_CUDA(cudaGetLastError());
@@ -1342,16 +1353,15 @@ template <typename Acc, int H>
 void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
     constexpr int bytes = (H == 2 && sizeof(Acc) == 4 ? MapBox<H>::HDR + MapBox<H>::NC + MapBox<H>::NF
                                                        : MapBox<H>::REC + MapBox<H>::NF + (H == 2 ? MapBox<H>::NC : 0)) * 4;
-    static const bool attr = [] {
+    static OncePerDevice attr;
+    attr([] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         // 3^3 EXACT (6 CTAs/SM, register-bound): a 132 KB carveout leaves the
         // gathers more L1 (measured 0.188 -> 0.186 ms on C3; FAST's default
         // carveout is already its best)
         if (sizeof(Acc) == 8 && H == 1)
             APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributePreferredSharedMemoryCarveout, 58));
-        return true;
-    }();
-    (void)attr;
+    });
     k_conv_map<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
     count_launch(ctx);
     APR_CUDA(cudaGetLastError());
@@ -1373,11 +1383,11 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, c
     const int pm = pad == APRGPU_PAD_ZERO ? 1 : 0;
     auto rec_bytes = [&](int l) { return (L.tile_off[l + 1] - L.tile_off[l]) * MapBox<H>::REC * sizeof(uint32_t); };
     for (int i = 0; i < b.n_levels; ++i)
-        if (L.tile_map_fail[H - 1][pm][b.lvl[i]]) return false;
+        if (__atomic_load_n(&L.tile_map_fail[H - 1][pm][b.lvl[i]], __ATOMIC_ACQUIRE)) return false;
     auto missing = [&] {
         size_t need = 0;
         for (int i = 0; i < b.n_levels; ++i)
-            if (!L.tile_map[H - 1][pm][b.lvl[i]]) need += rec_bytes(b.lvl[i]);
+            if (!acquire_ptr(L.tile_map[H - 1][pm][b.lvl[i]])) need += rec_bytes(b.lvl[i]);
         return need;
     };
     if (missing()) {
@@ -1387,14 +1397,22 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, c
             size_t free_b = 0, total_b = 0;
             APR_CUDA(cudaMemGetInfo(&free_b, &total_b));
             if (need > free_b / 2) {
-                for (int i = 0; i < b.n_levels; ++i) L.tile_map_fail[H - 1][pm][b.lvl[i]] = 1;
+                for (int i = 0; i < b.n_levels; ++i)
+                    __atomic_store_n(&L.tile_map_fail[H - 1][pm][b.lvl[i]], 1, __ATOMIC_RELEASE);
                 return false;
             }
             ensure_tile_flat<H>(apr, s);
-            for (int i = 0; i < b.n_levels; ++i)
-                if (!L.tile_map[H - 1][pm][b.lvl[i]]) APR_CUDA(cudaMalloc(&L.tile_map[H - 1][pm][b.lvl[i]], rec_bytes(b.lvl[i])));
+            // built into local buffers, published only after the build kernel
+            // has completed and passed the overflow check
+            uint32_t* fresh[kMaxLevels] = {};
             TileLaunch m = b;
-            for (int i = 0; i < b.n_levels; ++i) m.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
+            for (int i = 0; i < b.n_levels; ++i) {
+                m.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
+                if (!m.map[i]) {
+                    APR_CUDA(cudaMalloc(&fresh[i], rec_bytes(b.lvl[i])));
+                    m.map[i] = fresh[i];
+                }
+            }
             m.flat = L.tile_flat[H - 1];
             m.flat_off = L.tile_flat_off[H - 1];
             m.slab_lc = 1 << 20;  // every tile: a map serves every slab
@@ -1408,12 +1426,13 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, c
             APR_CUDA(cudaStreamSynchronize(s));
             if (over) {  // some tile has too many sources for k_conv_map: reconstruct these levels
                 for (int i = 0; i < b.n_levels; ++i) {
-                    cudaFree(L.tile_map[H - 1][pm][b.lvl[i]]);
-                    L.tile_map[H - 1][pm][b.lvl[i]] = nullptr;
-                    L.tile_map_fail[H - 1][pm][b.lvl[i]] = 1;
+                    if (fresh[i]) cudaFree(fresh[i]);
+                    __atomic_store_n(&L.tile_map_fail[H - 1][pm][b.lvl[i]], 1, __ATOMIC_RELEASE);
                 }
                 return false;
             }
+            for (int i = 0; i < b.n_levels; ++i)
+                if (fresh[i]) publish_ptr(L.tile_map[H - 1][pm][b.lvl[i]], fresh[i]);
         }
     }
     for (int i = 0; i < b.n_levels; ++i) b.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];

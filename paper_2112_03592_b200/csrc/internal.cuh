@@ -232,6 +232,32 @@ struct HostStencil {
 HostStencil restrict_stencil_host(const HostStencil& w, int delta);
 HostStencil gaussian_stencil_host(double sigma, int size);
 
+// Lazily built per-APR device caches are double-checked: read without the
+// lock (acquire), built and published under it (release) only after the
+// kernels that fill them have completed -- so a reader on another thread and
+// stream never sees a pointer to unfilled memory.
+template <class T>
+inline T* acquire_ptr(T* const& p) { return __atomic_load_n(&p, __ATOMIC_ACQUIRE); }
+template <class T>
+inline void publish_ptr(T*& p, T* v) { __atomic_store_n(&p, v, __ATOMIC_RELEASE); }
+
+// Kernel attributes (dynamic shared-memory limit, carveout) are per device:
+// `set` runs once per device ordinal (a context may live on any GPU of the
+// process).  Setting an attribute twice is harmless, so racing callers need no
+// lock -- only the published bit is ordered.
+struct OncePerDevice {
+    std::atomic<uint64_t> done{0};
+    template <class F>
+    void operator()(F&& set) {
+        int dev = 0;
+        APR_CUDA(cudaGetDevice(&dev));
+        const uint64_t bit = 1ull << (dev & 63);
+        if (done.load(std::memory_order_acquire) & bit) return;
+        set();
+        done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+};
+
 inline void count_launch(aprgpu_ctx* ctx, uint64_t n = 1) { ctx->launches.fetch_add(n, std::memory_order_relaxed); }
 
 inline cudaStream_t pick_stream(aprgpu_ctx* ctx, void* s) {

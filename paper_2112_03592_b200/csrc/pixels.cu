@@ -302,15 +302,14 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
         const unsigned g = static_cast<unsigned>(static_cast<uint64_t>(szd) * sxd * syd);
         const int h = kz / 2;
         const int rb = (kz + 2) * (kSx + 2 * h) * (kSy + 8) * static_cast<int>(sizeof(float));
-        static const bool sattr = [] {
+        static OncePerDevice sattr;
+        sattr([] {
             const int mx = 7 * (kSx + 4) * (kSy + 8) * static_cast<int>(sizeof(float));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<double, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<double, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<float, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            return true;
-        }();
-        (void)sattr;
+        });
         if (kz == 3) {
             if (ex) k_convolve_pixels_stream<double, 3><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
             else k_convolve_pixels_stream<float, 3><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
@@ -328,15 +327,14 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
         const unsigned g = static_cast<unsigned>(static_cast<uint64_t>(tzd) * txd * ityd);
         const int h = kz / 2;
         const int ib = (kPz + 2 * h) * (kPx + 2 * h) * (kIsoPy + 2 * h) * static_cast<int>(sizeof(float));
-        static const bool iattr = [] {
+        static OncePerDevice iattr;
+        iattr([] {
             const int mx = (kPz + 4) * (kPx + 4) * (kIsoPy + 4) * static_cast<int>(sizeof(float));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<double, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<double, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_iso<float, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            return true;
-        }();
-        (void)iattr;
+        });
         if (kz == 3) {
             if (ex) k_convolve_pixels_iso<double, 3><<<g, kPixThreads, ib, s>>>(a, ityd, txd);
             else k_convolve_pixels_iso<float, 3><<<g, kPixThreads, ib, s>>>(a, ityd, txd);
@@ -349,13 +347,12 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
         return;
     }
     const int bytes = (kPz + 2 * (kz / 2)) * (kPx + 2 * (kx / 2)) * (kPy + 2 * (ky / 2)) * static_cast<int>(sizeof(float));
-    static const bool attr = [] {
+    static OncePerDevice attr;
+    attr([] {
         const int mx = (kPz + kPixMaxK - 1) * (kPx + kPixMaxK - 1) * (kPy + kPixMaxK - 1) * static_cast<int>(sizeof(float));
         APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        return true;
-    }();
-    (void)attr;
+    });
     if (accum == APRGPU_ACCUM_EXACT)
         k_convolve_pixels<double><<<static_cast<unsigned>(blocks), kPixThreads, bytes, s>>>(a, tyd, txd);
     else

@@ -279,6 +279,10 @@ class SlabConvolver:
 
     def convolve(self, pyr, pad: int = L.PAD_REFLECT, accum: int = L.ACCUM_EXACT):
         p = self.plan
+        hw = pyr.half_width(p.lc, p.l_max) if hasattr(pyr, "half_width") else None
+        if hw is not None and hw > p.halo:
+            raise ValueError(f"stencil half-width {hw} at the partitioned levels exceeds the plan's halo "
+                             f"of {p.halo} rows: make the SlabPlan with halo >= {hw}")
         self.comm.exchange(self.states, "values", p.halo_transfers("leaf"))
         self.fill_tree()
         if p.tree is not None:

@@ -83,3 +83,39 @@ def test_concurrent_pipelined_host_calls(monkeypatch):
 
     for i, got in enumerate(_run_threads(job, 4)):
         assert np.array_equal(G.bits(got), G.bits(exp[i])), i
+
+
+@pytest.mark.parametrize("name", ["c1_256"])
+def test_concurrent_device_pointer_convolve_fresh_apr(name):
+    """Device-pointer convolve_apr (no per-APR scratch, no lock on the hot
+    path) from 6 threads, each on its own stream, against a FRESH APR: the
+    threads race to build the gather maps; a thread must never launch on a
+    map another thread has allocated but not yet built."""
+    import torch
+    d = G.load(name)
+    rng = np.random.default_rng(11)
+    ref_apr = G.product_apr(d)
+    values = rng.uniform(0, 100, ref_apr.access.particle_count()).astype(np.float32)
+    tv = P.fill_tree(ref_apr, values)
+    a = ref_apr.access
+    exp = {}
+    for k in (3, 5):
+        pyr = P.make_pyramid(P.gaussian_stencil(1.0, k), a.l_min, a.l_max, P.PyramidMode.Restricted)
+        exp[k] = (pyr, P.convolve_apr(ref_apr, values, tv, pyr))
+    fresh = G.product_apr(d).device()
+    dv = torch.from_numpy(values).cuda()
+    dt = torch.from_numpy(tv).cuda()
+    pyrs = {k: p.device(fresh.ctx) for k, (p, _) in exp.items()}
+    torch.cuda.synchronize()
+
+    def job(i):
+        k = 3 if i % 2 == 0 else 5
+        st = torch.cuda.Stream()
+        out = torch.full((fresh.n_particles,), float("nan"), device="cuda")
+        torch.cuda.synchronize()
+        fresh.convolve_ptr(dv.data_ptr(), dt.data_ptr(), pyrs[k], 1, L.ACCUM_EXACT, out.data_ptr(), st.cuda_stream)
+        st.synchronize()
+        return k, out.cpu().numpy()
+
+    for k, got in _run_threads(job, 6):
+        assert np.array_equal(G.bits(got), G.bits(exp[k][1])), k

@@ -111,3 +111,35 @@ def test_oracle_vs_live_reference_random():
                 a = R.convolve(apr, v, tv, pyr, pad, threads=2)
                 b = ORC.convolve(leaf, tree, v, tv, lv, leaf.l_min, pad)
                 assert np.array_equal(G.bits(a), G.bits(b))
+
+
+def test_oracle_builder_matches_c1_golden():
+    """The multi-threaded C builder (oracle/build_oracle.c) reproduces the
+    reference-built C1 fixture (256^3 spheres, BASELINE config 1) bit for bit:
+    structure and sampled values."""
+    d = G.load("c1_256")
+    acc, vals = ORC.build_spheres(256, 12, 6.0, 20.0, blur=2.0, seed=42, rel_error=0.1)
+    g = G.oracle_access(d, "leaf_")
+    assert (acc.l_min, acc.l_max) == (g.l_min, g.l_max)
+    assert np.array_equal(acc.y_idx, g.y_idx)
+    assert np.array_equal(acc.xz_end, g.xz_end)
+    assert np.array_equal(acc.level_offset[acc.l_min:], g.level_offset[g.l_min:])
+    assert np.array_equal(G.bits(vals), G.bits(d["values"]))
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("dims,count,rmin,rmax,seed", [((64, 64, 64), 6, 3.0, 10.0, 7), ((40, 33, 57), 5, 2.0, 8.0, 3),
+                                                       ((7, 9, 5), 2, 1.0, 3.0, 1), ((48, 40, 56), 7, 2.5, 9.0, 42)])
+def test_oracle_builder_matches_live_reference(dims, count, rmin, rmax, seed):
+    """generate_spheres + build_apr of the C builder vs the unmodified reference
+    (oracle/_ref), non-power-of-two and anisotropic dims included."""
+    R = Ref()
+    vol = ORC.generate_spheres(dims, count, rmin, rmax, 2.0, seed, threads=4)
+    rvol = R.generate_spheres(dims, count, rmin, rmax, 2.0, 0.0, seed)
+    assert np.array_equal(G.bits(vol), G.bits(rvol))
+    acc, vals = ORC.build_apr(vol, 0.1, threads=4)
+    r = R.build_apr(rvol, 0.1)
+    ra = r.leaf
+    for f in ("y_idx", "xz_end", "level_offset", "z_dim", "x_dim", "y_dim"):
+        assert np.array_equal(getattr(acc, f), getattr(ra, f)), f
+    assert np.array_equal(G.bits(vals), G.bits(r.values()))

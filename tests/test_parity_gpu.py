@@ -177,6 +177,42 @@ def test_rl_apr_bit_exact(name):
         assert np.array_equal(G.bits(out), G.bits(d[f"rl_g{k}_out"])), k
 
 
+def test_rl_apr_observer_bit_exact():
+    """rl_apr with an observer (deconv.hpp:103-104): the device iteration is
+    resumed every record_metrics_every iterations; the final estimate and every
+    observed estimate equal uninterrupted runs of that many iterations."""
+    d = G.load("rl_spheres64")
+    apr = G.product_apr(d)
+    psf = P.Stencil(3, 3, 3, weights=d["rl_g3_psf"])
+    seen = []
+    cfg = P.RLConfig(iterations=10, psf=psf, record_metrics_every=3)
+    out = P.rl_apr(apr, d["values"], cfg, observer=lambda k, est: seen.append((k, est.copy())))
+    assert [k for k, _ in seen] == [3, 6, 9]
+    assert np.array_equal(G.bits(out), G.bits(d["rl_g3_out"]))
+    for k, est in seen:
+        ref = P.rl_apr(apr, d["values"], P.RLConfig(iterations=k, psf=psf))
+        assert np.array_equal(G.bits(est), G.bits(ref)), k
+
+
+def test_rl_resume_in_place_device():
+    """aprgpu_rl_resume with estimate_in == out on device pointers (an in-place
+    resume) continues from the running estimate: 4 + 6 iterations == 10."""
+    import torch
+    from paper_2112_03592_b200.aprkit import _ptr
+    d = G.load("rl_spheres64")
+    apr = G.product_apr(d)
+    dev = apr.device()
+    psf = P.Stencil(3, 3, 3, weights=d["rl_g3_psf"])
+    obs = torch.from_numpy(np.ascontiguousarray(d["values"], np.float32)).cuda()
+    est = torch.empty_like(obs)
+    s = torch.cuda.current_stream().cuda_stream or None
+    dev.rl_ptr(obs.data_ptr(), psf, 4, 0.0, L.ACCUM_EXACT, est.data_ptr(), s or 0)
+    L.check(L.lib().aprgpu_rl_resume(dev.handle, obs.data_ptr(), est.data_ptr(), _ptr(psf.weights),
+                                     3, 3, 3, 6, 0.0, L.ACCUM_EXACT, est.data_ptr(), L.DEVICE, s))
+    torch.cuda.synchronize()
+    assert np.array_equal(G.bits(est.cpu().numpy()), G.bits(d["rl_g3_out"]))
+
+
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_random_values_and_stencils_vs_oracle(seed):
     """Fresh random values / stencils (incl. anisotropic, 7^3, 13^3, zero pad)
