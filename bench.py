@@ -1,15 +1,18 @@
 """Benchmark: APR-native 3x3x3 convolution (restricted Gaussian pyramid) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1] [--stencil 3|5]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1|c4] [--stencil 3|5]
+                    [--accum exact|fast] [--impl ours|reference]
 
 A "step" is one convolve_apr pass (conv-only protocol, bench.hpp:158-169) over
 the whole APR of the configuration, values and interior-node values resident in
-HBM.  value = pixel-equivalent GB/s (4 * N_pixels / t, metrics.hpp:15-21);
-particles/s, the roofline of the conv pass, the paper protocol (row index +
-tree fill + conv) and the end-to-end host-buffer number through
-the C-ABI are reported beside it.  --impl reference times the reference's own
-CPU convolve_apr (oracle/_ref, all host threads) on the same workload.
+HBM, accumulated in fp64 in the reference's tap order (EXACT, bit-identical to
+the reference; --accum fast for fp32).  value = pixel-equivalent GB/s
+(4 * N_pixels / t, metrics.hpp:15-21); particles/s, the roofline of the conv
+pass, the other stencil/accumulation variants, the paper protocol (row index +
+tree fill + conv), a cold first call and the end-to-end
+host-buffer number through the C-ABI are reported beside it.  --impl reference
+times the reference's own CPU convolve_apr (oracle/_ref, all host threads) on
+the same workload, never loading the product library.
 """
 from __future__ import annotations
 
@@ -113,27 +116,42 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload --
+WORKLOADS = {
+    "c1": "C1: 256^3 spheres (12, r 6-20, blur 2, seed 42) -> APR E=0.1",
+    "c3": "C3: 1024^3 spheres (48, r 24-80, blur 2, seed 42) -> APR E=0.1",
+    "c4": "C4: the C3 APR tiled 4(z) x 4(x) x 2(y) -> 4096 x 4096 x 2048 pixel-equivalent (paper's concatenated copies)",
+}
+SPHERES = {"c1": (256, 12, 6.0, 20.0), "c3": (1024, 48, 24.0, 80.0)}
+L2_NOTE = "GPU arm: L2 flushed between timed steps (256 MB write); reference arm: host CPU, no flush"
+
+
+def bench_config(cfg: str, k: int, n_p: int, n_t: int, n_pix: int) -> dict:
+    """The `config` dict -- identical in both arms (same workload, same stencil)."""
+    return {"workload": WORKLOADS[cfg], "stencil": f"gaussian(1.0,{k}) restricted pyramid", "pad": "reflect",
+            "particles": int(n_p), "interior_nodes": int(n_t), "pixels": int(n_pix), "cr": round(n_pix / n_p, 2),
+            "protocol": "conv-only (tree values filled outside the timed region, bench.hpp:158-169)", "l2": L2_NOTE}
+
+
 def workload(cfg: str):
-    """Returns (APR, leaf values, description dict)."""
-    import paper_2112_03592_b200 as P
+    """Returns (APR, leaf values, input provenance) built on the device (ours)."""
+    import paper_2112_03592_b200 as P  # noqa: F401
     if cfg == "c1":
         import goldens as G
         d = G.load("c1_256")
-        return G.product_apr(d), d["values"], {"workload": "C1: 256^3 spheres (12, r 6-20, blur 2, seed 42) -> "
-                                                            "APR E=0.1 (reference-built, committed fixture)"}
+        return G.product_apr(d), d["values"], "reference-built committed fixture (tests/golden/c1_256.npz)"
     if cfg == "c3":
         from paper_2112_03592_b200 import synth
-        apr, values = synth.build_spheres_apr(1024, count=48, rmin=24.0, rmax=80.0, blur=2.0, seed=42,
+        n, count, rmin, rmax = SPHERES["c3"]
+        apr, values = synth.build_spheres_apr(n, count=count, rmin=rmin, rmax=rmax, blur=2.0, seed=42,
                                               rel_error=0.1)
-        return apr, values, {"workload": "C3: 1024^3 spheres (48, r 24-80, blur 2, seed 42) -> APR E=0.1 "
-                                         "(built on the GPU by paper_2112_03592_b200.synth)"}
+        return apr, values, "built on the GPU by paper_2112_03592_b200.synth (bit-identical to the reference build)"
     raise SystemExit(f"unknown config {cfg}")
 
 
 def ncu_traffic(config: str, stencil: int, accum: str):
     """dram__bytes_read.sum + dram__bytes_write.sum of one conv pass, from the
-    committed ncu capture of this workload (profiles/<round>/traffic.json,
-    written by tools/traffic.py from tools/gpu_round.sh's ncu pass), or None."""
+    committed ncu capture of this workload (the newest profiles/<round>/traffic.json),
+    or None."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
         try:
@@ -147,13 +165,10 @@ def ncu_traffic(config: str, stencil: int, accum: str):
     return None, None
 
 
-def algorithmic_bytes(apr) -> int:
+def algorithmic_bytes(n_p: int, n_t: int, n_rows: int) -> int:
     """Per conv pass: y_idx u16 + value in f32 + out f32 per particle, y_idx u16 +
     value f32 per interior node, one u32 row begin per row (device layout)."""
-    n_p = apr.access.particle_count()
-    n_t = apr.tree_access.particle_count()
-    rows = apr.access.row_count() + apr.tree_access.row_count()
-    return 10 * n_p + 6 * n_t + 4 * rows
+    return 10 * n_p + 6 * n_t + 4 * n_rows
 
 
 # ------------------------------------------------------------------ our arm ---
@@ -172,6 +187,7 @@ def run_ours(args, rank, world):
     s = stream.cuda_stream
     assert s != 0
     t0 = time.time()
+    apr = values = None
     if args.config == "c4":
         # C3 built on the device, tiled 4(z) x 4(x) x 2(y) on the device
         from paper_2112_03592_b200 import synth
@@ -182,15 +198,13 @@ def run_ours(args, rank, world):
         v = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")
         synth.tile_values(d3, dapr, 4, 4, 2, v3.data_ptr(), v.data_ptr())
         del v3
-        apr, values = None, None
+        provenance = "C3 built on the GPU, tiled on the GPU (aprgpu_tile_apr)"
         li, ti = dapr.info(L.LEAF), dapr.info(L.TREE)
         n_p, n_t, n_rows = int(li.n_particles), int(ti.n_particles), int(li.n_rows + ti.n_rows)
         l_min, l_max = int(li.l_min), int(li.l_max)
         n_pix = int(np.prod(dapr.dims, dtype=np.int64))
-        desc = {"workload": "C4: the C3 APR tiled 4(z) x 4(x) x 2(y) -> 4096 x 4096 x 2048 pixel-equivalent "
-                            "(device tiler, paper's concatenated copies)"}
     else:
-        apr, values, desc = workload(args.config)
+        apr, values, provenance = workload(args.config)
         dapr = apr.device(ctx)
         v = torch.from_numpy(np.ascontiguousarray(values, np.float32)).cuda()
         n_p, n_t = apr.access.particle_count(), apr.tree_access.particle_count()
@@ -199,21 +213,24 @@ def run_ours(args, rank, world):
         n_pix = apr.pixel_count()
     k = args.stencil
     w = P.gaussian_stencil(1.0, k)
-    pyr = P.make_pyramid(w, l_min, l_max, P.PyramidMode.Restricted)
-    dpyr = pyr.device(ctx)
+    pyrs = {kk: P.make_pyramid(P.gaussian_stencil(1.0, kk), l_min, l_max, P.PyramidMode.Restricted)
+            for kk in sorted({k, 3, 5})}
+    dpyrs = {kk: p.device(ctx) for kk, p in pyrs.items()}
     setup_s = time.time() - t0
-    accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
+    modes = {"exact": L.ACCUM_EXACT, "fast": L.ACCUM_FAST}
+    accum = modes[args.accum]
     tv = torch.empty(max(dapr.n_tree, 1), dtype=torch.float32, device="cuda")
     out = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")
     dapr.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
-    def conv():
-        dapr.convolve_ptr(v.data_ptr(), tv.data_ptr(), dpyr, 1, accum, out.data_ptr(), s)
+    def conv_fn(kk, acc):
+        return lambda: dapr.convolve_ptr(v.data_ptr(), tv.data_ptr(), dpyrs[kk], 1, acc, out.data_ptr(), s)
 
-    def paper_step():
+    def paper_step():  # row index + tree fill + convolution
+        dapr.rebuild_index_ptr(s)
         dapr.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s)
-        conv()
+        dapr.convolve_ptr(v.data_ptr(), tv.data_ptr(), dpyrs[k], 1, accum, out.data_ptr(), s)
 
     def timed(fn, steps):
         times = []
@@ -227,18 +244,52 @@ def run_ours(args, rank, world):
             times.append(e0.elapsed_time(e1) / 1e3)
         return times
 
+    # cold first call: a fresh upload of the host structure + the per-APR lists,
+    # tree links, tile probe/runs and gather maps built by the first fill_tree +
+    # convolve_apr, with the values' H2D copy (host wall clock, synchronised)
+    cold = None
+    if apr is not None:
+        torch.cuda.synchronize()
+        hv = torch.from_numpy(np.ascontiguousarray(values, np.float32)).pin_memory()
+        c0 = time.perf_counter()
+        fresh = P.aprkit.DeviceApr.upload(ctx, P.APR(apr.access, apr.tree_access, apr.source_dims))
+        c1 = time.perf_counter()
+        fv = hv.to("cuda", non_blocking=True)
+        ftv = torch.empty(max(fresh.n_tree, 1), dtype=torch.float32, device="cuda")
+        fout = torch.empty(fresh.n_particles, dtype=torch.float32, device="cuda")
+        fresh.fill_tree_ptr(fv.data_ptr(), ftv.data_ptr(), s)
+        fresh.convolve_ptr(fv.data_ptr(), ftv.data_ptr(), dpyrs[k], 1, accum, fout.data_ptr(), s)
+        stream.synchronize()
+        c2 = time.perf_counter()
+        cold = {"ms": round((c2 - c0) * 1e3, 3), "upload_ms": round((c1 - c0) * 1e3, 3),
+                "first_call_ms": round((c2 - c1) * 1e3, 3),
+                "includes": "aprgpu_upload_access of the host structure (incl. its interior structure, row and tile "
+                            "lists) + values H2D + first fill_tree + first convolve_apr (tree links, tile probe, "
+                            "tile runs, gather maps), host wall clock"}
+        del fresh, fv, ftv, fout
+
+    headline = conv_fn(k, accum)
     for _ in range(args.warmup):
-        conv()
+        headline()
         paper_step()
+    for kk in dpyrs:
+        for acc in modes.values():
+            conv_fn(kk, acc)()  # (builds every variant's maps outside the timed regions)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     l0 = ctx.launch_count()
     with ClockSampler(dev_id) as clk:
-        t_conv = timed(conv, args.steps)
+        t_conv = timed(headline, args.steps)
         launches = ctx.launch_count() - l0
         t_paper = timed(paper_step, args.steps)
+        variants = {}
+        for kk in sorted(dpyrs):
+            for name, acc in modes.items():
+                if kk == k and acc == accum:
+                    continue
+                variants[(kk, name)] = timed(conv_fn(kk, acc), max(3, min(args.steps, 20)))
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -251,7 +302,7 @@ def run_ours(args, rank, world):
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         a = time.perf_counter()
-        L.check(L.lib().aprgpu_convolve(dapr.handle, hv.data_ptr(), htv.data_ptr(), dpyr.handle, 1, accum,
+        L.check(L.lib().aprgpu_convolve(dapr.handle, hv.data_ptr(), htv.data_ptr(), dpyrs[k].handle, 1, accum,
                                         hout.data_ptr(), L.HOST, None))
         b = time.perf_counter()
         if i >= args.warmup:
@@ -260,14 +311,17 @@ def run_ours(args, rank, world):
     # C5: rl_apr, 10 Richardson-Lucy iterations on the same APR (deconv.hpp:75-107:
     # 2 tree refreshes + 2 convolutions per iteration, ratio/multiply fused)
     rl_out = torch.empty_like(out)
-    rl_t = []
-    for i in range(2):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        dapr.rl_ptr(v.data_ptr(), w, args.rl_iters, 0.0, accum, rl_out.data_ptr(), s)
-        e1.record(stream)
-        e1.synchronize()
-        rl_t.append(e0.elapsed_time(e1) / 1e3)
+    rl = {}
+    for name, acc in modes.items():
+        rl_t = []
+        for i in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dapr.rl_ptr(v.data_ptr(), w, args.rl_iters, 0.0, acc, rl_out.data_ptr(), s)
+            e1.record(stream)
+            e1.synchronize()
+            rl_t.append(e0.elapsed_time(e1) / 1e3)
+        rl[name] = {"ms": round(rl_t[-1] * 1e3, 3), "ms_per_iteration": round(rl_t[-1] * 1e3 / max(args.rl_iters, 1), 4)}
 
     # reconstruct_full (reconstruct.hpp:87-90) of the same APR: the dense image,
     # bound by writing it (4 bytes per pixel); skipped when it would not fit easily
@@ -305,7 +359,7 @@ def run_ours(args, rank, world):
             pixels_conv = {"ms": round(tpx * 1e3, 4), "gbs_pixel_equiv": round(4 * n_pix / tpx / 1e9, 1),
                            "hbm_frac": round(8 * n_pix / tpx / 1e9 / peaks()[0], 4),
                            "note": "convolve_pixels of the reconstructed image (k_convolve_pixels), best of 2 "
-                                   "warm runs; includes a stream sync for the weight buffer"}
+                                   "warm runs, same accumulation mode as the headline"}
         del img
 
     def agg(x):
@@ -317,10 +371,24 @@ def run_ours(args, rank, world):
         return t
 
     tc, tp, te = agg(t_conv), agg(t_paper), agg(e2e)
-    B = 10 * n_p + 6 * n_t + 4 * n_rows  # algorithmic_bytes()
+    B = algorithmic_bytes(n_p, n_t, n_rows)
     peak, peak_kind = peaks()
-    achieved = B / tc / 1e9
-    traffic, traffic_src = ncu_traffic(args.config, k, args.accum)
+
+    def roof(t, kk, acc_name):
+        a_ = B / t / 1e9
+        traffic, src = ncu_traffic(args.config, kk, acc_name)
+        return {"bound": "hbm", "achieved": round(a_, 2), "peak": peak, "unit": "GB/s", "frac": round(a_ / peak, 4),
+                "traffic": traffic,
+                "note": f"algorithmic bytes {B} per pass (10/particle + 6/node + 4/row) / conv-pass time (CUDA events "
+                        f"on the launching stream); peak {peak_kind} (MEASURED_PEAKS.json hbm_gbs); traffic = ncu dram "
+                        f"bytes of one cold pass" + (f" ({src})" if src else " (no committed capture)")}
+
+    def line(t, kk, acc_name):
+        return {"ms_per_step": round(t * 1e3, 4), "gbps_pixel_equiv": round(world * 4 * n_pix / t / 1e9, 3),
+                "particles_per_s": round(world * n_p / t, 1), "roofline": roof(t, kk, acc_name)}
+
+    dtype = {"exact": "f32 values, f64 accumulate in the reference's tap order (bit-exact)",
+             "fast": "f32 values, f32 accumulate (rel <= 1e-5)"}
     res = {
         "metric": METRIC,
         "value": round(world * 4 * n_pix / tc / 1e9, 3),
@@ -332,22 +400,17 @@ def run_ours(args, rank, world):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32 values, " + ("f64 accumulate (bit-exact)" if accum == L.ACCUM_EXACT else "f32 accumulate"),
+        "dtype": dtype[args.accum],
         "data": "synthetic",
-        "config": dict(desc, stencil=f"gaussian(1.0,{k}) restricted pyramid", pad="reflect",
-                       particles=n_p, interior_nodes=n_t, pixels=n_pix,
-                       cr=round(n_pix / n_p, 2), l2="flushed between timed steps (256 MB write)",
-                       protocol="conv-only (tree filled outside the timed region, bench.hpp:158-169)",
-                       parallelism="single GPU"),
+        "config": bench_config(args.config, k, n_p, n_t, n_pix),
+        "input": provenance,
+        "parallelism": "single GPU",
         "particles_per_s": round(world * n_p / tc, 1),
         "paper_protocol": {"ms_per_step": round(tp * 1e3, 4), "gbps_pixel_equiv": round(4 * n_pix / tp / 1e9, 3),
-                           "includes": "fill_tree + convolve_apr (row index prebuilt at upload)"},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "note": f"algorithmic bytes {B} per pass (10/particle + 6/node + 4/row) / conv-pass time "
-                             f"(CUDA events on the launching stream); peak {peak_kind} (MEASURED_PEAKS.json hbm_gbs); "
-                             f"traffic = ncu dram bytes of one cold conv pass"
-                             + (f" ({traffic_src})" if traffic_src else " (no committed capture)")},
+                           "includes": "per step, stream-ordered: nonempty_row_index + tile lists rebuilt on the "
+                                       "device (aprgpu_rebuild_index) + fill_tree + convolve_apr (PAPER.md:379), "
+                                       "L2 flushed before each step"},
+        "roofline": roof(tc, k, args.accum),
         "e2e": {"value": round(world * 4 * n_pix / te / 1e9, 3), "unit": "GB/s (pixel-equivalent)",
                 "ms_per_step": round(te * 1e3, 4),
                 "h2d_bytes_per_step": int(4 * n_p + 4 * dapr.n_tree), "d2h_bytes_per_step": int(4 * n_p),
@@ -356,18 +419,19 @@ def run_ours(args, rank, world):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 2),
-        "rl_apr": {"iterations": args.rl_iters, "ms": round(rl_t[-1] * 1e3, 3),
-                   "ms_per_iteration": round(rl_t[-1] * 1e3 / max(args.rl_iters, 1), 4),
-                   "psf": f"gaussian(1.0,{k}), restricted pyramids of w and flip(w)",
-                   "note": "C5; second of two runs, includes the pyramid setup and one D2H for the mean"},
+        "variants": {f"k{kk}_{name}": line(agg(tt), kk, name) for (kk, name), tt in variants.items()},
+        "rl_apr": dict(rl, iterations=args.rl_iters, psf=f"gaussian(1.0,{k}), restricted pyramids of w and flip(w)",
+                       note="C5; second of two runs, includes the pyramid setup and the exact mean"),
     }
+    if cold:
+        res["cold_call"] = cold
     if recon:
         res["reconstruct_full"] = recon
     if pixels_conv:
         pixels_conv["apr_speedup"] = round(pixels_conv["ms"] / (tc * 1e3), 2)
         res["convolve_pixels"] = pixels_conv
     if rank == 0 and not args.no_cpu_baseline and apr is not None:
-        res["cpu_baseline"] = cpu_baseline(apr, values, tv[:dapr.n_tree].cpu().numpy(), pyr, args)
+        res["cpu_baseline"] = cpu_baseline(apr, values, tv[:dapr.n_tree].cpu().numpy(), pyrs[k], args)
     return res
 
 
@@ -411,7 +475,8 @@ def run_slab(args, rank, world):
                             "(device tiler): one C3-sized z-slab per GPU (weak scaling)"}
         scaling = "weak"
     else:
-        apr, values, desc = workload(args.config)
+        apr, values, _ = workload(args.config)
+        desc = {"workload": WORKLOADS[args.config]}
         dapr = apr.device(ctx)
         scaling = "strong"
     k = args.stencil
@@ -492,7 +557,8 @@ def run_slab(args, rank, world):
 
     tc, tp, te = agg(t_conv), agg(t_paper), agg(e2e)
     n_pix, n_p = apr.pixel_count(), apr.access.particle_count()
-    B = algorithmic_bytes(apr)
+    B = algorithmic_bytes(apr.access.particle_count(), apr.tree_access.particle_count(),
+                          apr.access.row_count() + apr.tree_access.row_count())
     peak, peak_kind = peaks()
     achieved = B / world / tc / 1e9  # per GPU: each owns ~1/N of the bytes
     return {
@@ -527,72 +593,72 @@ def run_slab(args, rank, world):
 
 
 # -------------------------------------------------------------- CPU baseline --
-def _ref_objects(apr, pyr):
-    from pyoracle import Ref
+def cpu_baseline(apr, values, tree_values, pyr, args):
+    """The reference's own convolve_apr (oracle/_ref) timed with its time_median
+    protocol (bench.hpp:106-117) on the full workload: all host threads, plus
+    one single-thread run."""
+    from pyoracle import Ref, ref_available
+    n_pix = apr.pixel_count()
+    if not ref_available():
+        return {"value": None, "unit": "GB/s (pixel-equivalent)", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built on this box"}
     R = Ref()
     rapr = R.apr_from_arrays(apr.access, apr.source_dims)
-    levels = [((s.kz, s.kx, s.ky), s.weights) for s in pyr.stencils]
-    rpyr = R.explicit_pyramid(levels, pyr.l_min)
-    return R, rapr, rpyr
-
-
-def cpu_baseline(apr, values, tree_values, pyr, args):
-    """The reference's own convolve_apr (oracle/_ref, all host threads) timed
-    with its time_median protocol (bench.hpp:106-117) on the full workload."""
-    from pyoracle import ref_available
-    n_pix = apr.pixel_count()
-    if ref_available():
-        R, rapr, rpyr = _ref_objects(apr, pyr)
-        threads = R.resolve_threads(0)
-        R.convolve(rapr, values, tree_values, rpyr, 1, threads)  # cold run discarded
-        times = []
-        budget = time.time() + args.cpu_seconds
-        while len(times) < 3 or (time.time() < budget and len(times) < 15):
-            a = time.perf_counter()
-            R.convolve(rapr, values, tree_values, rpyr, 1, threads)
-            times.append(time.perf_counter() - a)
-        t = statistics.median(times)
-        return {"value": round(4 * n_pix / t / 1e9, 4), "unit": "GB/s (pixel-equivalent)", "cores": threads,
-                "kind": "reference", "ms_per_step": round(t * 1e3, 2),
-                "particles_per_s": round(apr.access.particle_count() / t, 1),
-                "sample": f"full workload convolve_apr, median of {len(times)} after a discarded cold run"}
-    from pyoracle import Oracle
-    O = Oracle()
-    levels = [((s.kz, s.kx, s.ky), s.weights) for s in pyr.stencils]
+    rpyr = R.explicit_pyramid([((s.kz, s.kx, s.ky), s.weights) for s in pyr.stencils], pyr.l_min)
+    threads = R.resolve_threads(0)
+    R.convolve(rapr, values, tree_values, rpyr, 1, threads)  # cold run discarded
+    times = []
+    budget = time.time() + args.cpu_seconds
+    while len(times) < 3 or (time.time() < budget and len(times) < 15):
+        a = time.perf_counter()
+        R.convolve(rapr, values, tree_values, rpyr, 1, threads)
+        times.append(time.perf_counter() - a)
+    t = statistics.median(times)
     a = time.perf_counter()
-    O.convolve(apr.access, apr.tree_access, values, tree_values, levels, apr.access.l_min, 1)
-    t = time.perf_counter() - a
-    return {"value": round(4 * n_pix / t / 1e9, 4), "unit": "GB/s (pixel-equivalent)", "cores": 1, "kind": "port",
-            "ms_per_step": round(t * 1e3, 2), "sample": "full workload, one pass of the C oracle"}
+    R.convolve(rapr, values, tree_values, rpyr, 1, 1)
+    t1 = time.perf_counter() - a
+    return {"value": round(4 * n_pix / t / 1e9, 4), "unit": "GB/s (pixel-equivalent)", "cores": threads,
+            "kind": "reference", "ms_per_step": round(t * 1e3, 2),
+            "particles_per_s": round(apr.access.particle_count() / t, 1),
+            "single_thread": {"value": round(4 * n_pix / t1 / 1e9, 4), "ms_per_step": round(t1 * 1e3, 1),
+                              "cores": 1},
+            "sample": f"full workload convolve_apr (explicit pyramid of the same restricted levels), median of "
+                      f"{len(times)} after a discarded cold run; single_thread: one run with threads = 1"}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference CPU convolve_apr on the same workload."""
+    """--impl reference: the unmodified reference (oracle/_ref, compiled from
+    /root/reference's own headers) on the same workload.  Its input is made by
+    the C restatement of generate_spheres + build_apr (oracle/build_oracle.c,
+    bit-identical to the reference build; multi-threaded so it takes seconds,
+    not the reference's 3 minutes / 34 GB) -- this process never loads the
+    product library.  Then everything is the reference's own code:
+    init_tree_structure, fill_tree, gaussian_stencil, make_pyramid, and the
+    timed convolve_apr (all host threads)."""
     from pyoracle import Oracle, Ref, ref_available
-    apr, values, desc = workload(args.config)  # input generation only
-    n_pix = apr.pixel_count()
+    if args.config not in SPHERES:
+        return {"impl": "reference", "unavailable": f"no host-side input for config {args.config} "
+                                                    "(C4 is 548 M particles; the reference arm runs C1/C3)"}
+    O = Oracle()
+    n, count, rmin, rmax = SPHERES[args.config]
+    t0 = time.time()
+    leaf, values = O.build_spheres(n, count, rmin, rmax, blur=2.0, seed=42, rel_error=0.1)
+    t_build = time.time() - t0
+    n_pix = n ** 3
     k = args.stencil
-    if ref_available():
-        # everything below is the unmodified reference: tree, gaussian, make_pyramid, convolve_apr
-        R = Ref()
-        rapr = R.apr_from_arrays(apr.access, apr.source_dims)
-        k3, w = R.gaussian_stencil(1.0, k)
-        rpyr = R.make_pyramid(w, k3, apr.access.l_min, apr.access.l_max, 0)
-        threads = R.resolve_threads(0)
-        tv = R.fill_tree(rapr, values, threads)
-        kind = "reference"
-        fn = lambda: R.convolve(rapr, values, tv, rpyr, 1, threads)  # noqa: E731
-    else:
-        O = Oracle()
-        g = O  # the C restatement of the reference (single-threaded)
-        import paper_2112_03592_b200 as P
-        w = P.gaussian_stencil(1.0, k).weights
-        levels = O.restricted_levels(w, (k, k, k), apr.access.l_min, apr.access.l_max)
-        tree = apr.tree_access if apr.tree_access is not None else O.init_tree_structure(apr.access, apr.source_dims)
-        tv = g.fill_tree(apr.access, tree, apr.source_dims, values)
-        threads, kind = 1, "port"
-        fn = lambda: O.convolve(apr.access, tree, values, tv, levels, apr.access.l_min, 1)  # noqa: E731
-    fn()
+    if not ref_available():
+        return {"impl": "reference", "unavailable": "oracle/_ref (the compiled reference) is not on this box"}
+    R = Ref()
+    rapr = R.apr_from_arrays(leaf, (n, n, n))   # the reference's init_tree_structure
+    k3, w = R.gaussian_stencil(1.0, k)
+    t0 = time.time()
+    rpyr = R.make_pyramid(w, k3, leaf.l_min, leaf.l_max, 0)   # PyramidMode::Restricted
+    t_pyr = time.time() - t0
+    threads = R.resolve_threads(0)
+    tv = R.fill_tree(rapr, values, threads)
+    n_p, n_t = leaf.particle_count(), int(tv.size)
+    fn = lambda: R.convolve(rapr, values, tv, rpyr, 1, threads)  # noqa: E731
+    fn()  # cold run discarded
     for _ in range(args.warmup):
         fn()
     times = []
@@ -605,10 +671,13 @@ def run_reference(args, rank, world):
     return {"metric": METRIC, "value": v, "unit": "GB/s (pixel-equivalent)", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 values, f64 accumulate", "data": "synthetic", "impl": "reference",
-            "config": dict(desc, stencil=f"gaussian(1.0,{args.stencil}) restricted pyramid", pad="reflect"),
-            "particles_per_s": round(apr.access.particle_count() / t, 1),
-            "cpu_baseline": {"value": v, "unit": "GB/s (pixel-equivalent)", "cores": threads, "kind": kind,
-                             "sample": "full workload convolve_apr per step"},
+            "config": bench_config(args.config, k, n_p, n_t, n_pix),
+            "input": "oracle/build_oracle.c (C restatement of generate_spheres + build_apr, bit-identical to the "
+                     f"reference build; {t_build:.1f} s), make_pyramid {t_pyr:.1f} s",
+            "parallelism": f"{threads} host threads",
+            "particles_per_s": round(n_p / t, 1),
+            "cpu_baseline": {"value": v, "unit": "GB/s (pixel-equivalent)", "cores": threads, "kind": "reference",
+                             "sample": "full workload convolve_apr per step (unmodified reference, oracle/_ref)"},
             "e2e": {"value": v, "unit": "GB/s (pixel-equivalent)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -619,7 +688,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=os.environ.get("APR_BENCH_CONFIG", "c3"), choices=["c1", "c3", "c4"])
     ap.add_argument("--stencil", type=int, default=3)
-    ap.add_argument("--accum", default="fast", choices=["exact", "fast"])
+    ap.add_argument("--accum", default="exact", choices=["exact", "fast"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

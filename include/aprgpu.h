@@ -111,6 +111,14 @@ int aprgpu_download_access(const aprgpu_apr* apr, int which, uint16_t* y_idx, ui
 int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, uint16_t* y_min,
                      uint16_t* y_max, uint64_t cap, uint64_t* count);
 
+/* The per-call index step of the paper's GPU protocol ("row
+ * index + tree fill + convolution"): nonempty_row_index (convolve.hpp:32-44)
+ * for every level plus the occupied-tile lists derived from it, recomputed on
+ * the device into APR scratch, stream-ordered (no host synchronisation).  The
+ * convolution keeps using the identical lists built at upload; this entry
+ * point exists so a protocol that counts the index step can time it. */
+int aprgpu_rebuild_index(aprgpu_apr* apr, void* stream);
+
 /* ---- tree ----------------------------------------------------------------- */
 /* fill_tree (tree.hpp:110-150): leaf[n_particles] -> tree[n_tree]; fp64
  * accumulation in the reference's per-parent order, bit-exact. */

@@ -61,6 +61,7 @@ _SIGS = {
     "aprgpu_row_index": [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                          C.POINTER(C.c_uint64)],
     "aprgpu_fill_tree": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p],
+    "aprgpu_rebuild_index": [C.c_void_p, C.c_void_p],
     "aprgpu_restrict_stencil": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p],
     "aprgpu_gaussian_stencil": [C.c_double, C.c_int, C.c_void_p, C.c_void_p],
     "aprgpu_box_stencil": [C.c_int, C.c_void_p],

@@ -559,6 +559,10 @@ class DeviceApr:
     def fill_tree_ptr(self, leaf_ptr: int, tree_ptr: int, stream: int = 0) -> None:
         L.check(L.lib().aprgpu_fill_tree(self.handle, leaf_ptr, tree_ptr, L.DEVICE, stream or None))
 
+    def rebuild_index_ptr(self, stream: int = 0) -> None:
+        """The paper protocol's per-call index step (aprgpu_rebuild_index)."""
+        L.check(L.lib().aprgpu_rebuild_index(self.handle, stream or None))
+
     def convolve_ptr(self, values_ptr: int, tree_ptr: int, pyr: DevicePyramid, pad: int, accum: int, out_ptr: int,
                      stream: int = 0) -> None:
         L.check(L.lib().aprgpu_convolve(self.handle, values_ptr, tree_ptr, pyr.handle, int(pad), accum, out_ptr,

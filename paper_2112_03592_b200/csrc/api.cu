@@ -707,6 +707,16 @@ int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, u
     });
 }
 
+int aprgpu_rebuild_index(aprgpu_apr* apr, void* stream) {
+    return guard([&] {
+        need(apr, "null argument");
+        DeviceGuard g(apr->ctx->device);
+        cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
+        ScratchGuard sg(apr, s);
+        aprgpu::rebuild_index_device(apr, s);
+    });
+}
+
 int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream) {
     return guard([&] {
         need(apr && leaf && (tree || apr->tree.n_particles == 0), "null argument");

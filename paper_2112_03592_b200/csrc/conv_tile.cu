@@ -1498,6 +1498,91 @@ void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a) {
                                 cudaMemcpyHostToDevice));
 }
 
+namespace {
+
+struct RowNonEmpty {
+    const uint32_t* rb;
+    __host__ __device__ bool operator()(uint32_t r) const { return rb[r + 1] > rb[r]; }
+};
+
+struct LevelTiles {
+    LevelG g[kMaxLevels];
+    int txd[kMaxLevels], tyd[kMaxLevels];
+    uint64_t fbase[kMaxLevels];  // first flag of each level in the combined flag space
+    int l_min, l_max;
+};
+
+// every non-empty row of every level marks the (8z, 8x, 32y) tiles its particles fall in
+__global__ void k_mark_tiles_all(const uint32_t* __restrict__ work, const uint64_t* __restrict__ n_work_p,
+                                 const __grid_constant__ LevelTiles lt, const uint32_t* __restrict__ rb,
+                                 const uint16_t* __restrict__ y, uint8_t* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t n_work = *n_work_p;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = warp; w < n_work; w += nw) {
+        const uint32_t row = work[w];
+        int l = lt.l_max;
+        while (l > lt.l_min && row < lt.g[l].row0) --l;
+        const uint32_t loc = row - lt.g[l].row0;
+        const int z = static_cast<int>(loc / lt.g[l].xd), x = static_cast<int>(loc % lt.g[l].xd);
+        const uint64_t base = lt.fbase[l] + (static_cast<uint64_t>(z / kTZ) * lt.txd[l] + x / kTX) * lt.tyd[l];
+        const uint32_t b = rb[row], e = rb[row + 1];
+        for (uint32_t i = b + lane; i < e; i += 32) flags[base + y[i] / kTY] = 1;
+    }
+}
+
+}  // namespace
+
+// The per-call index step of the paper's GPU protocol ("row
+// index + tree fill + convolution"): nonempty_row_index (convolve.hpp:32-44)
+// over every level and the occupied-tile lists derived from it, recomputed on
+// the device into APR-owned scratch, stream-ordered with no host round trip.
+// (The convolution's own lists, built at upload, are identical; this step
+// exists so the protocol's timing includes the work.)  Returns nothing; the
+// counts land in scratch.
+void rebuild_index_device(aprgpu_apr* apr, cudaStream_t s) {
+    DevAccess& L = apr->leaf;
+    if (L.n_rows == 0) return;
+    LevelTiles lt{};
+    lt.l_min = L.l_min;
+    lt.l_max = L.l_max;
+    uint64_t nflags = 0;
+    for (int l = L.l_min; l <= L.l_max; ++l) {
+        lt.g[l] = LevelG{L.zd[l], L.xd[l], L.yd[l], static_cast<uint32_t>(L.level_offset[l])};
+        lt.txd[l] = L.tile_dims[3 * l + 1];
+        lt.tyd[l] = L.tile_dims[3 * l + 2];
+        lt.fbase[l] = nflags;
+        nflags += static_cast<uint64_t>(L.tile_dims[3 * l]) * lt.txd[l] * lt.tyd[l];
+    }
+    thrust::counting_iterator<uint32_t> it(0);
+    // scratch: [work list n_rows u32][2 counts u64][flags nflags][tile list nflags u32][cub temp]
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceSelect::If(nullptr, t1, it, static_cast<uint32_t*>(nullptr), static_cast<uint64_t*>(nullptr),
+                          static_cast<int64_t>(L.n_rows), RowNonEmpty{L.rb}, s);
+    cub::DeviceSelect::Flagged(nullptr, t2, it, static_cast<uint8_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                               static_cast<uint64_t*>(nullptr), static_cast<int64_t>(nflags), s);
+    const size_t o_cnt = (4 * L.n_rows + 15) & ~size_t(15);
+    const size_t o_flags = o_cnt + 16;
+    const size_t o_tiles = (o_flags + nflags + 15) & ~size_t(15);
+    const size_t o_temp = (o_tiles + 4 * nflags + 255) & ~size_t(255);
+    apr->index_scratch.ensure(o_temp + std::max(t1, t2) + 256);
+    char* base = apr->index_scratch.as<char>();
+    uint32_t* work = reinterpret_cast<uint32_t*>(base);
+    uint64_t* cnt = reinterpret_cast<uint64_t*>(base + o_cnt);
+    uint8_t* flags = reinterpret_cast<uint8_t*>(base + o_flags);
+    uint32_t* tiles = reinterpret_cast<uint32_t*>(base + o_tiles);
+    void* temp = base + o_temp;
+    size_t tb = std::max(t1, t2);
+    APR_CUDA(cub::DeviceSelect::If(temp, tb, it, work, cnt, static_cast<int64_t>(L.n_rows), RowNonEmpty{L.rb}, s));
+    APR_CUDA(cudaMemsetAsync(flags, 0, nflags, s));
+    k_mark_tiles_all<<<apr->ctx->sm_count * 16, 256, 0, s>>>(work, cnt, lt, L.rb, L.y, flags);
+    tb = std::max(t1, t2);
+    APR_CUDA(cub::DeviceSelect::Flagged(temp, tb, it, flags, tiles, cnt + 1, static_cast<int64_t>(nflags), s));
+    count_launch(apr->ctx, 3);
+    APR_CUDA(cudaGetLastError());
+}
+
 // Runs every level whose stencil is an isotropic 3^3 or 5^3 through the tile
 // kernel (one launch per extent and run of consecutive levels, coarse levels
 // first); sets done[l] for them.

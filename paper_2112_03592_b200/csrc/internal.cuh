@@ -126,6 +126,7 @@ struct aprgpu_apr {
     aprgpu::GpuBuf rl_u, rl_ratio, rl_tv;  // RL state
     aprgpu::GpuBuf tmp;                    // misc
     aprgpu::GpuBuf built_values;           // leaf values sampled by aprgpu_build_apr / read by aprgpu_load_apr
+    aprgpu::GpuBuf index_scratch;          // aprgpu_rebuild_index (the paper protocol's per-call index step)
     // z-chunk plan of host-pointer convolutions (api.cu, HostPipe): chunk of S
     // finest planes; levels >= lc split per chunk, [l - lc][j] = first particle
     // of chunk j's rows at level l (j = 0..K)
@@ -161,6 +162,8 @@ void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a);
 void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* values, const float* tree_values,
                       int pad, int accum, float* out, const struct EpiArgs& epi, const struct Slab& slab,
                       cudaStream_t s, bool* done);
+
+void rebuild_index_device(aprgpu_apr* apr, cudaStream_t s);
 
 // reconstruct.cu
 void reconstruct_level_device(aprgpu_apr* apr, const float* values, const float* tree_values, int l, float* out,
