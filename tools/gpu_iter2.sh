@@ -1,0 +1,14 @@
+# quick iteration on the hot kernel: parity subset + the bench's conv lines
+mkdir -p gpurun_out
+O=gpurun_out
+timeout 600 python -m pytest tests/test_parity_gpu.py tests/test_fullsize_gpu.py tests/test_concurrency_gpu.py tests/test_pipeline_gpu.py -q -x -rf 2>&1 | tail -5 > $O/iter_tests.log
+timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > $O/iter_bench.json 2> $O/iter_bench.err
+python - <<'PY' >> $O/iter_tests.log
+import json
+d = json.load(open("gpurun_out/iter_bench.json"))
+print("k3_exact", d["ms_per_step"], d["roofline"]["frac"])
+for k, v in d["variants"].items():
+    print(k, v["ms_per_step"], v["roofline"]["frac"])
+print("paper", d["paper_protocol"]["ms_per_step"], "cold", d.get("cold_call", {}).get("ms"), "rl", d["rl_apr"])
+PY
+cat $O/iter_tests.log
