@@ -242,6 +242,27 @@ int aprgpu_fill_tree_finalize(aprgpu_apr* apr, float* tree, void* stream);
 int aprgpu_convolve_slab(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
                          int pad_mode, int accum, int lc, int z_lo, int z_hi, float* out, void* stream);
 
+/* ---- multi-GPU z-slabs in one process (csrc/multi.cu) -------
+ * The volume cut into n_slabs z-slabs, slab s on device devices[s] (entries
+ * may repeat: several slabs on one GPU); every device holds the structure,
+ * levels >= the cut level are partitioned, coarser ones replicated, and the
+ * halo -- `halo` rows of every partitioned level, at least the stencils'
+ * half-width -- is copied peer to peer (NVLink / NVSwitch) while each slab's
+ * interior already convolves.  tree may be NULL (built on the devices).
+ * convolve_apr (convolve.hpp:220-303) over the slabs: HOST values[n_particles]
+ * and tree_values[n_tree] in, out[n_particles] out; the pyramid is explicit
+ * (w: level-by-level weights, k3: 3 extents per level, levels l_min..l_max).
+ * Bit-identical to aprgpu_convolve in EXACT mode.  RANGE: the volume is too
+ * thin for the slab count, or a stencil half-width exceeds the halo. */
+typedef struct aprgpu_multi aprgpu_multi;
+int aprgpu_multi_create(const int* devices, int n_slabs, const aprgpu_access_desc* leaf,
+                        const aprgpu_access_desc* tree, const int32_t source_dims[3], int halo, aprgpu_multi** out);
+int aprgpu_multi_free(aprgpu_multi* m);
+/* n_slabs, the cut level and each slab's finest-level planes [z_bounds[2s], z_bounds[2s+1]) */
+int aprgpu_multi_info(const aprgpu_multi* m, int* n_slabs, int* cut_level, int32_t* z_bounds);
+int aprgpu_multi_convolve(aprgpu_multi* m, const float* values, const float* tree_values, const float* w,
+                          const int32_t* k3, int l_min, int l_max, int pad_mode, int accum, float* out);
+
 /* rl_apr resumed from a running estimate (estimate_in[n_particles]; NULL =
  * start from the clamped observation, i.e. aprgpu_rl).  The reference's state
  * between iterations is exactly (u, epsilon, estimate), so running k iterations

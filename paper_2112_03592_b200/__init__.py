@@ -5,7 +5,7 @@ C-ABI in ``include/aprgpu.h``); this package is the thin host mirror of the
 reference's API (``aprkit``) used by tests, the benchmark and Python callers.
 """
 from .aprkit import *  # noqa: F401,F403
-from .aprkit import (APR, ConvolveOptions, Context, DeviceApr, DevicePyramid, LinearAccess, PadMode,  # noqa: F401
+from .aprkit import (APR, ConvolveOptions, Context, DeviceApr, DevicePyramid, LinearAccess, MultiApr, PadMode,  # noqa: F401,E501
                      PyramidMode, RLConfig, RowSpan, Stencil, StencilPyramid, box_stencil, cell_size,
                      compute_l_max, compute_l_min, computational_ratio, convolve_apr, default_context,
                      explicit_pyramid, fill_tree, flip_stencil, gaussian_stencil, grid_dim, identity_stencil,

@@ -81,6 +81,12 @@ _SIGS = {
     "aprgpu_fill_tree_sums": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p],
     "aprgpu_tree_scratch": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
     "aprgpu_fill_tree_finalize": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "aprgpu_multi_create": [C.c_void_p, C.c_int, C.POINTER(AccessDesc), C.POINTER(AccessDesc), C.c_void_p, C.c_int,
+                            C.POINTER(C.c_void_p)],
+    "aprgpu_multi_free": [C.c_void_p],
+    "aprgpu_multi_info": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+    "aprgpu_multi_convolve": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                              C.c_int, C.c_void_p],
     "aprgpu_convolve_slab": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_void_p, C.c_void_p],
     "aprgpu_tile_apr": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)],

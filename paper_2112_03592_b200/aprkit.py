@@ -579,6 +579,47 @@ class DeviceApr:
                                   int(iterations), float(epsilon), accum, out_ptr, L.DEVICE, stream or None))
 
 
+class MultiApr:
+    """An APR cut into z-slabs over several devices in ONE process
+    (aprgpu_multi_*: peer-to-peer halos, interior/boundary overlap; the C++
+    drop-in's multi-GPU path).  devices may repeat (several slabs on one GPU)."""
+
+    def __init__(self, apr: APR, devices: List[int], halo: int = 2):
+        dims = np.array(apr.source_dims, dtype=np.int32)
+        ld = apr.access.desc()
+        td = apr.tree_access.desc() if apr.tree_access is not None else None
+        devs = np.array(devices, dtype=np.int32)
+        h = C.c_void_p()
+        L.check(L.lib().aprgpu_multi_create(_ptr(devs), len(devices), C.byref(ld),
+                                            C.byref(td) if td is not None else None, _ptr(dims), int(halo),
+                                            C.byref(h)))
+        self.handle = h
+        self.n_particles = apr.access.particle_count()
+        n, lc = C.c_int(), C.c_int()
+        zb = np.zeros(2 * len(devices), np.int32)
+        L.check(L.lib().aprgpu_multi_info(h, C.byref(n), C.byref(lc), _ptr(zb)))
+        self.cut_level = lc.value
+        self.bounds = [(int(zb[2 * i]), int(zb[2 * i + 1])) for i in range(n.value)]
+
+    def convolve(self, values, tree_values, pyr: StencilPyramid, pad: PadMode = PadMode.Reflect,
+                 accum: str = "exact") -> np.ndarray:
+        v = np.ascontiguousarray(values, np.float32)
+        tv = np.ascontiguousarray(tree_values, np.float32)
+        k3 = np.array([[st.kz, st.kx, st.ky] for st in pyr.stencils], dtype=np.int32).reshape(-1)
+        w = np.concatenate([st.weights for st in pyr.stencils]).astype(np.float32)
+        out = np.empty(self.n_particles, np.float32)
+        L.check(L.lib().aprgpu_multi_convolve(self.handle, _ptr(v), _ptr(tv) if tv.size else None, _ptr(w), _ptr(k3),
+                                              pyr.l_min, pyr.l_max, int(pad), _accum(accum), _ptr(out)))
+        return out
+
+    def __del__(self):
+        try:
+            if self.handle:
+                L.lib().aprgpu_multi_free(self.handle)
+        except Exception:
+            pass
+
+
 # ----------------------------------------------------- reference front door --
 def init_tree_structure(apr_access: LinearAccess, source_dims, ctx: Optional[Context] = None) -> LinearAccess:
     """tree.hpp:26-82 -- built on the GPU, bit-identical."""

@@ -11,43 +11,20 @@
 
 #include "common.cuh"
 
+namespace aprgpu {
+std::string& last_error_slot() {
+    static thread_local std::string msg;
+    return msg;
+}
+}  // namespace aprgpu
+
 namespace {
 
-thread_local std::string g_last_error;
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return APRGPU_OK;
-    } catch (const aprgpu::Error& e) {
-        g_last_error = e.what();
-        return e.status;
-    } catch (const std::bad_alloc& e) {
-        g_last_error = e.what();
-        return APRGPU_ERR_OOM;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return APRGPU_ERR_INVALID;
-    }
-}
-
+using aprgpu::DeviceGuard;
 using aprgpu::fail;
-
-void need(bool cond, const char* what) {
-    if (!cond) fail(APRGPU_ERR_INVALID, what);
-}
-
-struct DeviceGuard {  // make the context's device current for the call
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
+using aprgpu::guard;
+using aprgpu::need;
+#define g_last_error (aprgpu::last_error_slot())
 
 int host_compute_l_max(int nz, int nx, int ny) {
     const int m = std::max(nz, std::max(nx, ny));

@@ -318,7 +318,7 @@ void convolve_device(aprgpu_apr* apr, const float* values, const float* tree_val
     bool done[kMaxLevels] = {};
     if (use_tiles()) conv_tile_levels(apr, pyr, values, tree_values, pad, accum, out, epi, slab, s, done);
     for (int l = L.l_max; l >= L.l_min; --l) {
-        if (done[l]) continue;
+        if (done[l] || (l < slab.lc && !slab.rep)) continue;
         a.n_work = L.work_off[l + 1] - L.work_off[l];
         if (a.n_work == 0) continue;
         a.work = L.work + L.work_off[l];

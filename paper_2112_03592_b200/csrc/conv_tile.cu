@@ -1626,12 +1626,14 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
             b.meta = L.tile_meta;
             b.runs = L.tile_runs[H - 1];
             b.run_off = L.tile_run_off[H - 1];
-            const int first = l;
+            int first = -1;  // the launch's first level with tiles (its tiles start the launch)
             uint32_t total = 0;
             for (; l <= L.l_max && ok(l); ++l) {
                 done[l] = true;
+                if (l < slab.lc && !slab.rep) continue;  // (a replicated level another pass computes)
                 const uint32_t c = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
                 if (!c) continue;
+                if (first < 0) first = l;
                 total += c;
                 b.woff[b.n_levels] = pyr->off[l - pyr->l_min];
                 set_level(b, L, l, total);

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdint>
 #include <mutex>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -33,6 +34,42 @@ struct Error : std::runtime_error {
             ::aprgpu::fail(APRGPU_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__));  \
         }                                                                                          \
     } while (0)
+
+// ---- C-ABI plumbing (api.cu, multi.cu) --------------------------------------
+std::string& last_error_slot();  // thread-local message of the last failed call
+
+// Runs f, converting exceptions into the C-ABI status (and the thread's message).
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return APRGPU_OK;
+    } catch (const Error& e) {
+        last_error_slot() = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        last_error_slot() = e.what();
+        return APRGPU_ERR_OOM;
+    } catch (const std::exception& e) {
+        last_error_slot() = e.what();
+        return APRGPU_ERR_INVALID;
+    }
+}
+
+inline void need(bool cond, const char* what) {
+    if (!cond) fail(APRGPU_ERR_INVALID, what);
+}
+
+struct DeviceGuard {  // make a device current for the call, restore on exit
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 // ---- device-resident access structure ---------------------------------------
 // Per level: grid dims and the index of the level's first row.  Row r of the
@@ -202,6 +239,7 @@ void validate_cover_device(aprgpu_ctx* ctx, const DevAccess& L, const int dims[3
 // levels are computed whole.  lc > l_max: no restriction.
 struct Slab {
     int lc = 1 << 20, z_lo = 0, z_hi = 1 << 30;
+    bool rep = true;  // compute the replicated levels < lc too (multi.cu's boundary passes skip them)
 };
 
 // conv.cu
