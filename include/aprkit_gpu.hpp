@@ -12,11 +12,15 @@
 // directory gets the GPU path with no source change.
 //
 // Runtime model: one aprgpu context per process on device $APRGPU_DEVICE
-// (default 0).  APRs are uploaded on first use and cached by a content
-// fingerprint (structure arrays + dims), so repeated fill_tree/convolve_apr
-// calls on the same APR reuse the device structure, tile lists and work lists.
-// Accumulation: EXACT (fp64 in the reference's order, bit-identical) unless
-// $APRGPU_ACCUM=fast.
+// (default 0).  APRs are uploaded on first use and cached: a call first looks
+// the APR up by the addresses and sizes of its arrays plus a sampled content
+// check (O(1) per call -- aprkit's structures are immutable once built, SPEC
+// §3), and only on a miss by a full content fingerprint, whose hit is then
+// verified against the device copy before it is trusted.  Stencil pyramids
+// are cached on the device by content.  With $APRGPU_DEVICES = "0,1,..." (more
+// than one entry) convolve_apr runs on z-slabs over those devices
+// (aprgpu_multi_*, peer-to-peer halos).  Accumulation: EXACT (fp64 in the
+// reference's order, bit-identical) unless $APRGPU_ACCUM=fast.
 #pragma once
 
 #include <array>
@@ -142,19 +146,80 @@ public:
     // by another thread frees it only after the last holder is done.
     using Ref = std::shared_ptr<aprgpu_apr>;
     Ref upload(const APR& apr) {
+        const bool tree = well_formed(apr.tree_access);
+        const AddrKey ak = addr_key(apr.access, tree ? &apr.tree_access : nullptr, apr.source_dims);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (auto it = cache_.begin(); it != cache_.end(); ++it)
+                if (it->addr == ak) {
+                    cache_.splice(cache_.begin(), cache_, it);
+                    return cache_.front().ref;
+                }
+        }
         Fingerprint f;
         f.access(apr.access);
-        const bool tree = well_formed(apr.tree_access);
         if (tree) f.access(apr.tree_access);
         f.bytes(apr.source_dims.data(), sizeof(int) * 3);
-        return lookup(f.value(), [&](aprgpu_apr** out) {
-            if (!well_formed(apr.access)) throw RangeError("APR access structure has no levels");
-            const aprgpu_access_desc leaf = describe(apr.access);
-            aprgpu_access_desc td{};
-            if (tree) td = describe(apr.tree_access);
-            const int32_t dims[3] = {apr.source_dims[0], apr.source_dims[1], apr.source_dims[2]};
-            return aprgpu_upload_access(ctx_, &leaf, tree ? &td : nullptr, dims, out);
-        });
+        return lookup(f.value(), ak, [&](aprgpu_apr* h) { return same_structure(h, apr.access); },
+                      [&](aprgpu_apr** out) {
+                          if (!well_formed(apr.access)) throw RangeError("APR access structure has no levels");
+                          const aprgpu_access_desc leaf = describe(apr.access);
+                          aprgpu_access_desc td{};
+                          if (tree) td = describe(apr.tree_access);
+                          const int32_t dims[3] = {apr.source_dims[0], apr.source_dims[1], apr.source_dims[2]};
+                          return aprgpu_upload_access(ctx_, &leaf, tree ? &td : nullptr, dims, out);
+                      });
+    }
+
+    // A StencilPyramid on the device, cached by content.
+    using PyrRef = std::shared_ptr<aprgpu_pyramid>;
+    PyrRef pyramid(const StencilPyramid& p) {
+        if (p.stencils.empty()) throw RangeError("StencilPyramid has no levels");
+        std::vector<float> w;
+        std::vector<int32_t> k3;
+        for (const Stencil& st : p.stencils) {
+            w.insert(w.end(), st.weights.begin(), st.weights.end());
+            k3.insert(k3.end(), {st.kz, st.kx, st.ky});
+        }
+        Fingerprint f;
+        f.vec(w);
+        f.vec(k3);
+        const std::uint64_t key = f.value() ^ (static_cast<std::uint64_t>(p.l_min) << 40) ^ p.l_max;
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto it = pyr_cache_.begin(); it != pyr_cache_.end(); ++it)
+            if (it->key == key && it->l_min == p.l_min && it->w == w && it->k3 == k3) {
+                pyr_cache_.splice(pyr_cache_.begin(), pyr_cache_, it);
+                return pyr_cache_.front().ref;
+            }
+        aprgpu_pyramid* h = nullptr;
+        check(aprgpu_pyramid_create_explicit(ctx_, w.data(), k3.data(), p.l_min, p.l_max, &h));
+        pyr_cache_.push_front(PyrEntry{key, p.l_min, w, k3, PyrRef(h, [](aprgpu_pyramid* q) { aprgpu_pyramid_free(q); })});
+        while (pyr_cache_.size() > kCacheSize * 2) pyr_cache_.pop_back();
+        return pyr_cache_.front().ref;
+    }
+
+    // $APRGPU_DEVICES with more than one device: the APR's z-slabs (cached like
+    // the single-device handles); null otherwise.
+    using MultiRef = std::shared_ptr<aprgpu_multi>;
+    MultiRef multi(const APR& apr, int halo) {
+        if (devices_.size() < 2) return nullptr;
+        const bool tree = well_formed(apr.tree_access);
+        const AddrKey ak = addr_key(apr.access, tree ? &apr.tree_access : nullptr, apr.source_dims);
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto it = multi_cache_.begin(); it != multi_cache_.end(); ++it)
+            if (it->first == ak && it->second.first >= halo) return it->second.second;
+        const aprgpu_access_desc leaf = describe(apr.access);
+        aprgpu_access_desc td{};
+        if (tree) td = describe(apr.tree_access);
+        const int32_t dims[3] = {apr.source_dims[0], apr.source_dims[1], apr.source_dims[2]};
+        aprgpu_multi* m = nullptr;
+        const int st = aprgpu_multi_create(devices_.data(), static_cast<int>(devices_.size()), &leaf,
+                                           tree ? &td : nullptr, dims, halo, &m);
+        if (st == APRGPU_ERR_RANGE) return nullptr;  // too thin to cut: one device does it
+        check(st);
+        multi_cache_.emplace_front(ak, std::make_pair(halo, MultiRef(m, [](aprgpu_multi* q) { aprgpu_multi_free(q); })));
+        while (multi_cache_.size() > 2) multi_cache_.pop_back();
+        return multi_cache_.front().second.second;
     }
 
     // Device handle of a bare access structure (leaf only; dims = its finest grid).
@@ -163,16 +228,19 @@ public:
         f.access(a);
         f.bytes(dims.data(), sizeof(int) * 3);
         f.bytes("access-only", 11);
-        return lookup(f.value(), [&](aprgpu_apr** out) {
-            if (!well_formed(a)) throw RangeError("access structure has no levels");
-            const aprgpu_access_desc leaf = describe(a);
-            const int32_t d3[3] = {dims[0], dims[1], dims[2]};
-            return aprgpu_upload_access(ctx_, &leaf, nullptr, d3, out);
-        });
+        return lookup(f.value(), AddrKey{}, [&](aprgpu_apr* h) { return same_structure(h, a); },
+                      [&](aprgpu_apr** out) {
+                          if (!well_formed(a)) throw RangeError("access structure has no levels");
+                          const aprgpu_access_desc leaf = describe(a);
+                          const int32_t d3[3] = {dims[0], dims[1], dims[2]};
+                          return aprgpu_upload_access(ctx_, &leaf, nullptr, d3, out);
+                      });
     }
 
     ~Runtime() {
         cache_.clear();  // (the handles free themselves)
+        pyr_cache_.clear();
+        multi_cache_.clear();
         if (ctx_) aprgpu_ctx_free(ctx_);
     }
 
@@ -182,50 +250,124 @@ private:
         check(aprgpu_init(dev ? std::atoi(dev) : 0, &ctx_));
         const char* acc = std::getenv("APRGPU_ACCUM");
         accum_ = (acc && std::string(acc) == "fast") ? APRGPU_ACCUM_FAST : APRGPU_ACCUM_EXACT;
+        if (const char* ds = std::getenv("APRGPU_DEVICES")) {  // "0,1,2,3": z-slabs over these devices
+            for (const char* p = ds; *p;) {
+                char* end = nullptr;
+                const long d = std::strtol(p, &end, 10);
+                if (end == p) break;
+                devices_.push_back(static_cast<int>(d));
+                p = *end ? end + 1 : end;
+            }
+        }
     }
 
-    template <class Upload>
-    Ref lookup(std::uint64_t key, Upload&& up) {
+    // The cheap identity of an APR: its arrays' addresses and sizes, its dims,
+    // and a strided sample of its contents (the arrays are immutable once
+    // built; the sample guards against a new APR reusing freed addresses).
+    struct AddrKey {
+        const void* p[4] = {};
+        std::size_t n[4] = {};
+        std::array<int, 3> dims{};
+        std::uint64_t sample = 0;
+        bool operator==(const AddrKey& o) const {
+            for (int i = 0; i < 4; ++i)
+                if (p[i] != o.p[i] || n[i] != o.n[i]) return false;
+            return dims == o.dims && sample == o.sample && p[0] != nullptr;
+        }
+    };
+    static AddrKey addr_key(const LinearAccess& a, const LinearAccess* t, const std::array<int, 3>& dims) {
+        AddrKey k;
+        k.p[0] = a.y_idx.data();
+        k.n[0] = a.y_idx.size();
+        k.p[1] = a.xz_end.data();
+        k.n[1] = a.xz_end.size();
+        if (t) {
+            k.p[2] = t->y_idx.data();
+            k.n[2] = t->y_idx.size();
+            k.p[3] = t->xz_end.data();
+            k.n[3] = t->xz_end.size();
+        }
+        k.dims = dims;
+        Fingerprint f;  // 1024 strided samples of each array (+ the last entry)
+        auto sample = [&f](const auto& v) {
+            const std::size_t n = v.size();
+            for (std::size_t i = 0, st = n / 1024 + 1; i < n; i += st) f.bytes(&v[i], sizeof(v[i]));
+            if (n) f.bytes(&v[n - 1], sizeof(v[n - 1]));
+        };
+        sample(a.y_idx);
+        sample(a.xz_end);
+        sample(a.level_offset);
+        if (t) {
+            sample(t->y_idx);
+            sample(t->xz_end);
+        }
+        k.sample = f.value();
+        return k;
+    }
+    // Full verification of a content-fingerprint hit: the device structure
+    // equals the host arrays (guards against 64-bit fingerprint collisions).
+    static bool same_structure(aprgpu_apr* h, const LinearAccess& a) {
+        aprgpu_access_info info{};
+        if (aprgpu_access_get_info(h, APRGPU_LEAF, &info) != APRGPU_OK) return false;
+        if (info.l_min != a.l_min || info.l_max != a.l_max || info.n_particles != a.y_idx.size() ||
+            info.n_rows != a.xz_end.size())
+            return false;
+        const std::size_t n = static_cast<std::size_t>(info.l_max) + 1;
+        std::vector<std::uint16_t> y(info.n_particles);
+        std::vector<std::uint64_t> xz(info.n_rows), lo(n);
+        std::vector<int32_t> zd(n), xd(n), yd(n);
+        if (aprgpu_download_access(h, APRGPU_LEAF, y.data(), xz.data(), lo.data(), zd.data(), xd.data(), yd.data()) !=
+            APRGPU_OK)
+            return false;
+        return y == a.y_idx && xz == a.xz_end;
+    }
+
+    template <class Verify, class Upload>
+    Ref lookup(std::uint64_t key, const AddrKey& ak, Verify&& verify, Upload&& up) {
         std::lock_guard<std::mutex> lk(mu_);
         for (auto it = cache_.begin(); it != cache_.end(); ++it)
-            if (it->first == key) {
+            if (it->key == key && verify(it->ref.get())) {
+                it->addr = ak;  // (the same structure at new addresses)
                 cache_.splice(cache_.begin(), cache_, it);
-                return cache_.front().second;
+                return cache_.front().ref;
             }
         aprgpu_apr* h = nullptr;
         check(up(&h));
-        cache_.emplace_front(key, Ref(h, [](aprgpu_apr* p) { aprgpu_apr_free(p); }));
+        cache_.push_front(Entry{key, ak, Ref(h, [](aprgpu_apr* p) { aprgpu_apr_free(p); })});
         while (cache_.size() > kCacheSize) cache_.pop_back();  // freed when its last holder lets go
-        return cache_.front().second;
+        return cache_.front().ref;
     }
 
+    struct Entry {
+        std::uint64_t key;
+        AddrKey addr;
+        Ref ref;
+    };
+    struct PyrEntry {
+        std::uint64_t key;
+        int l_min;
+        std::vector<float> w;
+        std::vector<int32_t> k3;
+        PyrRef ref;
+    };
     static constexpr std::size_t kCacheSize = 8;
     aprgpu_ctx* ctx_ = nullptr;
     int accum_ = APRGPU_ACCUM_EXACT;
+    std::vector<int> devices_;
     std::mutex mu_;
-    std::list<std::pair<std::uint64_t, Ref>> cache_;
+    std::list<Entry> cache_;
+    std::list<PyrEntry> pyr_cache_;
+    std::list<std::pair<AddrKey, std::pair<int, MultiRef>>> multi_cache_;
 };
 
-// A StencilPyramid held on the device for one call.
+// A StencilPyramid held on the device (cached by content in the Runtime).
 class DevicePyramid {
 public:
-    explicit DevicePyramid(const StencilPyramid& p) {
-        std::vector<float> w;
-        std::vector<int32_t> k3;
-        for (const Stencil& s : p.stencils) {
-            w.insert(w.end(), s.weights.begin(), s.weights.end());
-            k3.insert(k3.end(), {s.kz, s.kx, s.ky});
-        }
-        if (p.stencils.empty()) throw RangeError("StencilPyramid has no levels");
-        check(aprgpu_pyramid_create_explicit(Runtime::get().ctx(), w.data(), k3.data(), p.l_min, p.l_max, &h_));
-    }
-    ~DevicePyramid() { aprgpu_pyramid_free(h_); }
-    DevicePyramid(const DevicePyramid&) = delete;
-    DevicePyramid& operator=(const DevicePyramid&) = delete;
-    aprgpu_pyramid* get() const { return h_; }
+    explicit DevicePyramid(const StencilPyramid& p) : ref_(Runtime::get().pyramid(p)) {}
+    aprgpu_pyramid* get() const { return ref_.get(); }
 
 private:
-    aprgpu_pyramid* h_ = nullptr;
+    Runtime::PyrRef ref_;
 };
 
 inline std::uint64_t count(aprgpu_apr* h, int which) {

@@ -19,6 +19,8 @@
 #undef nonempty_row_index
 #undef convolve_pixels
 
+#include <algorithm>
+
 #include "aprkit_gpu.hpp"
 
 namespace aprkit {
@@ -90,9 +92,28 @@ inline ParticleValues convolve_apr(const APR& apr, const ParticleValues& values,
         gpu::check(aprgpu_fill_tree(h, values.data(), tree_filled.data(), APRGPU_HOST, nullptr));
         tv = &tree_filled;
     }
-    gpu::DevicePyramid dp(pyramid);
     ParticleValues out(values.size(), 0.0f);
     if (out.empty()) return out;
+    // $APRGPU_DEVICES: z-slabs over several GPUs (halo = the largest half-width)
+    int hw = 1;
+    for (int l = a.l_min; l <= a.l_max; ++l) {
+        const Stencil& w = pyramid.at(l);
+        hw = std::max(hw, std::max(w.kz, std::max(w.kx, w.ky)) / 2);
+    }
+    if (const auto m = rt.multi(apr, std::max(hw, 2))) {
+        std::vector<float> w;
+        std::vector<int32_t> k3;
+        for (const Stencil& st : pyramid.stencils) {
+            w.insert(w.end(), st.weights.begin(), st.weights.end());
+            k3.insert(k3.end(), {st.kz, st.kx, st.ky});
+        }
+        gpu::check(aprgpu_multi_convolve(m.get(), values.data(), tv->empty() ? nullptr : tv->data(), w.data(),
+                                         k3.data(), pyramid.l_min, pyramid.l_max,
+                                         pad == PadMode::Zero ? APRGPU_PAD_ZERO : APRGPU_PAD_REFLECT, rt.accum(),
+                                         out.data()));
+        return out;
+    }
+    gpu::DevicePyramid dp(pyramid);
     gpu::check(aprgpu_convolve(h, values.data(), tv->empty() ? nullptr : tv->data(), dp.get(),
                                pad == PadMode::Zero ? APRGPU_PAD_ZERO : APRGPU_PAD_REFLECT, rt.accum(), out.data(),
                                APRGPU_HOST, nullptr));

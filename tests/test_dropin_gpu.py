@@ -18,10 +18,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "cpp", "_build")
 
 
-def _run(args, timeout):
+def _run(args, timeout, env=None):
     if not os.path.exists(args[0]):
         pytest.skip(f"{os.path.basename(args[0])} not built (needs /root/reference at build time)")
-    p = subprocess.run(args, capture_output=True, text=True, timeout=timeout)
+    p = subprocess.run(args, capture_output=True, text=True, timeout=timeout,
+                       env=dict(os.environ, **env) if env else None)
     return p.returncode, p.stdout + p.stderr
 
 
@@ -45,4 +46,21 @@ def test_reference_acceptance_serialization_on_the_dropin(tmp_path):
     rc, out = _run([exe, str(tmp_path), "--write-fixtures", "10"], 900)
     assert rc == 0 and "PASS" in out, out[-3000:]
     rc, out = _run([exe, str(tmp_path), "10"], 900)
+    assert rc == 0 and "PASS" in out, out[-3000:]
+
+
+# The same unmodified reference tests with APRGPU_DEVICES=0,0: every
+# convolve_apr the drop-in serves runs on two z-slabs (aprgpu_multi_*) -- two
+# virtual slabs of device 0 on this one-GPU box, the N-GPU code path verbatim
+# (structures too thin to cut fall back to one slab).
+def test_reference_unit_tests_pass_on_two_slabs():
+    rc, out = _run([os.path.join(BUILD, "unit_tests")], 900, env={"APRGPU_DEVICES": "0,0"})
+    assert rc == 0, out[-4000:]
+    assert "failed: 0 | assertions" in out, out[-2000:]
+
+
+@pytest.mark.parametrize("criterion", [3, 4, 8, 9])
+def test_reference_acceptance_on_two_slabs(criterion, tmp_path):
+    rc, out = _run([os.path.join(BUILD, "acceptance"), str(tmp_path), str(criterion)], 1800,
+                   env={"APRGPU_DEVICES": "0,0"})
     assert rc == 0 and "PASS" in out, out[-3000:]
