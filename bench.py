@@ -438,15 +438,18 @@ def run_ours(args, rank, world):
 # ------------------------------------------------------- multi-GPU z-slabs ---
 def run_slab(args, rank, world):
     """N > 1: one volume cut into z-slabs, one per GPU (paper_2112_03592_b200.slab,
-    DESIGN.md §6) -- for C3, the C3 APR tiled N times along z (weak scaling:
-    each GPU holds a C3-sized slab); other configs: the one volume (strong).  A conv-only step is the halo
-    exchange of leaf and tree values over NCCL plus each rank's slab
-    convolution; the paper step adds the slab tree fill with its cut-level
-    all-gather.  Time = max over ranks of the CUDA-event step time."""
+    DESIGN.md §6).  --config c3 (default): the C3 APR tiled N times along z --
+    weak scaling, each GPU holds a C3-sized slab; --config c4: the C4 APR (C3
+    tiled 4 x 4 x 2) cut into N slabs -- strong scaling of BASELINE config 4.
+    A conv-only step is the leaf + tree halo exchange over NCCL in flight while
+    every rank convolves its slab's interior, then the boundary bands; the
+    paper step adds the slab tree fill with its cut-level all-gather.  Time =
+    max over ranks of the CUDA-event step time."""
     import torch
     import torch.distributed as dist
     import paper_2112_03592_b200 as P
     from paper_2112_03592_b200 import _lib as L
+    from paper_2112_03592_b200 import synth
     from paper_2112_03592_b200.slab import GpuRankState, SlabConvolver, SlabPlan, TorchComm
 
     dev_id = int(os.environ.get("LOCAL_RANK", 0))
@@ -454,36 +457,44 @@ def run_slab(args, rank, world):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = P.default_context(dev_id)
-    vdev = None
-    tz = int(os.environ.get("APRGPU_BENCH_TILEZ", world))  # (a test hook: the tiling at any world size)
-    if args.config == "c3" and tz > 1:
-        # weak scaling: the C3 APR tiled N times along z on the device -- one
-        # C3-sized z-slab per GPU, neighbours exchanging halos
-        from paper_2112_03592_b200 import synth
+    tz = int(os.environ.get("APRGPU_BENCH_TILEZ", world))  # (a test hook: the tiled C3 at any world size)
+    if args.config == "c4":
+        tiling, scaling = (4, 4, 2), "strong"
+    elif args.config == "c3" and tz > 1:
+        tiling, scaling = (tz, 1, 1), "weak"
+    else:
+        tiling, scaling = None, "strong"
+    if tiling:
         apr3, values3, _ = workload("c3")
         d3 = apr3.device(ctx)
-        dapr = synth.tile_apr(d3, tz, 1, 1)
+        dapr = synth.tile_apr(d3, *tiling)
         v3 = torch.from_numpy(np.ascontiguousarray(values3, np.float32)).cuda()
         vdev = torch.empty(dapr.n_particles, dtype=torch.float32, device="cuda")
-        synth.tile_values(d3, dapr, tz, 1, 1, v3.data_ptr(), vdev.data_ptr())
+        synth.tile_values(d3, dapr, *tiling, v3.data_ptr(), vdev.data_ptr())
         torch.cuda.synchronize()
         del v3, d3
-        apr = P.APR(dapr.download(L.LEAF), dapr.download(L.TREE), tuple(int(d) for d in dapr.dims))
-        apr._dev[ctx.device] = dapr
-        values = vdev.cpu().numpy()
-        desc = {"workload": f"C3 tiled {tz}(z) x 1 x 1 -> {1024 * tz} x 1024 x 1024 pixel-equivalent "
-                            "(device tiler): one C3-sized z-slab per GPU (weak scaling)"}
-        scaling = "weak"
+        leaf, tree = dapr.download(L.LEAF, rows_only=True), dapr.download(L.TREE, rows_only=True)
+        dims = tuple(int(d) for d in dapr.dims)
+        values = None
+        if args.config == "c4":
+            desc = WORKLOADS["c4"]
+        else:
+            desc = (f"C3 tiled {tz}(z) x 1 x 1 -> {1024 * tz} x 1024 x 1024 pixel-equivalent (device tiler): "
+                    "one C3-sized z-slab per GPU (weak scaling)")
     else:
         apr, values, _ = workload(args.config)
-        desc = {"workload": WORKLOADS[args.config]}
+        desc = WORKLOADS[args.config]
         dapr = apr.device(ctx)
-        scaling = "strong"
+        leaf, tree, dims = apr.access, apr.tree_access, tuple(apr.source_dims)
+        vdev = None
+    li, ti = dapr.info(L.LEAF), dapr.info(L.TREE)
+    n_p, n_t, n_rows = int(li.n_particles), int(ti.n_particles), int(li.n_rows + ti.n_rows)
+    n_pix = int(np.prod(dims, dtype=np.int64))
     k = args.stencil
-    pyr = P.make_pyramid(P.gaussian_stencil(1.0, k), apr.access.l_min, apr.access.l_max, P.PyramidMode.Restricted)
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, k), int(li.l_min), int(li.l_max), P.PyramidMode.Restricted)
     dpyr = pyr.device(ctx)
     accum = L.ACCUM_EXACT if args.accum == "exact" else L.ACCUM_FAST
-    plan = SlabPlan.make(apr.access, apr.tree_access, apr.source_dims, world, rank, halo=max(k // 2, 1))
+    plan = SlabPlan.make(leaf, tree, dims, world, rank, halo=max(k // 2, 1))
     st = GpuRankState(plan, dapr, dev_id, stream)
     if vdev is not None:
         st.values.copy_(vdev)
@@ -493,12 +504,9 @@ def run_slab(args, rank, world):
     comm = TorchComm()
     sc = SlabConvolver([st], comm)
     sc.fill_tree()
-    leaf_x, tree_x = plan.halo_transfers("leaf"), plan.halo_transfers("tree")
 
     def conv():
-        comm.exchange([st], "values", leaf_x)
-        comm.exchange([st], "tree", tree_x)
-        st.convolve_slab(dpyr, 1, accum)
+        sc.exchange_and_convolve(dpyr, 1, accum)
 
     def paper_step():
         sc.convolve(dpyr, 1, accum)
@@ -533,8 +541,10 @@ def run_slab(args, rank, world):
     # end to end: this rank's owned values from pinned host memory, the step,
     # its owned outputs back to the host
     owned = plan.owned("leaf") + [plan.replicated("leaf")]
-    hv = torch.from_numpy(np.ascontiguousarray(values, np.float32)).pin_memory()
-    hout = torch.empty(dapr.n_particles, dtype=torch.float32).pin_memory()
+    hv = torch.empty(max(n_p, 1), dtype=torch.float32).pin_memory()
+    for b, e in owned:
+        hv[b:e].copy_(st.values[b:e])
+    hout = torch.empty(max(n_p, 1), dtype=torch.float32).pin_memory()
     e2e = []
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
@@ -556,11 +566,11 @@ def run_slab(args, rank, world):
         return float(tt.item())
 
     tc, tp, te = agg(t_conv), agg(t_paper), agg(e2e)
-    n_pix, n_p = apr.pixel_count(), apr.access.particle_count()
-    B = algorithmic_bytes(apr.access.particle_count(), apr.tree_access.particle_count(),
-                          apr.access.row_count() + apr.tree_access.row_count())
+    B = algorithmic_bytes(n_p, n_t, n_rows)
     peak, peak_kind = peaks()
     achieved = B / world / tc / 1e9  # per GPU: each owns ~1/N of the bytes
+    cfg = bench_config(args.config, k, n_p, n_t, n_pix)
+    cfg["workload"] = desc
     return {
         "metric": METRIC,
         "value": round(4 * n_pix / tc / 1e9, 3),
@@ -572,12 +582,12 @@ def run_slab(args, rank, world):
         "higher_is_better": True,
         "scaling": scaling,
         "vs_baseline": None,
-        "dtype": "f32 values, " + ("f64 accumulate (bit-exact)" if accum == L.ACCUM_EXACT else "f32 accumulate"),
+        "dtype": "f32 values, " + ("f64 accumulate in the reference's tap order (bit-exact)"
+                                   if accum == L.ACCUM_EXACT else "f32 accumulate"),
         "data": "synthetic",
-        "config": dict(desc, stencil=f"gaussian(1.0,{k}) restricted pyramid", pad="reflect", particles=n_p,
-                       pixels=n_pix, l2="flushed between timed steps (256 MB write)",
-                       protocol="conv-only: NCCL halo exchange (leaf + tree) + slab convolution",
-                       parallelism=f"z-slabs x{world} (cut level {plan.lc}, halo {plan.halo} rows/level)"),
+        "config": cfg,
+        "parallelism": f"z-slabs x{world} (cut level {plan.lc}, halo {plan.halo} rows/level), NCCL halo exchange "
+                       "overlapped with each slab's interior",
         "particles_per_s": round(n_p / tc, 1),
         "paper_protocol": {"ms_per_step": round(tp * 1e3, 4), "gbps_pixel_equiv": round(4 * n_pix / tp / 1e9, 3),
                            "includes": "halo exchange + slab fill_tree (cut-level all-gather) + slab convolution"},

@@ -241,6 +241,13 @@ int aprgpu_fill_tree_finalize(aprgpu_apr* apr, float* tree, void* stream);
  * every level < lc; other outputs are left untouched. */
 int aprgpu_convolve_slab(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
                          int pad_mode, int accum, int lc, int z_lo, int z_hi, float* out, void* stream);
+/* The same over a band of a slab, the replicated levels < lc computed only when
+ * `replicated` is nonzero: how a rank convolves its interior (planes at least
+ * halo * 2^(l_max - lc) from a cut) while the halo exchange is in flight, then
+ * its boundary bands once the halos have landed. */
+int aprgpu_convolve_slab_band(aprgpu_apr* apr, const float* values, const float* tree_values,
+                              const aprgpu_pyramid* pyr, int pad_mode, int accum, int lc, int z_lo, int z_hi,
+                              int replicated, float* out, void* stream);
 
 /* ---- multi-GPU z-slabs in one process (csrc/multi.cu) -------
  * The volume cut into n_slabs z-slabs, slab s on device devices[s] (entries

@@ -87,6 +87,8 @@ _SIGS = {
     "aprgpu_multi_info": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "aprgpu_multi_convolve": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                               C.c_int, C.c_void_p],
+    "aprgpu_convolve_slab_band": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, C.c_void_p, C.c_void_p],
     "aprgpu_convolve_slab": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_void_p, C.c_void_p],
     "aprgpu_tile_apr": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)],

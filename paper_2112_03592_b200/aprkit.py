@@ -456,15 +456,17 @@ class DeviceApr:
         L.check(L.lib().aprgpu_access_get_info(self.handle, which, C.byref(i)))
         return i
 
-    def download(self, which: int) -> LinearAccess:
+    def download(self, which: int, rows_only: bool = False) -> LinearAccess:
+        """The access structure back in the reference layout; rows_only skips
+        y_idx (the row geometry a slab plan needs, without C4's 1.1 GB)."""
         i = self.info(which)
         n = i.l_max + 1
-        y = np.empty(i.n_particles, np.uint16)
+        y = np.empty(0 if rows_only else i.n_particles, np.uint16)
         e = np.empty(i.n_rows, np.uint64)
         lo = np.zeros(n, np.uint64)
         zd, xd, yd = (np.zeros(n, np.int32) for _ in range(3))
-        L.check(L.lib().aprgpu_download_access(self.handle, which, _ptr(y), _ptr(e), _ptr(lo), _ptr(zd), _ptr(xd),
-                                               _ptr(yd)))
+        L.check(L.lib().aprgpu_download_access(self.handle, which, None if rows_only else _ptr(y), _ptr(e), _ptr(lo),
+                                               _ptr(zd), _ptr(xd), _ptr(yd)))
         return LinearAccess(i.l_min, i.l_max, zd, xd, yd, y, e, lo)
 
     def row_index(self, level: int):

@@ -1133,6 +1133,12 @@ int aprgpu_fill_tree_finalize(aprgpu_apr* apr, float* tree, void* stream) {
 
 int aprgpu_convolve_slab(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
                          int pad_mode, int accum, int lc, int z_lo, int z_hi, float* out, void* stream) {
+    return aprgpu_convolve_slab_band(apr, values, tree_values, pyr, pad_mode, accum, lc, z_lo, z_hi, 1, out, stream);
+}
+
+int aprgpu_convolve_slab_band(aprgpu_apr* apr, const float* values, const float* tree_values,
+                              const aprgpu_pyramid* pyr, int pad_mode, int accum, int lc, int z_lo, int z_hi,
+                              int replicated, float* out, void* stream) {
     return guard([&] {
         need(apr && values && pyr && out, "null argument");
         need(tree_values || apr->tree.n_particles == 0, "tree values are required");
@@ -1145,6 +1151,7 @@ int aprgpu_convolve_slab(aprgpu_apr* apr, const float* values, const float* tree
         slab.lc = lc;
         slab.z_lo = z_lo;
         slab.z_hi = z_hi;
+        slab.rep = replicated != 0;
         aprgpu::EpiArgs epi;
         aprgpu::convolve_device(apr, values, tree_values, pyr, pad_mode, accum, out, epi,
                                 aprgpu::pick_stream(apr->ctx, stream), slab);

@@ -142,6 +142,23 @@ class SlabPlan:
                     out.append((r + 1, r, rng))
         return out
 
+    def bands(self, r: Optional[int] = None):
+        """(interior, [boundary bands]) of rank r's slab, in finest planes: the
+        interior lies at least halo level-lc rows (= halo * 2^c planes, which
+        covers every partitioned level's halo) from each cut, so its outputs
+        read no halo; the bands are the rest of the slab."""
+        r = self.rank if r is None else r
+        z0, z1 = self.bounds[r]
+        m = self.halo << self.c
+        lo = z0 + (m if r > 0 else 0)
+        hi = z1 - (m if r + 1 < self.world else 0)
+        edges = []
+        if r > 0:
+            edges.append((z0, min(z0 + m, z1)))
+        if r + 1 < self.world:
+            edges.append((max(hi, lo, z0), z1))
+        return (lo, hi), [(a, b) for a, b in edges if b > a]
+
     def cut_ranges(self, which: str) -> List[Range]:
         """Per rank, its rows of the cut level lc (leaf level lc / tree level lc)."""
         a = self.leaf if which == "leaf" else self.tree
@@ -158,6 +175,13 @@ class LocalComm:
         for src, dst, (b, e) in transfers:
             getattr(states[dst], attr)[b:e].copy_(getattr(states[src], attr)[b:e])
 
+    def exchange_async(self, states, attr: str, transfers):
+        self.exchange(states, attr, transfers)
+        return []
+
+    def wait(self, works):
+        pass
+
     def allgather_ranges(self, states, attr: str, ranges):
         for s in states:
             for r, (b, e) in enumerate(ranges):
@@ -173,6 +197,11 @@ class TorchComm:
         self.dist, self.group = dist, group
 
     def exchange(self, states, attr: str, transfers):
+        self.wait(self.exchange_async(states, attr, transfers))
+
+    def exchange_async(self, states, attr: str, transfers):
+        """Grouped point-to-point sends/receives, returned in flight (NCCL runs
+        them on its own stream, after the work already queued on ours)."""
         (s,) = states
         arr = getattr(s, attr)
         ops = []
@@ -181,9 +210,11 @@ class TorchComm:
                 ops.append(self.dist.P2POp(self.dist.isend, arr[b:e], dst, self.group))
             elif s.rank == dst:
                 ops.append(self.dist.P2POp(self.dist.irecv, arr[b:e], src, self.group))
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
+        return self.dist.batch_isend_irecv(ops) if ops else []
+
+    def wait(self, works):
+        for req in works:
+            req.wait()  # (NCCL: the current stream waits; the host does not)
 
     def allgather_ranges(self, states, attr: str, ranges):
         import torch
@@ -249,6 +280,13 @@ class GpuRankState:
                                              pyr.handle, int(pad), int(accum), self.plan.lc, z_lo, z_hi,
                                              self.out.data_ptr(), self._s()))
 
+    def convolve_band(self, pyr, pad: int, accum: int, z_lo: int, z_hi: int, replicated: bool):
+        if z_hi <= z_lo and not replicated:
+            return
+        L.check(L.lib().aprgpu_convolve_slab_band(self.dev.handle, self.values.data_ptr(), self.tree.data_ptr(),
+                                                  pyr.handle, int(pad), int(accum), self.plan.lc, z_lo,
+                                                  max(z_lo, z_hi), int(replicated), self.out.data_ptr(), self._s()))
+
 
 # ------------------------------------------------------------ algorithm ------
 class SlabConvolver:
@@ -276,6 +314,22 @@ class SlabConvolver:
                 s.tree_sums(t.l_min, p.lc - 1, slab=False)
         for s in self.states:
             s.finalize()
+
+    def exchange_and_convolve(self, pyr, pad: int = L.PAD_REFLECT, accum: int = L.ACCUM_EXACT):
+        """The conv-only step with the tree values already filled: the leaf and
+        tree halo exchanges in flight while every rank convolves its interior,
+        then the boundary bands once the halos have landed."""
+        p = self.plan
+        works = self.comm.exchange_async(self.states, "values", p.halo_transfers("leaf"))
+        if p.tree is not None:
+            works += self.comm.exchange_async(self.states, "tree", p.halo_transfers("tree"))
+        for s in self.states:
+            (lo, hi), _ = p.bands(s.rank)
+            s.convolve_band(pyr, pad, accum, lo, hi, True)
+        self.comm.wait(works)
+        for s in self.states:
+            for lo, hi in p.bands(s.rank)[1]:
+                s.convolve_band(pyr, pad, accum, lo, hi, False)
 
     def convolve(self, pyr, pad: int = L.PAD_REFLECT, accum: int = L.ACCUM_EXACT):
         p = self.plan

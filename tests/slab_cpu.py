@@ -119,3 +119,18 @@ class CpuRankState:
         full = Oracle().convolve(self.plan.leaf, self.plan.tree, self.values.numpy(), self.tree.numpy(),
                                  self.levels, self.level_min, int(pad))
         self.out.copy_(torch.from_numpy(full))
+
+    def convolve_band(self, pyr, pad, accum, z_lo, z_hi, replicated):
+        """aprgpu_convolve_slab_band restated: only the outputs of the band's
+        rows at the partitioned levels (and the replicated levels if asked)."""
+        from paper_2112_03592_b200.slab import _row_particles
+        full = torch.from_numpy(Oracle().convolve(self.plan.leaf, self.plan.tree, self.values.numpy(),
+                                                  self.tree.numpy(), self.levels, self.level_min, int(pad)))
+        p = self.plan
+        if replicated:
+            b, e = p.replicated("leaf")
+            self.out[b:e] = full[b:e]
+        for l in p._levels(p.leaf):
+            sh = p.l_max - l
+            b, e = _row_particles(p.leaf, l, z_lo >> sh, (z_hi + (1 << sh) - 1) >> sh)
+            self.out[b:e] = full[b:e]

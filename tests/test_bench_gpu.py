@@ -50,7 +50,7 @@ def test_bench_slab_path_over_nccl():
     d = _line(r.stdout)
     for k in KEYS:
         assert k in d, k
-    assert d["scaling"] == "strong" and d["gpu_launches"] > 0 and "z-slabs" in d["config"]["parallelism"]
+    assert d["scaling"] == "strong" and d["gpu_launches"] > 0 and "z-slabs" in d["parallelism"]
 
 
 @pytest.mark.gpu
@@ -65,3 +65,18 @@ def test_bench_weak_scaling_slab_workload():
     d = _line(r.stdout)
     assert d["scaling"] == "weak" and "2048 x 1024 x 1024" in d["config"]["workload"]
     assert d["config"]["particles"] > 30_000_000
+
+
+@pytest.mark.gpu
+def test_bench_c4_slab_path():
+    # BASELINE config 4 through the N > 1 path (strong scaling of the C4 APR
+    # over z-slabs; one rank here), as `bench.py --gpus N --config c4` runs it
+    env = dict(os.environ, APRGPU_BENCH_SLAB="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "1",
+                        "--config", "c4", "--steps", "3", "--warmup", "3"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=1200, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _line(r.stdout)
+    assert d["scaling"] == "strong" and d["config"]["particles"] == 547570496
+    assert d["value"] > 0 and d["gpu_launches"] > 0

@@ -167,3 +167,83 @@ def test_slab_gpu_virtual_ranks_bit_identical(name, world, accum):
         town = _owned_mask(st.plan, "tree", d["tree_values"].size)
         tv = st.tree.cpu().numpy()[:town.size]
         assert np.array_equal(G.bits(tv[town]), G.bits(d["tree_values"][town])), st.rank
+
+
+class DeferredComm(LocalComm):
+    """Virtual ranks whose halo exchanges only land at wait(): the interior
+    pass of exchange_and_convolve runs while every halo entry is still NaN."""
+
+    def exchange_async(self, states, attr, transfers):
+        return [lambda: LocalComm.exchange(self, states, attr, transfers)]
+
+    def wait(self, works):
+        for w in works:
+            w()
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("world", [2, 3])
+def test_interior_bands_need_no_halo_cpu(name, world):
+    """exchange_and_convolve (interior while the exchange is in flight, then
+    the boundary bands) with NaN halos during the interior pass: every owned
+    output still equals the reference bit for bit (CPU, C oracle ranks)."""
+    d = G.load(name)
+    apr, plans = _plans(d, world)
+    conv = sorted(k for k in G.conv_names(d))[0]
+    levels = G.pyramid_levels(d, conv)
+    states = []
+    for p in plans:
+        st = CpuRankState(p, apr.source_dims, levels, int(d["leaf_l_range"][0]))
+        v = d["values"].copy()
+        v[~_owned_mask(p, "leaf", v.size)] = np.nan
+        st.values.copy_(torch.from_numpy(v))
+        states.append(st)
+    sc = SlabConvolver(states, DeferredComm())
+    sc.fill_tree()
+    for st in states:  # the tree halos are NaN too until the exchange lands
+        t = st.tree.numpy()
+        t[~_owned_mask(st.plan, "tree", t.size)] = np.nan
+    sc.exchange_and_convolve(None, int(d[f"conv_{conv}_pad"][0]), L.ACCUM_EXACT)
+    for st in states:
+        own = _owned_mask(st.plan, "leaf", d["values"].size)
+        assert np.array_equal(G.bits(st.out.numpy()[own]), G.bits(d[f"conv_{conv}_out"][own])), st.rank
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES + ["c1_256"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_interior_bands_need_no_halo_gpu(name, world):
+    """The same on device state (aprgpu_convolve_slab_band), virtual ranks."""
+    from paper_2112_03592_b200.slab import GpuRankState
+    d = G.load(name)
+    apr = G.product_apr(d)
+    try:
+        plans = [SlabPlan.make(apr.access, apr.tree_access, apr.source_dims, world, r, halo=2) for r in range(world)]
+    except ValueError:
+        pytest.skip("volume too thin for this many slabs")
+    a = apr.access
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, 5), a.l_min, a.l_max, P.PyramidMode.Restricted)
+    tv = P.fill_tree(apr, d["values"])
+    ref = P.convolve_apr(apr, d["values"], tv, pyr)
+    ctx = P.default_context()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    states = []
+    for p in plans:
+        dev = P.DeviceApr.upload(ctx, apr)
+        st = GpuRankState(p, dev)
+        v = d["values"].copy()
+        v[~_owned_mask(p, "leaf", v.size)] = np.nan
+        st.values.copy_(torch.from_numpy(v))
+        states.append((st, dev))
+    sts = [s for s, _ in states]
+    sc = SlabConvolver(sts, DeferredComm())
+    sc.fill_tree()
+    for st in sts:
+        own_t = torch.from_numpy(_owned_mask(st.plan, "tree", st.tree.numel())).to(st.tree.device)
+        st.tree[~own_t] = float("nan")
+    sc.exchange_and_convolve(pyr.device(ctx), 1, L.ACCUM_EXACT)
+    torch.cuda.synchronize()
+    for st in sts:
+        own = _owned_mask(st.plan, "leaf", ref.size)
+        assert np.array_equal(G.bits(st.out.cpu().numpy()[:ref.size][own]), G.bits(ref[own])), st.rank
