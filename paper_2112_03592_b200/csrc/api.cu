@@ -104,6 +104,41 @@ aprgpu::HostStencil make_host_stencil(const float* w, int kz, int kx, int ky) {
     return s;
 }
 
+// Rank-1 factors of a stencil from its marginals: w[a][b][c] ~ Mz[a] Mx[b] My[c]
+// / S^2 (S = sum of w).  Accepted when every weight matches to 5e-7 relative
+// (a truncated Gaussian, stencil.hpp:59-79, and its restrictions are products
+// of per-axis factors); appended to sep as floats fz = Mz/S, fx = Mx/S, fy = My.
+bool separable_factors(const float* w, int kz, int kx, int ky, std::vector<float>& sep) {
+    std::vector<double> mz(kz, 0.0), mx(kx, 0.0), my(ky, 0.0);
+    double sum = 0.0;
+    for (int a = 0; a < kz; ++a)
+        for (int b = 0; b < kx; ++b)
+            for (int c = 0; c < ky; ++c) {
+                const double v = w[(static_cast<size_t>(a) * kx + b) * ky + c];
+                if (v < 0.0) return false;
+                mz[a] += v;
+                mx[b] += v;
+                my[c] += v;
+                sum += v;
+            }
+    if (!(sum > 0.0)) return false;
+    std::vector<float> fz(kz), fx(kx), fy(ky);
+    for (int a = 0; a < kz; ++a) fz[a] = static_cast<float>(mz[a] / sum);
+    for (int b = 0; b < kx; ++b) fx[b] = static_cast<float>(mx[b] / sum);
+    for (int c = 0; c < ky; ++c) fy[c] = static_cast<float>(my[c]);
+    for (int a = 0; a < kz; ++a)
+        for (int b = 0; b < kx; ++b)
+            for (int c = 0; c < ky; ++c) {
+                const double v = w[(static_cast<size_t>(a) * kx + b) * ky + c];
+                const double f = static_cast<double>(fz[a]) * fx[b] * fy[c];
+                if (std::fabs(f - v) > 5e-7 * std::fabs(v)) return false;
+            }
+    sep.insert(sep.end(), fz.begin(), fz.end());
+    sep.insert(sep.end(), fx.begin(), fx.end());
+    sep.insert(sep.end(), fy.begin(), fy.end());
+    return true;
+}
+
 void pyramid_upload(aprgpu_pyramid* p) {
     DeviceGuard g(p->ctx->device);
     const size_t n = p->w_host.size();
@@ -112,6 +147,17 @@ void pyramid_upload(aprgpu_pyramid* p) {
     std::vector<double> wd(p->w_host.begin(), p->w_host.end());
     APR_CUDA(cudaMemcpy(p->w_dev, p->w_host.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
     APR_CUDA(cudaMemcpy(p->wd_dev, wd.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    std::vector<float> sep;
+    p->sep_off.assign(p->off.size(), -1);
+    for (size_t i = 0; i < p->off.size(); ++i) {
+        const int* k = &p->k3[3 * i];
+        const size_t at = sep.size();
+        if (separable_factors(p->w_host.data() + p->off[i], k[0], k[1], k[2], sep))
+            p->sep_off[i] = static_cast<int64_t>(at);
+    }
+    APR_CUDA(cudaMalloc(&p->sep_dev, sizeof(float) * (sep.size() + 1)));
+    if (!sep.empty())
+        APR_CUDA(cudaMemcpy(p->sep_dev, sep.data(), sizeof(float) * sep.size(), cudaMemcpyHostToDevice));
 }
 
 void push_level(aprgpu_pyramid* p, const aprgpu::HostStencil& s) {
@@ -824,6 +870,7 @@ int aprgpu_pyramid_free(aprgpu_pyramid* p) {
         if (!p) return;
         cudaFree(p->w_dev);
         cudaFree(p->wd_dev);
+        cudaFree(p->sep_dev);
         delete p;
     });
 }

@@ -82,6 +82,7 @@ struct TileLaunch {
     uint64_t woff[kMaxLevels];      // weight offset of each segment's level
     const float* wf;
     const double* wd;
+    const float* sep[kMaxLevels];   // per segment: rank-1 factors fz, fx, fy of its stencil, or null
     int tree_lmin, tree_lmax;       // interior levels present (tree_lmax < tree_lmin: none)
     int pad;
     float* out;
@@ -530,11 +531,15 @@ __device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int q
     } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = Acc(0);
+        // output (oz, ox, oy) reads neighbourhood cell (oz + 2H - az, ox + 2H - ax, oy + 2H - ay).
+        // Rows stream from the top plane and, within a plane, from the last
+        // row: each output then sees (az, ax) ascending and ay ascending within
+        // a row -- the reference's (az, ax, ay) order -- while only ONE row of
+        // doubles is live (a plane of them would cost (2+2H)^2 more registers)
 #pragma unroll
-        for (int nz = N - 1; nz >= 0; --nz) {
-            Acc v[N][N];
+        for (int nz = N - 1; nz >= 0; --nz)
 #pragma unroll
-            for (int nx = 0; nx < N; ++nx) {
+            for (int nx = N - 1; nx >= 0; --nx) {
                 Acc r[2 * NP];
 #pragma unroll
                 for (int pp = 0; pp < NP; ++pp) {  // exact: every float is a double
@@ -543,27 +548,23 @@ __device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int q
                     r[2 * pp + 1] = static_cast<Acc>(t2.y);
                 }
 #pragma unroll
-                for (int ny = 0; ny < N; ++ny) v[nx][ny] = r[SH + ny];
-            }
-            // output (oz, ox, oy) reads neighbourhood cell (oz + 2H - az, ox + 2H - ax, oy + 2H - ay);
-            // planes stream from the top, so each output sees az ascending
+                for (int oz = 0; oz < 2; ++oz) {
+                    const int az = oz + 2 * H - nz;
+                    if (az < 0 || az > 2 * H) continue;
 #pragma unroll
-            for (int oz = 0; oz < 2; ++oz) {
-                const int az = oz + 2 * H - nz;
-                if (az < 0 || az > 2 * H) continue;
+                    for (int ox = 0; ox < 2; ++ox) {
+                        const int ax = ox + 2 * H - nx;
+                        if (ax < 0 || ax > 2 * H) continue;
 #pragma unroll
-                for (int ox = 0; ox < 2; ++ox)
-#pragma unroll
-                    for (int oy = 0; oy < 2; ++oy)
-#pragma unroll
-                        for (int ax = 0; ax < K; ++ax)
+                        for (int oy = 0; oy < 2; ++oy)
 #pragma unroll
                             for (int ay = 0; ay < K; ++ay)
-                                acc[(oz * 2 + ox) * 2 + oy] =
-                                    fma_t<Acc>(W[(az * K + ax) * K + ay], v[ox + 2 * H - ax][oy + 2 * H - ay],
-                                               acc[(oz * 2 + ox) * 2 + oy]);
+                                acc[(oz * 2 + ox) * 2 + oy] = fma_t<Acc>(W[(az * K + ax) * K + ay],
+                                                                         r[SH + oy + 2 * H - ay],
+                                                                         acc[(oz * 2 + ox) * 2 + oy]);
+                    }
+                }
             }
-        }
     }
 }
 
@@ -571,6 +572,59 @@ template <typename Acc, int H, int BX, int BY, int PADY>
 __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz, int qx, int qy, Acc (&acc)[8]) {
     apply_block_pairs<Acc, H, BX, BY, PADY>(
         [S](int c) { return *reinterpret_cast<const float2*>(S + c); }, W, qz, qx, qy, acc);
+}
+
+// FAST, rank-1 stencil (w = fz (x) fx (x) fy): the same 8 outputs in three
+// passes -- y per neighbourhood row, then x, then z -- 2x fewer FMAs than the
+// dense 5^3 taps.  Tolerance-matched like every FAST path (the sums are
+// reassociated), never used for EXACT.
+template <int H, int BX, int BY, int PADY>
+__device__ __forceinline__ void apply_block_sep(const float* S, const float* f, int qz, int qx, int qy,
+                                                float (&acc)[8]) {
+    constexpr int K = 2 * H + 1, N = 2 + 2 * H, NP = N / 2;
+    static_assert((PADY - H) % 2 == 0, "aligned pair loads");
+    const float* fz = f;
+    const float* fx = f + K;
+    const float* fy = f + 2 * K;
+    const int base = ((2 * qz) * BX + 2 * qx) * BY + 2 * qy + PADY - H;
+    float2 o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int nz = 0; nz < N; ++nz) {
+        float2 u[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+#pragma unroll
+        for (int nx = 0; nx < N; ++nx) {
+            float r[N];
+#pragma unroll
+            for (int pp = 0; pp < NP; ++pp) {
+                const float2 t2 = *reinterpret_cast<const float2*>(S + base + (nz * BX + nx) * BY + 2 * pp);
+                r[2 * pp] = t2.x;
+                r[2 * pp + 1] = t2.y;
+            }
+            float2 t = make_float2(0.0f, 0.0f);  // (oy = 0, 1) reads r[oy + 2H - ay]
+#pragma unroll
+            for (int ay = 0; ay < K; ++ay)
+                t = ffma2(make_float2(fy[ay], fy[ay]), make_float2(r[2 * H - ay], r[2 * H + 1 - ay]), t);
+#pragma unroll
+            for (int ox = 0; ox < 2; ++ox) {
+                const int ax = ox + 2 * H - nx;
+                if (ax >= 0 && ax < K) u[ox] = ffma2(make_float2(fx[ax], fx[ax]), t, u[ox]);
+            }
+        }
+#pragma unroll
+        for (int oz = 0; oz < 2; ++oz) {
+            const int az = oz + 2 * H - nz;
+            if (az < 0 || az >= K) continue;
+#pragma unroll
+            for (int ox = 0; ox < 2; ++ox) o[oz * 2 + ox] = ffma2(make_float2(fz[az], fz[az]), u[ox], o[oz * 2 + ox]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        acc[2 * i] = o[i].x;
+        acc[2 * i + 1] = o[i].y;
+    }
 }
 
 // The block's (up to 8) outputs through the epilogue, batched: all indices
@@ -722,6 +776,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __shared__ __align__(16) uint8_t omap[kTZ * kTX * kTY];
     __shared__ uint32_t orow[kTZ * kTX];
     __shared__ Acc W[KW];
+    __shared__ float SF[3 * K];  // FAST 5^3, rank-1 stencil: its factors (as k_conv_map)
     __shared__ uint8_t blist[kBlocks];
     __shared__ int nreg;
     __shared__ Region<float> reg[kMaxRegions];
@@ -750,6 +805,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     const int tree = (l >= a.tree_lmin && l <= a.tree_lmax) ? 1 : 0;
 
     // ---- init: weights, output map, (holes only) zeroed box, source table
+    constexpr bool kSepOk = H == 2 && sizeof(Acc) == 4 && !MAP;
+    const bool sep = kSepOk && a.sep[s] != nullptr;
+    if (kSepOk && sep && tid < 3 * K) SF[tid] = a.sep[s][tid];
     for (int i = tid; i < KW; i += kTileThreads)
         W[i] = sizeof(Acc) == 8 ? static_cast<Acc>(a.wd[a.woff[s] + i]) : static_cast<Acc>(a.wf[a.woff[s] + i]);
     {
@@ -1034,7 +1092,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
         Acc acc[8];
-        apply_block<Acc, H, B::BX, B::BY, kPadY>(S, W, qz, qx, qy, acc);
+        if constexpr (kSepOk) {
+            if (sep)
+                apply_block_sep<H, B::BX, B::BY, kPadY>(S, SF, qz, qx, qy, acc);
+            else
+                apply_block<Acc, H, B::BX, B::BY, kPadY>(S, W, qz, qx, qy, acc);
+        } else {
+            apply_block<Acc, H, B::BX, B::BY, kPadY>(S, W, qz, qx, qy, acc);
+        }
         const uint8_t* o = omap + ((2 * qz) * kTX + 2 * qx) * kTY + 2 * qy;
 #pragma unroll
         for (int oz = 0; oz < 2; ++oz)
@@ -1054,7 +1119,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
 // each code's value, then the same block-compacted apply as k_conv_tile.
 // Results are bit-identical to k_conv_tile's (same box contents, same taps).
 template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 : 6) : (H == 2 ? 5 : 8))
+__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H == 2 ? 5 : 8))
     k_conv_map(const __grid_constant__ TileLaunch a) {
     using M = MapBox<H>;
     constexpr int K = 2 * H + 1, KW = K * K * K;
@@ -1069,8 +1134,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     float* F = reinterpret_cast<float*>(Mb + (kInPlace ? M::HDR + M::NC : M::REC));
     __shared__ __align__(8) uint64_t mbar;
     __shared__ Acc W[KW];
+    __shared__ float SF[3 * K];  // FAST 5^3, rank-1 stencil: its factors
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
+    constexpr bool kSepOk = H == 2 && sizeof(Acc) == 4;
+    const bool sep = kSepOk && a.sep[s] != nullptr;
+    if (kSepOk && sep && tid < 3 * K) SF[tid] = a.sep[s][tid];
     const int l = a.lvl[s];
     const uint32_t tix = a.tile_base + blockIdx.x;
     const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
@@ -1160,7 +1229,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
         Acc acc[8];
         if constexpr (kBox) {
-            apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+            if constexpr (kSepOk) {
+                if (sep)
+                    apply_block_sep<H, M::BX, M::BY, H>(S, SF, qz, qx, qy, acc);
+                else
+                    apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+            } else {
+                apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+            }
         } else {  // box cells straight from their codes: no box is materialised
             apply_block_pairs<Acc, H, M::BX, M::BY, H>(
                 [Mb](int c) {  // codes are byte offsets into F, which sits at a fixed offset
@@ -1636,6 +1712,8 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
                 if (first < 0) first = l;
                 total += c;
                 b.woff[b.n_levels] = pyr->off[l - pyr->l_min];
+                b.sep[b.n_levels] = pyr->sep_off[l - pyr->l_min] >= 0 ? pyr->sep_dev + pyr->sep_off[l - pyr->l_min]
+                                                                      : nullptr;
                 set_level(b, L, l, total);
                 if (split) {
                     ++l;

@@ -184,6 +184,12 @@ struct aprgpu_pyramid {
     std::vector<uint64_t> off;             // per level offset into w_host
     float* w_dev = nullptr;                // device copy (float)
     double* wd_dev = nullptr;              // device copy (double)
+    // rank-1 (separable) levels: float factors fz[kz], fx[kx], fy[ky] with
+    // w == fz (x) fx (x) fy to within 5e-7 relative per weight (a Gaussian and
+    // its restrictions); offset into sep_dev per level, or -1.  Only the FAST
+    // 5^3 apply uses them (tolerance-matched; EXACT keeps the weights).
+    std::vector<int64_t> sep_off;
+    float* sep_dev = nullptr;
 };
 
 namespace aprgpu {
