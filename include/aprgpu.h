@@ -290,6 +290,17 @@ int aprgpu_generate_spheres(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, 
  * leaf access + interior access + sampled particle values (aprgpu_apr_values). */
 int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny, double rel_error, int ptr_kind,
                      aprgpu_apr** out);
+/* build_apr (build.hpp:290-312) with any BuildParams (apr.hpp:16-33), on the
+ * device: gradient_magnitude central differences or Sobel (:42-75),
+ * smoothing_passes 3^3 box passes (:22-38, :298), local_scale constant or
+ * local range with its box smoothing and floor (:80-108), level_function
+ * (:113-129) with the constant-sigma safety level, then solve_levels,
+ * init_tree_structure and sample_particles -- structure and values
+ * bit-identical to the reference (a reference compiled with
+ * -ffp-contract=off).  aprgpu_build_apr is this with
+ * SigmaPolicy::constant(intensity_range(volume)) and the other defaults. */
+int aprgpu_build_apr_params(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny,
+                            const aprgpu_build_params* params, int ptr_kind, aprgpu_apr** out);
 /* The C4 tiler: a power-of-two cube APR tiled (tz, tx, ty) times into a new
  * APR built directly in the device layout (structure + interior structure),
  * and the matching tiling of particle values (device pointers; big_values

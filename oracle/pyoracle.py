@@ -383,6 +383,9 @@ class Ref:
                                            C.c_double, C.c_uint64, vp]
         L.ref_build_apr.restype = vp
         L.ref_build_apr.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int]
+        L.ref_build_apr_params.restype = vp
+        L.ref_build_apr_params.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_int,
+                                           C.c_double, C.c_int, C.c_int, C.c_int]
         L.ref_sample_particles.argtypes = [vp, vp, vp]
         L.ref_apr_free.argtypes = [vp]
         L.ref_apr_info.argtypes = [vp, C.c_int, vp]
@@ -475,6 +478,17 @@ class Ref:
     def build_apr(self, vol: np.ndarray, rel_error=0.1, threads=0) -> RefApr:
         v = np.ascontiguousarray(vol, np.float32)
         h = self.L.ref_build_apr(v.ctypes.data, v.shape[0], v.shape[1], v.shape[2], rel_error, threads)
+        if not h:
+            raise RuntimeError(self.err())
+        return RefApr(self, h)
+
+    def build_apr_params(self, vol: np.ndarray, rel_error=0.1, sigma_mode=0, sigma_value=1.0, sigma_window=2,
+                         sigma_floor=0.0, gradient_mode=0, smoothing_passes=0, threads=0) -> RefApr:
+        """build_apr (build.hpp:290-312) with every BuildParams field."""
+        v = np.ascontiguousarray(vol, np.float32)
+        h = self.L.ref_build_apr_params(v.ctypes.data, v.shape[0], v.shape[1], v.shape[2], rel_error, sigma_mode,
+                                        sigma_value, sigma_window, sigma_floor, gradient_mode, smoothing_passes,
+                                        threads)
         if not h:
             raise RuntimeError(self.err())
         return RefApr(self, h)

@@ -194,6 +194,31 @@ REF_API void* ref_build_apr(const float* vol, int nz, int nx, int ny, double rel
     return st == 0 ? out : nullptr;
 }
 
+// build_apr with every BuildParams field (apr.hpp:16-33): sigma_mode 0 constant
+// (sigma_value) / 1 local range (sigma_window, sigma_floor); gradient_mode 0
+// central difference / 1 Sobel; smoothing_passes box passes on the gradient
+REF_API void* ref_build_apr_params(const float* vol, int nz, int nx, int ny, double rel_error, int sigma_mode,
+                                   double sigma_value, int sigma_window, double sigma_floor, int gradient_mode,
+                                   int smoothing_passes, int threads) {
+    RefApr* out = nullptr;
+    int st = guarded([&] {
+        aprkit::PixelVolume v(nz, nx, ny);
+        std::memcpy(v.values.data(), vol, sizeof(float) * v.values.size());
+        aprkit::BuildParams bp;
+        bp.rel_error = rel_error;
+        bp.sigma = sigma_mode == 0 ? aprkit::SigmaPolicy::constant(sigma_value)
+                                   : aprkit::SigmaPolicy::local_range(sigma_window, sigma_floor);
+        bp.gradient = gradient_mode == 0 ? aprkit::GradientMode::CentralDiff : aprkit::GradientMode::Sobel;
+        bp.smoothing_passes = smoothing_passes;
+        auto built = aprkit::build_apr(v, bp, threads);
+        auto h = std::make_unique<RefApr>();
+        h->apr = std::move(built.first);
+        h->values = std::move(built.second);
+        out = h.release();
+    });
+    return st == 0 ? out : nullptr;
+}
+
 // sample_particles (build.hpp:252-284)
 REF_API int ref_sample_particles(void* hp, const float* vol, float* out) {
     return guarded([&] {

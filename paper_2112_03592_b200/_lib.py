@@ -96,6 +96,8 @@ _SIGS = {
     "aprgpu_launch_count": [C.c_void_p, C.POINTER(C.c_uint64)],
     "aprgpu_generate_spheres": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                 C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_void_p, C.c_int],
+    "aprgpu_build_apr_params": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                C.POINTER(C.c_void_p)],
     "aprgpu_build_apr": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                          C.POINTER(C.c_void_p)],
     "aprgpu_apr_values": [C.c_void_p, C.c_void_p, C.c_int],

@@ -1230,6 +1230,12 @@ int aprgpu_generate_spheres(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, 
 
 int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny, double rel_error, int ptr_kind,
                      aprgpu_apr** out) {
+    aprgpu_build_params p{rel_error, -1, 0.0, 0, 0.0, 0, 0};  // (sigma_mode -1: the spheres recipe)
+    return aprgpu_build_apr_params(ctx, volume, nz, nx, ny, &p, ptr_kind, out);
+}
+
+int aprgpu_build_apr_params(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny,
+                            const aprgpu_build_params* params, int ptr_kind, aprgpu_apr** out) {
     aprgpu_apr* apr = nullptr;
     int st = guard([&] {
         need(ctx && volume && out, "null argument");
@@ -1250,7 +1256,10 @@ int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int n
         } else {
             need(ptr_kind == APRGPU_DEVICE, "bad pointer kind");
         }
-        aprgpu::build_apr_device(ctx, vol, nz, nx, ny, rel_error, apr, apr->built_values, ctx->stream);
+        need(params != nullptr, "null build parameters");
+        const bool recipe = params->sigma_mode == -1;
+        aprgpu::build_apr_device(ctx, vol, nz, nx, ny, recipe ? nullptr : params, params->rel_error, apr,
+                                 apr->built_values, ctx->stream);
         APR_CUDA(cudaStreamSynchronize(ctx->stream));  // (the staged volume is freed on return)
         apr->geom_l_max = std::max(apr->leaf.l_max, host_compute_l_max(nz, nx, ny));
         *out = apr;

@@ -121,6 +121,103 @@ __global__ void k_targets(const float* __restrict__ v, int8_t* __restrict__ T, i
     }
 }
 
+// ---- the general BuildParams path (apr.hpp:16-33) -----------------------------
+__device__ __forceinline__ int clampi(int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); }
+
+// gradient_magnitude (build.hpp:42-75): central differences or Sobel, replicate
+// boundary; float result.  Sobel's coefficient products d*s*s are powers of two,
+// so every term is exact and only the (a, b, c)-ordered sums round.
+__global__ void k_gradient(const float* __restrict__ v, float* __restrict__ out, int nz, int nx, int ny, int sobel) {
+    const uint64_t n = static_cast<uint64_t>(nz) * nx * ny;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        int z, x, y;
+        decode(i, nx, ny, z, x, y);
+        auto at = [&](int zz, int xx, int yy) {
+            return v[(static_cast<uint64_t>(zz) * nx + xx) * ny + yy];
+        };
+        double gz = 0.0, gx = 0.0, gy = 0.0;
+        if (!sobel) {
+            gz = __dmul_rn(0.5, static_cast<double>(__fsub_rn(at(clampi(z + 1, nz), x, y), at(clampi(z - 1, nz), x, y))));
+            gx = __dmul_rn(0.5, static_cast<double>(__fsub_rn(at(z, clampi(x + 1, nx), y), at(z, clampi(x - 1, nx), y))));
+            gy = __dmul_rn(0.5, static_cast<double>(__fsub_rn(at(z, x, clampi(y + 1, ny)), at(z, x, clampi(y - 1, ny)))));
+        } else {
+            const double sm[3] = {0.25, 0.5, 0.25}, dd[3] = {-0.5, 0.0, 0.5};
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    for (int c = 0; c < 3; ++c) {
+                        const double val = at(clampi(z + a - 1, nz), clampi(x + b - 1, nx), clampi(y + c - 1, ny));
+                        gz = __dadd_rn(gz, __dmul_rn(__dmul_rn(__dmul_rn(dd[a], sm[b]), sm[c]), val));
+                        gx = __dadd_rn(gx, __dmul_rn(__dmul_rn(__dmul_rn(sm[a], dd[b]), sm[c]), val));
+                        gy = __dadd_rn(gy, __dmul_rn(__dmul_rn(__dmul_rn(sm[a], sm[b]), dd[c]), val));
+                    }
+        }
+        const double s2 = __dadd_rn(__dadd_rn(__dmul_rn(gz, gz), __dmul_rn(gx, gx)), __dmul_rn(gy, gy));
+        out[i] = __double2float_rn(__dsqrt_rn(s2));
+    }
+}
+
+// detail::box_smooth (build.hpp:22-38): 3^3 mean, replicate boundary, fp64 sum
+// in (dz, dx, dy) order; floor > 0 also applies local_scale's final
+// max(s, float(floor)) (build.hpp:105).
+__global__ void k_box_smooth(const float* __restrict__ v, float* __restrict__ out, int nz, int nx, int ny,
+                             float floor_value, int use_floor) {
+    const uint64_t n = static_cast<uint64_t>(nz) * nx * ny;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        int z, x, y;
+        decode(i, nx, ny, z, x, y);
+        double acc = 0.0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dx = -1; dx <= 1; ++dx)
+                for (int dy = -1; dy <= 1; ++dy)
+                    acc = __dadd_rn(acc, static_cast<double>(
+                                             v[(static_cast<uint64_t>(clampi(z + dz, nz)) * nx + clampi(x + dx, nx)) * ny +
+                                               clampi(y + dy, ny)]));
+        float r = __double2float_rn(__ddiv_rn(acc, 27.0));
+        if (use_floor) r = fmaxf(r, floor_value);
+        out[i] = r;
+    }
+}
+
+// local_scale's local range (build.hpp:89-103): max - min of the in-domain
+// (2r+1)^3 window, in float
+__global__ void k_local_range(const float* __restrict__ v, float* __restrict__ out, int nz, int nx, int ny, int r) {
+    const uint64_t n = static_cast<uint64_t>(nz) * nx * ny;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        int z, x, y;
+        decode(i, nx, ny, z, x, y);
+        float lo = v[i], hi = lo;
+        for (int zz = max(z - r, 0); zz <= min(z + r, nz - 1); ++zz)
+            for (int xx = max(x - r, 0); xx <= min(x + r, nx - 1); ++xx)
+                for (int yy = max(y - r, 0); yy <= min(y + r, ny - 1); ++yy) {
+                    const float val = v[(static_cast<uint64_t>(zz) * nx + xx) * ny + yy];
+                    lo = fminf(lo, val);
+                    hi = fmaxf(hi, val);
+                }
+        out[i] = __fsub_rn(hi, lo);
+    }
+}
+
+// level_function (build.hpp:113-129) over a gradient field and a sigma field
+// (sigma == null: the constant sigma_c), the constant-sigma safety level
+// (:301-303) when safety, and solve_levels' clamp (:172)
+__global__ void k_levels(const float* __restrict__ grad, const float* __restrict__ sigma, double sigma_c,
+                         int8_t* __restrict__ T, uint64_t n, double E, double omega, int l_min, int l_max, int safety) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double g = grad[i];
+        int lev;
+        if (g <= 0.0) {
+            lev = l_min;
+        } else {
+            const double sg = sigma ? static_cast<double>(sigma[i]) : sigma_c;
+            const double L = __ddiv_rn(__dmul_rn(E, sg), g);
+            const int l = static_cast<int>(ceil(log2(__ddiv_rn(omega, L))));
+            lev = min(max(l, l_min), l_max);
+        }
+        if (safety) lev = min(lev + 1, l_max);
+        T[i] = static_cast<int8_t>(min(max(lev, l_min), l_max));
+    }
+}
+
 struct Grid3 {
     int zd, xd, yd;
     __host__ __device__ uint64_t size() const { return static_cast<uint64_t>(zd) * xd * yd; }
@@ -338,6 +435,13 @@ void generate_spheres_device(aprgpu_ctx* ctx, int nz, int nx, int ny, int count,
 
 void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny, double rel_error, aprgpu_apr* apr,
                       GpuBuf& values_out, cudaStream_t s) {
+    build_apr_device(ctx, vol, nz, nx, ny, nullptr, rel_error, apr, values_out, s);
+}
+
+// params == null: the spheres recipe, SigmaPolicy::constant(intensity_range(v))
+void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny, const aprgpu_build_params* params,
+                      double rel_error, aprgpu_apr* apr, GpuBuf& values_out, cudaStream_t s) {
+    if (params) rel_error = params->rel_error;
     if (nz < 1 || nx < 1 || ny < 1) fail(APRGPU_ERR_RANGE, "build_apr: empty volume");
     if (ny > 65536) fail(APRGPU_ERR_CAPABILITY, "y dimension exceeds the 16-bit index limit");
     const int l_max = compute_l_max(nz, nx, ny);
@@ -361,17 +465,51 @@ void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny,
     APR_CUDA(cudaMemcpyAsync(mm, red.p, sizeof(mm), cudaMemcpyDeviceToHost, s));
     APR_CUDA(cudaStreamSynchronize(s));
     const float range = mm[1] - mm[0];
-    const double floor_value = 1e-3 * std::max(1e-30f, range);
-    const double sigma = static_cast<double>(static_cast<float>(std::max(static_cast<double>(range), floor_value)));
-    apr->params = aprgpu_build_params{rel_error, 0, static_cast<double>(range), 2, 0.0, 0, 0};  // SigmaPolicy::constant(range)
+    const aprgpu_build_params bp =
+        params ? *params : aprgpu_build_params{rel_error, 0, static_cast<double>(range), 2, 0.0, 0, 0};
+    if (bp.sigma_mode != 0 && bp.sigma_mode != 1) fail(APRGPU_ERR_INVALID, "build_apr: bad sigma mode");
+    if (bp.gradient_mode != 0 && bp.gradient_mode != 1) fail(APRGPU_ERR_INVALID, "build_apr: bad gradient mode");
+    if (bp.smoothing_passes < 0 || bp.sigma_window < 0) fail(APRGPU_ERR_RANGE, "build_apr: negative pass count or window");
+    // local_scale (build.hpp:80-108): floor = policy.floor, or 1e-3 x intensity range
+    const double floor_value = bp.sigma_floor > 0.0 ? bp.sigma_floor : 1e-3 * std::max(1e-30f, range);
+    const double sigma = static_cast<double>(static_cast<float>(std::max(bp.sigma_value, floor_value)));
+    apr->params = bp;
     const double omega = static_cast<double>(1u << l_max);
 
     // dense per-level grids
     std::vector<GpuBuf> T(l_max + 1), need(l_max + 1), Gm(l_max + 1);
     T[l_max].ensure(n);
-    k_targets<<<grid_for(ctx, n), 256, 0, s>>>(vol, T[l_max].as<int8_t>(), nz, nx, ny, rel_error, sigma, omega, l_min,
-                                               l_max);
-    count_launch(ctx);
+    if (bp.sigma_mode == 0 && bp.gradient_mode == 0 && bp.smoothing_passes == 0) {
+        // fused: central differences -> constant sigma -> levels
+        k_targets<<<grid_for(ctx, n), 256, 0, s>>>(vol, T[l_max].as<int8_t>(), nz, nx, ny, rel_error, sigma, omega,
+                                                   l_min, l_max);
+        count_launch(ctx);
+    } else {
+        GpuBuf grad, tmp, sig;
+        grad.ensure(4 * n);
+        k_gradient<<<grid_for(ctx, n), 256, 0, s>>>(vol, grad.as<float>(), nz, nx, ny, bp.gradient_mode);
+        count_launch(ctx);
+        for (int pass = 0; pass < bp.smoothing_passes; ++pass) {  // build.hpp:298
+            tmp.ensure(4 * n);
+            k_box_smooth<<<grid_for(ctx, n), 256, 0, s>>>(grad.as<float>(), tmp.as<float>(), nz, nx, ny, 0.0f, 0);
+            count_launch(ctx);
+            std::swap(grad.p, tmp.p);  // (GpuBuf is move-only: swap the owned buffers)
+            std::swap(grad.bytes, tmp.bytes);
+        }
+        if (bp.sigma_mode == 1) {  // local range -> box_smooth -> floor
+            sig.ensure(4 * n);
+            tmp.ensure(4 * n);
+            k_local_range<<<grid_for(ctx, n), 256, 0, s>>>(vol, tmp.as<float>(), nz, nx, ny, bp.sigma_window);
+            k_box_smooth<<<grid_for(ctx, n), 256, 0, s>>>(tmp.as<float>(), sig.as<float>(), nz, nx, ny,
+                                                          static_cast<float>(floor_value), 1);
+            count_launch(ctx, 2);
+        }
+        k_levels<<<grid_for(ctx, n), 256, 0, s>>>(grad.as<float>(), bp.sigma_mode == 1 ? sig.as<float>() : nullptr,
+                                                  sigma, T[l_max].as<int8_t>(), n, rel_error, omega, l_min, l_max,
+                                                  bp.sigma_mode == 0 ? 1 : 0);
+        count_launch(ctx);
+        APR_CUDA(cudaStreamSynchronize(s));  // (the temporaries are freed on scope exit)
+    }
     APR_CUDA(cudaGetLastError());
     for (int l = l_max - 1; l >= l_min; --l) {
         const Grid3 g = gdim(l);

@@ -266,6 +266,8 @@ void generate_spheres_device(aprgpu_ctx* ctx, int nz, int nx, int ny, int count,
                              cudaStream_t s);
 void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny, double rel_error, aprgpu_apr* apr,
                       GpuBuf& values_out, cudaStream_t s);
+void build_apr_device(aprgpu_ctx* ctx, const float* vol, int nz, int nx, int ny, const aprgpu_build_params* params,
+                      double rel_error, aprgpu_apr* apr, GpuBuf& values_out, cudaStream_t s);
 
 // tile.cu
 void tile_apr_device(aprgpu_ctx* ctx, const aprgpu_apr* src, int TZ, int TX, int TY, aprgpu_apr* big,

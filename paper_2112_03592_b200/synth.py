@@ -57,6 +57,28 @@ def build_apr(volume, rel_error: float = 0.1, ctx: Optional[Context] = None) -> 
     return _wrap_built(ctx, h, (nz, nx, ny))
 
 
+def build_apr_params(volume, params, ctx: Optional[Context] = None) -> Tuple[APR, np.ndarray]:
+    """build_apr (build.hpp:290-312) with any BuildParams on the GPU: params is
+    a paper_2112_03592_b200.BuildParams (sigma_mode 0 constant / 1 local range,
+    gradient_mode 0 central difference / 1 Sobel, smoothing_passes).
+    volume: host (nz,nx,ny) float32 array, or a CUDA torch tensor."""
+    ctx = ctx or default_context()
+    p = L.BuildParamsC(float(params.rel_error), int(params.sigma_mode), float(params.sigma_value),
+                       int(params.sigma_window), float(params.sigma_floor), int(params.gradient_mode),
+                       int(params.smoothing_passes))
+    h = C.c_void_p()
+    if hasattr(volume, "data_ptr"):
+        nz, nx, ny = (int(s) for s in volume.shape)
+        L.check(L.lib().aprgpu_build_apr_params(ctx.handle, volume.data_ptr(), nz, nx, ny, C.byref(p), L.DEVICE,
+                                                C.byref(h)))
+    else:
+        v = np.ascontiguousarray(volume, np.float32)
+        nz, nx, ny = v.shape
+        L.check(L.lib().aprgpu_build_apr_params(ctx.handle, v.ctypes.data, nz, nx, ny, C.byref(p), L.HOST,
+                                                C.byref(h)))
+    return _wrap_built(ctx, h, (nz, nx, ny))
+
+
 def build_spheres_apr(n, count: int, rmin: float, rmax: float, blur: float = 2.0, seed: int = 42,
                       rel_error: float = 0.1, ctx: Optional[Context] = None) -> Tuple[APR, np.ndarray]:
     """generate_spheres -> build_apr entirely on the device (the BASELINE.md

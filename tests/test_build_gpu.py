@@ -54,3 +54,32 @@ def test_built_apr_convolves_like_oracle():
     levels = [((s.kz, s.kx, s.ky), s.weights) for s in pyr.stencils]
     exp = O.convolve(apr.access, apr.tree_access, vals, tv, levels, apr.access.l_min, 1)
     assert np.array_equal(G.bits(out), G.bits(exp))
+
+
+PARAMS = [  # (sigma_mode, sigma_value, sigma_window, sigma_floor, gradient_mode, smoothing_passes)
+    (0, 250.0, 2, 0.0, 1, 0),    # Sobel
+    (0, 250.0, 2, 0.0, 0, 2),    # two box passes on the gradient
+    (1, 1.0, 2, 0.0, 0, 0),      # local range sigma, default floor
+    (1, 1.0, 1, 5.0, 1, 1),      # local range r=1, explicit floor, Sobel, one pass
+    (0, 1e-9, 2, 40.0, 0, 0),    # constant below the floor
+]
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("params", PARAMS)
+@pytest.mark.parametrize("dims,seed", [((40, 33, 57), 3), ((64, 64, 64), 11), ((9, 17, 6), 5)])
+def test_build_apr_params_vs_live_reference(params, dims, seed):
+    """build_apr with every BuildParams option (build.hpp:290-312): Sobel,
+    smoothing passes, local-range sigma with its box pass and floor -- structure
+    and sampled values bit-identical to the unmodified reference."""
+    sm, sv, sw, sf, gm, sp = params
+    R = Ref()
+    vol = R.generate_spheres(dims, 5, 2.0, 8.0, 1.5, 20.0, seed)  # with noise: gradients everywhere
+    r = R.build_apr_params(vol, 0.1, sm, sv, sw, sf, gm, sp)
+    apr, vals = synth.build_apr_params(vol, P.aprkit.BuildParams(0.1, sm, sv, sw, sf, gm, sp))
+    ra = r.leaf
+    for f in ("y_idx", "xz_end"):
+        assert np.array_equal(getattr(apr.access, f), getattr(ra, f)), f
+    assert np.array_equal(apr.access.level_offset[ra.l_min:], ra.level_offset[ra.l_min:])
+    assert np.array_equal(apr.tree_access.y_idx, r.tree.y_idx)
+    assert np.array_equal(G.bits(vals), G.bits(r.values()))
