@@ -1432,11 +1432,14 @@ void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s
     static OncePerDevice attr;
     attr([] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        // 3^3 EXACT (6 CTAs/SM, register-bound): a 132 KB carveout leaves the
-        // gathers more L1 (measured 0.188 -> 0.186 ms on C3; FAST's default
-        // carveout is already its best)
-        if (sizeof(Acc) == 8 && H == 1)
-            APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributePreferredSharedMemoryCarveout, 58));
+        // 3^3 EXACT (8 CTAs/SM by registers, 7 by shared memory): a 164 KB
+        // carveout leaves the gathers L1 (A/B on C3: 58 % 0.185, 72 % 0.180,
+        // 86 % 0.184 ms); FAST and 5^3 are best at the default
+        int carve = sizeof(Acc) == 8 && H == 1 ? 72 : -1;
+        if (const char* e = std::getenv(sizeof(Acc) == 8 ? "APRGPU_CARVEOUT_EXACT" : "APRGPU_CARVEOUT_FAST"))
+            carve = std::atoi(e);  // (A/B experiments)
+        if (carve >= 0)
+            APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     });
     k_conv_map<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
     count_launch(ctx);
