@@ -92,6 +92,10 @@ struct TileLaunch {
     uint32_t* flat;                   // per H flattened source lists (DevAccess::tile_flat)
     const uint32_t* flat_off;         // n_tiles + 1 offsets into flat
     int* map_overflow;                // set by the build when a tile has > MapBox::NC sources
+    int* map_maxg;                    // the build's largest per-tile chunk count (atomicMax)
+    uint32_t n_leaf, n_tree;          // value-array lengths (a tail chunk copies only valid elements)
+    int map_ng;                       // k_conv_map: largest chunk count of the launch's tiles
+    int aligned16;                    // both value arrays 16-byte aligned (else 4-byte copies)
 };
 
 struct Geo {
@@ -123,7 +127,18 @@ struct Box {
 // cell has one source, so a tile has at most NC sources (the build checks; a
 // malformed APR's overlapping sources can exceed it, and its levels then
 // reconstruct).
-constexpr int kFlat0 = 4;  // F[0 .. 3]: the zero (and 16-byte alignment of the copied list)
+constexpr int kFlat0 = 4;  // F[0 .. 3]: the zero (and 16-byte alignment of the staged values)
+// The staged source list is stored in aligned 16-byte CHUNKS: every source run
+// of the tile (a contiguous particle or node range starting at particle b) is
+// placed in F at a fresh 4-slot boundary plus b mod 4 and covers whole chunks,
+// so each chunk is ONE 16-byte copy whose source (4 particles from b - b mod 4
+// on) is 16-byte aligned too; the few extra particles it brings land in
+// padding slots no code points at.  One u32 per chunk: its first particle
+// (bit 31: interior node, bit 30: the array's tail chunk -- only its valid
+// elements are copied).  A tile's chunk count is padded to 4 (16-byte bulk
+// copies of the list).
+constexpr uint32_t kChunkTree = 1u << 31, kChunkTail = 1u << 30, kChunkIdx = kChunkTail - 1;
+constexpr int kMaxChunks = 4000;  // 16-bit byte offsets into F: 4 * (kFlat0 + 4 * chunks) < 65536
 template <int H>
 struct MapBox {
     static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * H;
@@ -720,6 +735,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {  // (16-byte aligned both sides)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Ordered compaction of the tile's 2x2x2 output blocks (block-id order, so a
@@ -787,6 +805,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __shared__ uint16_t rslot[kRuns];  // run -> source-row slot
     __shared__ int8_t rorid[kRuns];    // run -> inner output row of the tile (-1: none)
     __shared__ int roff[kRuns + 1];    // flattened offsets; roff[kRuns] = total
+    __shared__ uint16_t rpad[MAP ? kRuns + 1 : 1];  // MAP: each run's first F slot (whole 16-byte chunks)
     __shared__ int wsum[kTileThreads / 32];
     __shared__ int wcnt[2 * kTileThreads / 32];
     __shared__ __align__(16) uint16_t rid[kMaxFlat];  // run of each flattened particle (current chunk)
@@ -837,6 +856,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                 const uint2 e = __ldg(a.runs + run0 + j);
                 const int t = static_cast<int>(e.y & 0xffff);
                 n = static_cast<int>(e.y >> 16);
+                if (MAP) n |= static_cast<int>(((e.x & 3u) + n + 3) & ~3u) << 16;  // (and its F slots, one scan)
                 RowJob J;
                 resolve_row<H, false>(a, G, T, t, J);  // geometry only
                 const uint32_t rbase = static_cast<uint32_t>(J.r00 + G.by0);
@@ -866,10 +886,15 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         for (int w = 0; w < warp; ++w) base += wsum[w];
 #pragma unroll
         for (int k = 0; k < kRuns / kTileThreads; ++k) {
-            roff[kRuns / kTileThreads * tid + k] = base;
+            const int j = kRuns / kTileThreads * tid + k;
+            roff[j] = MAP ? base & 0xffff : base;
+            if (MAP) rpad[j] = static_cast<uint16_t>(base >> 16);
             base += cnt[k];
         }
-        if (tid == kTileThreads - 1) roff[kRuns] = base;
+        if (tid == kTileThreads - 1) {
+            roff[kRuns] = MAP ? base & 0xffff : base;
+            if (MAP) rpad[kRuns] = static_cast<uint16_t>(base >> 16);
+        }
     }
     __syncthreads();
 
@@ -885,9 +910,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
         const uint32_t gi = rsrc[t] + static_cast<uint32_t>(p - roff[t]);
         const int yy = __ldg((is_tree ? a.tree.y : a.leaf.y) + gi);
         float v;
-        if constexpr (MAP) {
-            if (p < MapBox<H>::NC) a.flat[flat0 + p] = gi;
-            v = __uint_as_float(static_cast<uint32_t>(4 * (kFlat0 + p)));  // byte offset into F
+        if constexpr (MAP) {  // byte offset into F of the source's slot (its run's chunks, phase b mod 4)
+            v = __uint_as_float(static_cast<uint32_t>(4 * (kFlat0 + rpad[t] + (rsrc[t] & 3u) + (p - roff[t]))));
         } else {
             v = __ldg((is_tree ? a.tval : a.val) + gi);
         }
@@ -1013,7 +1037,20 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     if constexpr (MAP) {
         using M = MapBox<H>;
         uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
-        if (tid == 0 && roff[nruns] > M::NC) atomicOr(a.map_overflow, 1);
+        const int nchunks = ((rpad[nruns] >> 2) + 3) & ~3;  // (== k_tile_nflat)
+        if (tid == 0) {
+            if (roff[nruns] > M::NC || nchunks > kMaxChunks) atomicOr(a.map_overflow, 1);
+            atomicMax(a.map_maxg, nchunks);
+        }
+        if (nchunks <= kMaxChunks)  // the chunk list: one u32 per 16-byte chunk of every run
+            for (int t = tid; t < nruns; t += kTileThreads) {
+                const bool tr = (rinfo[t] >> 5) & 1u;
+                const uint32_t b0 = rsrc[t] & ~3u, lim = tr ? a.n_tree : a.n_leaf;
+                for (int c = rpad[t] >> 2; c < rpad[t + 1] >> 2; ++c) {
+                    const uint32_t first = b0 + 4u * (c - (rpad[t] >> 2));
+                    a.flat[flat0 + c] = first | (tr ? kChunkTree : 0u) | (first + 4 > lim ? kChunkTail : 0u);
+                }
+            }
         auto code = [&](int c) -> uint32_t {
             const int r = c / M::BY;
             return __float_as_uint(S[r * B::BY + (c - r * M::BY) + (kPadY - H)]);
@@ -1031,10 +1068,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
             rec[M::MASK0 + tid] = m;
             rec[M::MASK0 + kTZ * kTX + tid] = m ? orow[tid] + first : 0u;
         }
-        if (tid == 0) {  // runs are in row-slot order: interior rows come last
-            int j = 0;
-            while (j < nruns && !((rinfo[j] >> 5) & 1u)) ++j;
-            rec[M::W_NLEAF] = static_cast<uint32_t>(roff[j]);
+        if (tid == 0) {
+            rec[M::W_NLEAF] = static_cast<uint32_t>(nchunks);
             // the active 2x2x2 blocks, dealt round-robin over their bank keys so
             // that a warp's 32 blocks start on as many distinct banks as possible
             // (every tap load of the apply shifts all lanes alike)
@@ -1146,33 +1181,44 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 :
     const RowRange rr = slab_rows(a, l, z0);
     if (rr.lo >= rr.hi) return;  // slab decomposition: no row of this tile is in the slab
     const uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
-    // the record and the flattened source list stream in by two bulk copies; the
+    // the record and the tile's chunk list stream in by two bulk copies; the
     // record's is issued before the list's extent is known (its bytes are
     // expected without an arrival; the one arrival comes with the list's)
-    uint32_t* Fi = reinterpret_cast<uint32_t*>(F + kFlat0);
+    const int nf = kFlat0 + 4 * a.map_ng;  // F floats of this launch
+    // the staged chunk list: after F -- or, for EXACT 5^3, inside the box S it
+    // precedes (S is written only after the gather)
+    constexpr bool kListInBox = H == 2 && !kInPlace;
+    uint32_t* Gs = reinterpret_cast<uint32_t*>(F + nf);
     if (tid == 0) {
         mbar_init(&mbar, 1);
         asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(M::REC * 4) : "memory");
         bulk_copy(Mb, rec, M::REC * 4, &mbar);
     }
-    const uint32_t f0 = __ldg(a.flat_off + tix), nflat = __ldg(a.flat_off + tix + 1) - f0;
+    const uint32_t f0 = __ldg(a.flat_off + tix), nchunk = __ldg(a.flat_off + tix + 1) - f0;
     if (tid == 0) {
-        mbar_expect(&mbar, nflat * 4);  // (arrive.expect_tx)
-        if (nflat) bulk_copy(Fi, a.flat + f0, nflat * 4, &mbar);
+        mbar_expect(&mbar, nchunk * 4);  // (arrive.expect_tx)
+        if (nchunk) bulk_copy(Gs, a.flat + f0, nchunk * 4, &mbar);
     }
     if (tid < kFlat0) F[tid] = 0.0f;
     for (int i = tid; i < KW; i += kTileThreads)
         W[i] = sizeof(Acc) == 8 ? static_cast<Acc>(a.wd[a.woff[s] + i]) : static_cast<Acc>(a.wf[a.woff[s] + i]);
     __syncthreads();  // (the barrier's init is visible)
     mbar_wait(&mbar, 0);
-    // every source value copied once, in place over its list entry (entry q is
-    // read and overwritten by the same thread); a warp's entries are mostly
-    // consecutive particles
-    {
-        const uint32_t nleaf = Mb[M::W_NLEAF];
-        uint32_t q = tid;
-        for (; q < nleaf; q += kTileThreads) cp_async4(Fi + q, a.val + Fi[q]);
-        for (; q < nflat; q += kTileThreads) cp_async4(Fi + q, a.tval + Fi[q]);
+    // every source value copied once: one 16-byte copy per chunk (a warp's
+    // chunks are mostly consecutive 16-byte pieces of one run: coalesced);
+    // the array's tail chunk copies only its valid elements
+    for (uint32_t c = tid; c < nchunk; c += kTileThreads) {
+        const uint32_t e = Gs[c];
+        const float* src = ((e & kChunkTree) ? a.tval : a.val) + (e & kChunkIdx);
+        float* dst = F + kFlat0 + 4 * c;
+        if (!(e & kChunkTail) && a.aligned16) {
+            cp_async16(dst, src);
+        } else {
+            const uint32_t lim = (e & kChunkTree) ? a.n_tree : a.n_leaf;
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                if ((e & kChunkIdx) + k < lim) cp_async4(dst + k, src + k);
+        }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -1184,7 +1230,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 :
     // codes and values read before its writes, never clobber a code still to
     // be read -- so the box needs no storage of its own beyond the codes'.
     constexpr bool kBox = H == 2;
-    float* S = kInPlace ? reinterpret_cast<float*>(Mb + M::HDR) : F + M::NF;  // (kBox: NC floats)
+    float* S = kInPlace ? reinterpret_cast<float*>(Mb + M::HDR) : F + nf + (kListInBox ? 0 : a.map_ng);  // (NC floats)
     if constexpr (kBox) {
         const uint4* C4 = reinterpret_cast<const uint4*>(Mb + M::CODE0);
         float4* S4 = reinterpret_cast<float4*>(S);
@@ -1275,6 +1321,8 @@ TileLaunch base_launch(const aprgpu_apr* apr) {
     a.tree = Tr.view();
     a.tree_lmin = Tr.n_particles ? Tr.l_min : 1;
     a.tree_lmax = Tr.n_particles ? Tr.l_max : 0;
+    a.n_leaf = static_cast<uint32_t>(L.n_particles);
+    a.n_tree = static_cast<uint32_t>(Tr.n_particles);
     return a;
 }
 
@@ -1368,14 +1416,14 @@ void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
     publish_ptr(L.tile_runs[H - 1], runs);  // (tile_run_off is read only after tile_runs)
 }
 
-// per tile: its flattened source count (sum of its run lengths), padded to 4
+// per tile: its chunk count (k_conv_tile's map mode writes the chunks)
 __global__ void k_tile_nflat(const uint32_t* __restrict__ run_off, const uint2* __restrict__ runs, uint64_t n,
                              uint32_t* __restrict__ counts) {
     for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n;
          t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        uint32_t c = 0;
-        for (uint32_t j = run_off[t]; j < run_off[t + 1]; ++j) c += runs[j].y >> 16;
-        counts[t] = (c + 3) & ~3u;
+        uint32_t c = 0;  // F slots: every run covers whole 16-byte chunks from its first particle's phase
+        for (uint32_t j = run_off[t]; j < run_off[t + 1]; ++j) c += ((runs[j].x & 3u) + (runs[j].y >> 16) + 3) & ~3u;
+        counts[t] = ((c >> 2) + 3) & ~3u;  // chunks, padded to 4 (16-byte bulk copies of the list)
     }
 }
 
@@ -1427,11 +1475,16 @@ void launch_tiles(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t
 
 template <typename Acc, int H>
 void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s) {
-    constexpr int bytes = (H == 2 && sizeof(Acc) == 4 ? MapBox<H>::HDR + MapBox<H>::NC + MapBox<H>::NF
-                                                       : MapBox<H>::REC + MapBox<H>::NF + (H == 2 ? MapBox<H>::NC : 0)) * 4;
+    // [record (FAST 5^3: header + box)][F: kFlat0 + 4 chunks][chunk list][EXACT 5^3: box]
+    using M = MapBox<H>;
+    const int fw = kFlat0 + 5 * a.map_ng;
+    const int bytes = (H == 2 && sizeof(Acc) == 4 ? M::HDR + M::NC + fw
+                       : H == 2                   ? M::REC + fw - a.map_ng + std::max(M::NC, a.map_ng)  // list in the box
+                                                  : M::REC + fw) * 4;
+    if (bytes > 225 * 1024) fail(APRGPU_ERR_CAPABILITY, "gather map exceeds shared memory");
     static OncePerDevice attr;
     attr([] {
-        APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
         // 3^3 EXACT (8 CTAs/SM by registers, 7 by shared memory): a 164 KB
         // carveout leaves the gathers L1 (A/B on C3: 58 % 0.185, 72 % 0.180,
         // 86 % 0.184 ms); FAST and 5^3 are best at the default
@@ -1497,12 +1550,16 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, c
             m.slab_lc = 1 << 20;  // every tile: a map serves every slab
             GpuBuf flag;
             flag.ensure(16);
-            APR_CUDA(cudaMemsetAsync(flag.p, 0, 4, s));
+            APR_CUDA(cudaMemsetAsync(flag.p, 0, 8, s));
             m.map_overflow = flag.as<int>();
+            m.map_maxg = flag.as<int>() + 1;
             launch_tiles<float, H, true>(apr->ctx, m, total, s);
-            int over = 0;
-            APR_CUDA(cudaMemcpyAsync(&over, flag.p, 4, cudaMemcpyDeviceToHost, s));
+            int fl[2] = {0, 0};
+            APR_CUDA(cudaMemcpyAsync(fl, flag.p, 8, cudaMemcpyDeviceToHost, s));
             APR_CUDA(cudaStreamSynchronize(s));
+            const int over = fl[0];
+            for (int i = 0; i < b.n_levels; ++i)
+                L.tile_map_ng[H - 1][b.lvl[i]] = std::max(L.tile_map_ng[H - 1][b.lvl[i]], fl[1]);
             if (over) {  // some tile has too many sources for k_conv_map: reconstruct these levels
                 for (int i = 0; i < b.n_levels; ++i) {
                     if (fresh[i]) cudaFree(fresh[i]);
@@ -1514,9 +1571,14 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, c
                 if (fresh[i]) publish_ptr(L.tile_map[H - 1][pm][b.lvl[i]], fresh[i]);
         }
     }
-    for (int i = 0; i < b.n_levels; ++i) b.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
+    b.map_ng = 0;
+    for (int i = 0; i < b.n_levels; ++i) {
+        b.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
+        b.map_ng = std::max(b.map_ng, L.tile_map_ng[H - 1][b.lvl[i]]);
+    }
     b.flat = L.tile_flat[H - 1];
     b.flat_off = L.tile_flat_off[H - 1];
+    b.aligned16 = ((reinterpret_cast<uintptr_t>(b.val) | reinterpret_cast<uintptr_t>(b.tval)) & 15) == 0;
     return true;
 }
 
