@@ -1309,7 +1309,10 @@ __global__ void k_mark_tiles(const uint32_t* __restrict__ work, uint64_t n_work,
         const int z = static_cast<int>(loc / g.xd), x = static_cast<int>(loc % g.xd);
         const uint64_t base = (static_cast<uint64_t>(z / kTZ) * txd + x / kTX) * tyd;
         const uint32_t b = rb[row], e = rb[row + 1];
-        for (uint32_t i = b + lane; i < e; i += 32) flags[base + y[i] / kTY] = 1;
+        for (uint32_t i = b + lane; i < e; i += 32) {  // (one store per distinct tile of the ascending row)
+            const uint32_t t = y[i] / kTY;
+            if (i == b || y[i - 1] / kTY != t) flags[base + t] = 1;
+        }
     }
 }
 
@@ -1650,18 +1653,26 @@ struct LevelTiles {
     LevelG g[kMaxLevels];
     int txd[kMaxLevels], tyd[kMaxLevels];
     uint64_t fbase[kMaxLevels];  // first flag of each level in the combined flag space
+    uint64_t col0[kMaxLevels];   // first (8 x 8 row) tile column of each level
     int l_min, l_max;
 };
 
-// every non-empty row of every level marks the (8z, 8x, 32y) tiles its particles fall in
+// every non-empty row of every level marks the (8z, 8x, 32y) tiles its
+// particles fall in.  Four rows per warp (8 lanes each) keep four rows' loads
+// in flight (a warp per row is latency-bound on its work -> rb -> y chain);
+// a row's y are ascending, so a lane stores only where the tile changes from
+// its left neighbour (a shuffle, not a reload)
 __global__ void k_mark_tiles_all(const uint32_t* __restrict__ work, const uint64_t* __restrict__ n_work_p,
                                  const __grid_constant__ LevelTiles lt, const uint32_t* __restrict__ rb,
                                  const uint16_t* __restrict__ y, uint8_t* __restrict__ flags) {
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, sub = lane >> 3, sl = lane & 7;
+    const unsigned grp = 0xffu << (8 * sub);
     const uint64_t n_work = *n_work_p;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t w = warp; w < n_work; w += nw) {
+    for (uint64_t w0 = warp * 4; w0 < n_work; w0 += nw * 4) {
+        const uint64_t w = w0 + sub;
+        if (w >= n_work) continue;  // (whole 8-lane groups drop out together)
         const uint32_t row = work[w];
         int l = lt.l_max;
         while (l > lt.l_min && row < lt.g[l].row0) --l;
@@ -1669,7 +1680,15 @@ __global__ void k_mark_tiles_all(const uint32_t* __restrict__ work, const uint64
         const int z = static_cast<int>(loc / lt.g[l].xd), x = static_cast<int>(loc % lt.g[l].xd);
         const uint64_t base = lt.fbase[l] + (static_cast<uint64_t>(z / kTZ) * lt.txd[l] + x / kTX) * lt.tyd[l];
         const uint32_t b = rb[row], e = rb[row + 1];
-        for (uint32_t i = b + lane; i < e; i += 32) flags[base + y[i] / kTY] = 1;
+        uint32_t prev = 0xffffffffu;  // the tile of the particle before this 8-lane chunk
+        for (uint32_t i0 = b; i0 < e; i0 += 8) {
+            const uint32_t i = i0 + sl;
+            const uint32_t t = i < e ? static_cast<uint32_t>(y[i]) / kTY : 0xffffffffu;
+            const uint32_t left = __shfl_up_sync(grp, t, 1, 8);
+            if (i < e && t != (sl ? left : prev)) flags[base + t] = 1;
+            prev = __shfl_sync(grp, t, 7, 8);
+            if (prev == 0xffffffffu) break;
+        }
     }
 }
 
@@ -1722,6 +1741,29 @@ void rebuild_index_device(aprgpu_apr* apr, cudaStream_t s) {
     APR_CUDA(cub::DeviceSelect::Flagged(temp, tb, it, flags, tiles, cnt + 1, static_cast<int64_t>(nflags), s));
     count_launch(apr->ctx, 3);
     APR_CUDA(cudaGetLastError());
+    static const bool verify = [] {  // APRGPU_VERIFY_INDEX=1: check the rebuilt lists against the upload's
+        const char* e = std::getenv("APRGPU_VERIFY_INDEX");
+        return e && e[0] == '1';
+    }();
+    if (verify) {
+        uint64_t c[2];
+        APR_CUDA(cudaMemcpyAsync(c, cnt, 16, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+        const uint64_t nwork = L.work_off[L.l_max + 1], ntiles = L.tile_off[L.l_max + 1];
+        bool ok = c[0] == nwork && c[1] == ntiles;
+        if (ok) {
+            std::vector<uint32_t> w0(nwork), w1(nwork), t0(ntiles), t1v(ntiles);
+            APR_CUDA(cudaMemcpy(w0.data(), L.work, 4 * nwork, cudaMemcpyDeviceToHost));
+            APR_CUDA(cudaMemcpy(w1.data(), work, 4 * nwork, cudaMemcpyDeviceToHost));
+            APR_CUDA(cudaMemcpy(t0.data(), L.tiles, 4 * ntiles, cudaMemcpyDeviceToHost));
+            APR_CUDA(cudaMemcpy(t1v.data(), tiles, 4 * ntiles, cudaMemcpyDeviceToHost));
+            ok = w0 == w1;
+            for (int l = L.l_min; l <= L.l_max && ok; ++l)  // combined flag ids -> per-level tile ids
+                for (uint64_t i = L.tile_off[l]; i < L.tile_off[l + 1] && ok; ++i)
+                    ok = t1v[i] - lt.fbase[l] == t0[i];
+        }
+        if (!ok) fail(APRGPU_ERR_INTEGRITY, "rebuild_index: the rebuilt row / tile lists differ from the upload's");
+    }
 }
 
 // Runs every level whose stencil is an isotropic 3^3 or 5^3 through the tile

@@ -657,7 +657,7 @@ void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, in
             return flat_ok && z_hi < 0 && a.nz % c == 0 && a.nx % c == 0 && a.ny % c == 0;
         };
         const int lo = std::max(lt_lo, T.l_min);
-        if (apr->tree_level_first[lt + 1] - apr->tree_level_first[lt] <= 8192) {
+        if (apr->tree_level_first[lt + 1] - apr->tree_level_first[lt] <= 2048) {  // (<= 2 nodes per thread: latency-bound levels)
             bool all = true;  // this level and every coarser one: one fused launch
             for (int l = lt; l >= lo && all; --l) all = flat_level(l);
             if (all) {

@@ -323,3 +323,19 @@ def test_nonempty_row_index_and_init_tree_front_doors():
         off += n
     t = P.init_tree_structure(apr.access, apr.source_dims)
     assert t.equals(apr.tree_access)
+
+
+@pytest.mark.parametrize("name", ["c1_256", "spheres64", "random_apr_03", "random_apr_09", "dense16"])
+def test_rebuild_index_equals_upload_lists(name, monkeypatch):
+    """aprgpu_rebuild_index (the paper protocol's per-call index step): the
+    non-empty row lists and occupied-tile lists it recomputes equal the ones
+    built at upload (APRGPU_VERIFY_INDEX=1 compares them in the library)."""
+    monkeypatch.setenv("APRGPU_VERIFY_INDEX", "1")
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0]=['tests','.']; import goldens as G; d=G.load(%r); "
+            "a=G.product_apr(d).device(); a.rebuild_index_ptr(0); import torch; torch.cuda.synchronize(); print('ok')"
+            % name)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
