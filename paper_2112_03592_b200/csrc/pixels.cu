@@ -168,30 +168,41 @@ __device__ __forceinline__ void cp_async_4(float* dst, const float* src) {
 }
 
 // Isotropic K^3 (K = 3, 5), streamed along z (2.5-D blocking): a CTA owns a
-// 16 (x) x 64 (y) column of outputs over kZc planes and keeps a ring of K + 2
+// 32 (x) x 64 (y) column of outputs over kZc planes and keeps a ring of K + 2
 // input planes -- the K the current output plane reads and the next two,
 // prefetched with cp.async while the current plane is evaluated (padding
 // applied on load).  Every input plane is read from HBM about once (x / y halo
-// 1.16x, z halo 2H / kZc).  Each thread computes 4 consecutive y outputs of
-// one x from a register window (converted to the accumulator type once per row).
-constexpr int kSx = 16, kSy = 64, kZc = 32;
-template <typename Acc, int K>
+// 1.1x, z halo 2H / kZc).  Lane = x row, warp = a run of 8 consecutive y
+// outputs: a warp's window loads are 16-byte loads from 32 different rows
+// whose stride (kPY = 76 floats, 12 banks) puts every quarter-warp on distinct
+// banks -- conflict-free (lanes along y, 32 bytes apart, were 8-way conflicted).
+// FAST keeps the K^3 weights in registers, EXACT reads them as doubles from
+// shared memory (one broadcast load per tap).  SKIP: some weight is zero and
+// is skipped like the reference (convolve.hpp:86-88) -- which only matters
+// for non-finite inputs; otherwise no per-tap test.
+constexpr int kSx = 32, kSy = 64, kZc = 32, kRY = 8, kPY = 76;
+template <typename Acc, int K, bool SKIP>
 __global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_stream(PixArgs a, int txd, int tyd) {
     constexpr int D = 2;  // prefetch distance (planes)
-    // a plane row: 4 - H unused floats, H left halo, the 64-float interior at a
-    // 16-byte boundary (16-byte copies), H right halo, padded to 16 bytes
-    constexpr int H = K / 2, PX = kSx + 2 * H, OFF = 4 - H, PY = kSy + 8, PLANE = PX * PY, RY = 4, NW = RY + K - 1,
-                  NS = K + D;
-    static_assert(kSx * (kSy / RY) == kPixThreads, "one output run per thread");
+    // a plane row: [4 - H unused][H halo][64 interior at a 16-byte boundary][H halo], kPY floats
+    constexpr int H = K / 2, PX = kSx + 2 * H, OFF = 4 - H, PY = kPY, PLANE = PX * PY, RY = kRY,
+                  NS = K + D, KW = K * K * K;
+    static_assert(kSx * (kSy / RY) == kPixThreads && kSx == 32, "lane = x row, warp = y run");
+    static_assert(PY >= kSy + 8 && PY % 4 == 0, "16-byte rows");
     extern __shared__ __align__(16) float ring[];  // NS planes
-    __shared__ float W[K * K * K];
+    __shared__ Acc Ws[KW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ty = blockIdx.x % tyd, t2 = blockIdx.x / tyd;
     const int tx = t2 % txd, tzc = t2 / txd;
     const int x0 = tx * kSx, y0 = ty * kSy, zc0 = tzc * kZc, zc1 = min(zc0 + kZc, a.nz);
-    for (int i = tid; i < K * K * K; i += kPixThreads) W[i] = a.w[i];
+    for (int i = tid; i < KW; i += kPixThreads) Ws[i] = static_cast<Acc>(a.w[i]);
+    float wr[sizeof(Acc) == 4 ? KW : 1];  // FAST: the weights in registers
+    if constexpr (sizeof(Acc) == 4) {
+#pragma unroll
+        for (int i = 0; i < KW; ++i) wr[i] = __ldg(a.w + i);
+    }
     auto slot = [&](int z) { return ring + (((z % NS) + NS) % NS) * PLANE; };
-    const bool vec = (a.ny & 3) == 0;  // rows 16-byte aligned
+    const bool vec = (a.ny & 3) == 0 && y0 + kSy <= a.ny;  // 16-byte aligned, whole interior in range
     // input plane z into its slot (reflected / zero outside the volume), asynchronously
     auto load = [&](int z) {
         float* pl = slot(z);
@@ -205,20 +216,23 @@ __global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_stream(PixArgs 
                 continue;
             }
             const float* src = a.in + (static_cast<size_t>(zr) * a.nx + reflect_p(x, a.nx)) * a.ny;
-            if (lane < kSy / 4 && vec && y0 + kSy <= a.ny) {  // the interior: 16-byte copies
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                 static_cast<unsigned>(__cvta_generic_to_shared(dst + H + 4 * lane))),
-                             "l"(src + y0 + 4 * lane)
-                             : "memory");
-            } else if (lane < kSy / 4) {  // (ragged or unaligned rows)
-                for (int c = H + 4 * lane; c < H + 4 * lane + 4; ++c) {
+            if (vec) {  // the interior: 16-byte copies
+                if (lane < kSy / 4)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     static_cast<unsigned>(__cvta_generic_to_shared(dst + H + 4 * lane))),
+                                 "l"(src + y0 + 4 * lane)
+                                 : "memory");
+            } else {  // (ragged or unaligned rows)
+                for (int c = H + lane; c < H + kSy; c += 32) {
                     const int y = y0 + c - H;
                     if (y < a.ny) cp_async_4(dst + c, src + y);
                     else if (a.pad == APRGPU_PAD_REFLECT) cp_async_4(dst + c, src + reflect_p(y, a.ny));
                     else dst[c] = 0.0f;
                 }
-            } else if (lane < kSy / 4 + 2 * H) {  // the halos
-                const int c = lane - kSy / 4 < H ? lane - kSy / 4 : kSy + (lane - kSy / 4);
+            }
+            if (lane >= 32 - 2 * H) {  // the halos (lanes the interior copies leave idle)
+                const int k = lane - (32 - 2 * H);
+                const int c = k < H ? k : kSy + k;
                 const int y = y0 + c - H;
                 if (y >= 0 && y < a.ny) cp_async_4(dst + c, src + y);
                 else if (a.pad == APRGPU_PAD_REFLECT) cp_async_4(dst + c, src + reflect_p(y, a.ny));
@@ -227,7 +241,7 @@ __global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_stream(PixArgs 
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    const int ox = tid / (kSy / RY), oy = (tid % (kSy / RY)) * RY;  // this thread's outputs
+    const int ox = lane, oy = warp * RY;  // this thread's outputs: row ox, y oy .. oy + 7
     // planes zc0 - H .. zc0 + H + D - 1 in flight; then one group per plane
     for (int z = zc0 - H; z < zc0 + H + D; ++z) {
         if (z < zc1 + H) load(z);
@@ -248,21 +262,25 @@ __global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_stream(PixArgs 
                 const float* plz = slot(o + H - az);  // input plane read with weight plane az
 #pragma unroll
                 for (int ax = 0; ax < K; ++ax) {
-                    const float* row = plz + (ox + 2 * H - ax) * PY + OFF + oy;
-                    // pairs from the even index at or below the window (8-byte loads)
-                    constexpr int SH = OFF & 1, NL = (NW + SH + 1) & ~1;
+                    // outputs oy + j read cells c = oy + j + 2H - ay, c in [oy, oy + 7 + 2H]: the
+                    // window from the 16-byte boundary at or below row + OFF + oy
+                    const float* row = plz + (ox + 2 * H - ax) * PY;
+                    constexpr int SH = OFF & 3, NL = (SH + RY + 2 * H + 3) & ~3;
                     Acc win[NL];  // (converted once per row, not per tap)
 #pragma unroll
-                    for (int i = 0; i < NL; i += 2) {
-                        const float2 t = *reinterpret_cast<const float2*>(row - SH + i);
+                    for (int i = 0; i < NL; i += 4) {
+                        const float4 t = *reinterpret_cast<const float4*>(row + (OFF - SH) + oy + i);
                         win[i] = static_cast<Acc>(t.x);
                         win[i + 1] = static_cast<Acc>(t.y);
+                        win[i + 2] = static_cast<Acc>(t.z);
+                        win[i + 3] = static_cast<Acc>(t.w);
                     }
 #pragma unroll
                     for (int ay = 0; ay < K; ++ay) {
-                        const float wv = W[(az * K + ax) * K + ay];
-                        if (wv == 0.0f) continue;  // (convolve.hpp:86-88)
-                        const Acc wa = static_cast<Acc>(wv);
+                        const int wi = (az * K + ax) * K + ay;
+                        Acc wa;
+                        if constexpr (sizeof(Acc) == 4) wa = wr[wi]; else wa = Ws[wi];
+                        if (SKIP && wa == Acc(0)) continue;  // (convolve.hpp:86-88)
 #pragma unroll
                         for (int j = 0; j < RY; ++j) acc[j] = fma(wa, win[SH + j + 2 * H - ay], acc[j]);
                     }
@@ -288,7 +306,7 @@ __global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_stream(PixArgs 
 }  // namespace
 
 void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w_dev, int kz,
-                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s) {
+                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s, bool any_zero_w) {
     if (kz > kPixMaxK || kx > kPixMaxK || ky > kPixMaxK)
         fail(APRGPU_ERR_CAPABILITY, "convolve_pixels: stencil extent exceeds the supported maximum");
     if (nz <= 0 || nx <= 0 || ny <= 0) return;
@@ -301,22 +319,32 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
         const int sxd = (nx + kSx - 1) / kSx, syd = (ny + kSy - 1) / kSy, szd = (nz + kZc - 1) / kZc;
         const unsigned g = static_cast<unsigned>(static_cast<uint64_t>(szd) * sxd * syd);
         const int h = kz / 2;
-        const int rb = (kz + 2) * (kSx + 2 * h) * (kSy + 8) * static_cast<int>(sizeof(float));
+        const int rb = (kz + 2) * (kSx + 2 * h) * kPY * static_cast<int>(sizeof(float));
         static OncePerDevice sattr;
         sattr([] {
-            const int mx = 7 * (kSx + 4) * (kSy + 8) * static_cast<int>(sizeof(float));
-            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<double, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<double, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<float, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            const int mx = 7 * (kSx + 4) * kPY * static_cast<int>(sizeof(float));
+#define APRGPU_SET_PIX(A, K_, S_) \
+    APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<A, K_, S_>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx))
+            APRGPU_SET_PIX(double, 3, false);
+            APRGPU_SET_PIX(double, 3, true);
+            APRGPU_SET_PIX(float, 3, false);
+            APRGPU_SET_PIX(float, 3, true);
+            APRGPU_SET_PIX(double, 5, false);
+            APRGPU_SET_PIX(double, 5, true);
+            APRGPU_SET_PIX(float, 5, false);
+            APRGPU_SET_PIX(float, 5, true);
+#undef APRGPU_SET_PIX
         });
+        const bool skip = any_zero_w;  // (a zero weight is skipped like the reference)
+#define APRGPU_LAUNCH_PIX(A, K_) \
+    (skip ? k_convolve_pixels_stream<A, K_, true><<<g, kPixThreads, rb, s>>>(a, sxd, syd) \
+          : k_convolve_pixels_stream<A, K_, false><<<g, kPixThreads, rb, s>>>(a, sxd, syd))
         if (kz == 3) {
-            if (ex) k_convolve_pixels_stream<double, 3><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
-            else k_convolve_pixels_stream<float, 3><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
+            if (ex) APRGPU_LAUNCH_PIX(double, 3); else APRGPU_LAUNCH_PIX(float, 3);
         } else {
-            if (ex) k_convolve_pixels_stream<double, 5><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
-            else k_convolve_pixels_stream<float, 5><<<g, kPixThreads, rb, s>>>(a, sxd, syd);
+            if (ex) APRGPU_LAUNCH_PIX(double, 5); else APRGPU_LAUNCH_PIX(float, 5);
         }
+#undef APRGPU_LAUNCH_PIX
         count_launch(ctx);
         APR_CUDA(cudaGetLastError());
         return;
