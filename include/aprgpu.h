@@ -101,6 +101,10 @@ int aprgpu_upload_access(aprgpu_ctx* ctx, const aprgpu_access_desc* leaf, const 
 int aprgpu_apr_free(aprgpu_apr* apr);
 int aprgpu_apr_dims(const aprgpu_apr* apr, int32_t dims_out[3]);
 int aprgpu_access_get_info(const aprgpu_apr* apr, int which, aprgpu_access_info* out);
+/* Resident gather maps of the tile kernel: *built = tile records held over all
+ * (stencil extent, pad mode, level) maps, *n_tiles = the APR's output tiles.  A
+ * z-slab's convolutions build records only for the tiles they compute. */
+int aprgpu_apr_map_tiles(const aprgpu_apr* apr, uint64_t* built, uint64_t* n_tiles);
 /* Downloads an access structure back into the reference layout (bit-exact
  * round trip).  Arrays sized by aprgpu_access_get_info: y_idx[n_particles],
  * xz_end[n_rows], level_offset/z_dim/x_dim/y_dim[l_max+1]. */

@@ -31,7 +31,7 @@ import enum
 import os
 import math
 from dataclasses import dataclass, field
-from typing import List, NamedTuple, Optional, Sequence
+from typing import List, NamedTuple, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -560,6 +560,12 @@ class DeviceApr:
     # device-pointer entry points (stream-ordered; pointers are raw ints) -----
     def fill_tree_ptr(self, leaf_ptr: int, tree_ptr: int, stream: int = 0) -> None:
         L.check(L.lib().aprgpu_fill_tree(self.handle, leaf_ptr, tree_ptr, L.DEVICE, stream or None))
+
+    def map_tiles(self) -> Tuple[int, int]:
+        """(tile records held by the resident gather maps, output tiles of the APR)."""
+        built, total = C.c_uint64(), C.c_uint64()
+        L.check(L.lib().aprgpu_apr_map_tiles(self.handle, C.byref(built), C.byref(total)))
+        return built.value, total.value
 
     def rebuild_index_ptr(self, stream: int = 0) -> None:
         """The paper protocol's per-call index step (aprgpu_rebuild_index)."""

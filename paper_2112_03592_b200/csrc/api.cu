@@ -693,6 +693,21 @@ int aprgpu_access_get_info(const aprgpu_apr* apr, int which, aprgpu_access_info*
     });
 }
 
+int aprgpu_apr_map_tiles(const aprgpu_apr* apr, uint64_t* built, uint64_t* n_tiles) {
+    return guard([&] {
+        need(apr && built && n_tiles, "null argument");
+        std::lock_guard<std::mutex> lk(apr->ctx->mu);
+        const aprgpu::DevAccess& L = apr->leaf;
+        uint64_t b = 0;
+        for (int h = 0; h < 2; ++h)
+            for (int pm = 0; pm < 2; ++pm)
+                for (int l = 0; l < aprgpu::kMaxLevels; ++l)
+                    if (const auto* w = L.tile_map[h][pm][l]) b += w->a1 - w->a0;
+        *built = b;
+        *n_tiles = L.tile_off.empty() ? 0 : L.tile_off.back();
+    });
+}
+
 int aprgpu_download_access(const aprgpu_apr* apr, int which, uint16_t* y_idx, uint64_t* xz_end,
                            uint64_t* level_offset, int32_t* z_dim, int32_t* x_dim, int32_t* y_dim) {
     return guard([&] {

@@ -78,6 +78,9 @@ struct TileLaunch {
     int n_levels;                   // level segments in this launch
     int lvl[kMaxLevels];            // level of each segment
     uint32_t seg_end[kMaxLevels];   // exclusive end (in blocks) of each level segment
+    // per segment: tiles skipped before its first block (a slab's launch covers only the z-range of
+    // tiles it computes), so block b of segment s is tile tile_base + b + seg_shift[s]
+    uint32_t seg_shift[kMaxLevels];
     int tdim[kMaxLevels][3];        // tile grid dims of each segment's level
     uint64_t woff[kMaxLevels];      // weight offset of each segment's level
     const float* wf;
@@ -89,6 +92,7 @@ struct TileLaunch {
     EpiArgs epi;
     int slab_lc, slab_zlo, slab_zhi;  // z-slab restriction (Slab, internal.cuh)
     uint32_t* map[kMaxLevels];        // per segment: gather-map records (k_conv_map), or the build target
+    uint32_t map_base[kMaxLevels];    // per segment: the tile whose record is map[s][0]
     uint32_t* flat;                   // per H flattened source lists (DevAccess::tile_flat)
     const uint32_t* flat_off;         // n_tiles + 1 offsets into flat
     int* map_overflow;                // set by the build when a tile has > MapBox::NC sources
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
     const int l = a.lvl[s];
     const LevelG g = a.leaf.g[l];
-    const uint32_t tix = a.tile_base + blockIdx.x;
+    const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
     const Geo G = make_geo<H>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], g);
     if (l >= a.slab_lc) {  // slab decomposition: only tiles touching this slab's planes
         const int sh = a.leaf.l_max - l;
@@ -1036,7 +1040,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
 
     if constexpr (MAP) {
         using M = MapBox<H>;
-        uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
+        uint32_t* rec = a.map[s] + static_cast<size_t>(tix - a.map_base[s]) * M::REC;
         const int nchunks = ((rpad[nruns] >> 2) + 3) & ~3;  // (== k_tile_nflat)
         if (tid == 0) {
             if (roff[nruns] > M::NC || nchunks > kMaxChunks) atomicOr(a.map_overflow, 1);
@@ -1176,11 +1180,11 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 :
     const bool sep = kSepOk && a.sep[s] != nullptr;
     if (kSepOk && sep && tid < 3 * K) SF[tid] = a.sep[s][tid];
     const int l = a.lvl[s];
-    const uint32_t tix = a.tile_base + blockIdx.x;
+    const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
     const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
     const RowRange rr = slab_rows(a, l, z0);
     if (rr.lo >= rr.hi) return;  // slab decomposition: no row of this tile is in the slab
-    const uint32_t* rec = a.map[s] + static_cast<size_t>(blockIdx.x - (s ? a.seg_end[s - 1] : 0)) * M::REC;
+    const uint32_t* rec = a.map[s] + static_cast<size_t>(tix - a.map_base[s]) * M::REC;
     // the record and the tile's chunk list stream in by two bulk copies; the
     // record's is issued before the list's extent is known (its bytes are
     // expected without an arrival; the one arrival comes with the list's)
@@ -1336,6 +1340,21 @@ void set_level(TileLaunch& a, const DevAccess& L, int l, uint32_t end) {
     a.tdim[s][1] = L.tile_dims[3 * l + 1];
     a.tdim[s][2] = L.tile_dims[3 * l + 2];
     a.seg_end[s] = end;
+}
+
+// The tiles of level l a launch for slab sl computes, as absolute tile
+// indices [first, second): the whole level below the cut, else the tile z-rows
+// that meet the slab's planes (the kernels' own slab test, k_conv_tile)
+std::pair<uint64_t, uint64_t> tile_range(const DevAccess& L, int l, const Slab& sl) {
+    const uint64_t b = L.tile_off[l], e = L.tile_off[l + 1];
+    if (l < sl.lc || e == b) return {b, e};
+    const int sh = L.l_max - l, tzd = L.tile_dims[3 * l];
+    const int64_t zlo = static_cast<int64_t>(sl.z_lo) >> sh;
+    const int64_t zhi = (static_cast<int64_t>(sl.z_hi) + (int64_t(1) << sh) - 1) >> sh;
+    const int t0 = static_cast<int>(std::clamp<int64_t>(zlo / kTZ, 0, tzd));
+    const int t1 = static_cast<int>(std::clamp<int64_t>((zhi + kTZ - 1) / kTZ, t0, tzd));
+    const uint32_t* zf = L.tile_zfirst.data() + L.tile_zfirst_off[l];
+    return {b + zf[t0], b + zf[t1]};
 }
 
 // First use of an APR by the tile path: probe every tile once.
@@ -1509,48 +1528,71 @@ bool maps_enabled() {
 }
 
 // The gather maps of launch b's levels for half-width H and pad mode: built on
-// first use (one map-mode launch of k_conv_tile), kept with the APR.  Returns
-// false -- the caller reconstructs -- when the missing maps would take more
-// than half of the free device memory.
+// first use (one map-mode launch of k_conv_tile), kept with the APR.  A map
+// holds the records of the tiles [a0, a1) of its level: a slab launch (rng:
+// each segment's absolute tile range) builds only the tiles it computes, and
+// a later launch that needs more replaces the window by the hull of both (the
+// old one is kept until the APR is freed: launches in flight may read it).
+// Returns false -- the caller reconstructs -- when the missing maps would take
+// more than half of the free device memory.
 template <int H>
-bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, cudaStream_t s) {
+bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], int pad, cudaStream_t s) {
+    using Win = DevAccess::MapWin;
     DevAccess& L = apr->leaf;
     const int pm = pad == APRGPU_PAD_ZERO ? 1 : 0;
-    auto rec_bytes = [&](int l) { return (L.tile_off[l + 1] - L.tile_off[l]) * MapBox<H>::REC * sizeof(uint32_t); };
     for (int i = 0; i < b.n_levels; ++i)
         if (__atomic_load_n(&L.tile_map_fail[H - 1][pm][b.lvl[i]], __ATOMIC_ACQUIRE)) return false;
-    auto missing = [&] {
-        size_t need = 0;
-        for (int i = 0; i < b.n_levels; ++i)
-            if (!acquire_ptr(L.tile_map[H - 1][pm][b.lvl[i]])) need += rec_bytes(b.lvl[i]);
-        return need;
+    auto covers = [&](int i) {
+        const Win* w = acquire_ptr(L.tile_map[H - 1][pm][b.lvl[i]]);
+        return w && w->a0 <= rng[i][0] && w->a1 >= rng[i][1];
     };
-    if (missing()) {
+    auto all_covered = [&] {
+        for (int i = 0; i < b.n_levels; ++i)
+            if (!covers(i)) return false;
+        return true;
+    };
+    if (!all_covered()) {
         std::lock_guard<std::mutex> lk(apr->ctx->mu);
-        const size_t need = missing();
-        if (need) {
+        // the build launch: one segment per level whose window is missing or too narrow
+        TileLaunch m = b;
+        m.n_levels = 0;
+        uint64_t lo[kMaxLevels], hi[kMaxLevels];
+        uint32_t total = 0;
+        size_t need = 0;
+        for (int i = 0; i < b.n_levels; ++i) {
+            if (covers(i)) continue;
+            const Win* w = L.tile_map[H - 1][pm][b.lvl[i]];
+            const int j = m.n_levels;
+            lo[j] = w ? std::min(w->a0, rng[i][0]) : rng[i][0];
+            hi[j] = w ? std::max(w->a1, rng[i][1]) : rng[i][1];
+            total += static_cast<uint32_t>(hi[j] - lo[j]);
+            need += (hi[j] - lo[j]) * MapBox<H>::REC * sizeof(uint32_t);
+            set_level(m, L, b.lvl[i], total);
+            m.woff[j] = b.woff[i];
+            m.sep[j] = b.sep[i];
+        }
+        if (m.n_levels) {
             size_t free_b = 0, total_b = 0;
             APR_CUDA(cudaMemGetInfo(&free_b, &total_b));
             if (need > free_b / 2) {
-                for (int i = 0; i < b.n_levels; ++i)
-                    __atomic_store_n(&L.tile_map_fail[H - 1][pm][b.lvl[i]], 1, __ATOMIC_RELEASE);
+                for (int j = 0; j < m.n_levels; ++j)
+                    __atomic_store_n(&L.tile_map_fail[H - 1][pm][m.lvl[j]], 1, __ATOMIC_RELEASE);
                 return false;
             }
             ensure_tile_flat<H>(apr, s);
             // built into local buffers, published only after the build kernel
             // has completed and passed the overflow check
             uint32_t* fresh[kMaxLevels] = {};
-            TileLaunch m = b;
-            for (int i = 0; i < b.n_levels; ++i) {
-                m.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
-                if (!m.map[i]) {
-                    APR_CUDA(cudaMalloc(&fresh[i], rec_bytes(b.lvl[i])));
-                    m.map[i] = fresh[i];
-                }
+            m.tile_base = static_cast<uint32_t>(lo[0]);
+            for (int j = 0; j < m.n_levels; ++j) {
+                APR_CUDA(cudaMalloc(&fresh[j], (hi[j] - lo[j]) * MapBox<H>::REC * sizeof(uint32_t) + 16));
+                m.map[j] = fresh[j];
+                m.map_base[j] = static_cast<uint32_t>(lo[j]);
+                m.seg_shift[j] = static_cast<uint32_t>(lo[j] - m.tile_base - (j ? m.seg_end[j - 1] : 0));
             }
             m.flat = L.tile_flat[H - 1];
             m.flat_off = L.tile_flat_off[H - 1];
-            m.slab_lc = 1 << 20;  // every tile: a map serves every slab
+            m.slab_lc = 1 << 20;  // every tile of the windows
             GpuBuf flag;
             flag.ensure(16);
             APR_CUDA(cudaMemsetAsync(flag.p, 0, 8, s));
@@ -1560,23 +1602,27 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, uint32_t total, int pad, c
             int fl[2] = {0, 0};
             APR_CUDA(cudaMemcpyAsync(fl, flag.p, 8, cudaMemcpyDeviceToHost, s));
             APR_CUDA(cudaStreamSynchronize(s));
-            const int over = fl[0];
-            for (int i = 0; i < b.n_levels; ++i)
-                L.tile_map_ng[H - 1][b.lvl[i]] = std::max(L.tile_map_ng[H - 1][b.lvl[i]], fl[1]);
-            if (over) {  // some tile has too many sources for k_conv_map: reconstruct these levels
-                for (int i = 0; i < b.n_levels; ++i) {
-                    if (fresh[i]) cudaFree(fresh[i]);
-                    __atomic_store_n(&L.tile_map_fail[H - 1][pm][b.lvl[i]], 1, __ATOMIC_RELEASE);
+            if (fl[0]) {  // some tile has too many sources for k_conv_map: reconstruct these levels
+                for (int j = 0; j < m.n_levels; ++j) {
+                    cudaFree(fresh[j]);
+                    __atomic_store_n(&L.tile_map_fail[H - 1][pm][m.lvl[j]], 1, __ATOMIC_RELEASE);
                 }
                 return false;
             }
-            for (int i = 0; i < b.n_levels; ++i)
-                if (fresh[i]) publish_ptr(L.tile_map[H - 1][pm][b.lvl[i]], fresh[i]);
+            for (int j = 0; j < m.n_levels; ++j) {
+                const int l = m.lvl[j];
+                L.tile_map_ng[H - 1][l] = std::max(L.tile_map_ng[H - 1][l], fl[1]);
+                Win* old = L.tile_map[H - 1][pm][l];
+                publish_ptr(L.tile_map[H - 1][pm][l], new Win{fresh[j], lo[j], hi[j]});
+                if (old) L.tile_map_retired.push_back(old);
+            }
         }
     }
     b.map_ng = 0;
     for (int i = 0; i < b.n_levels; ++i) {
-        b.map[i] = L.tile_map[H - 1][pm][b.lvl[i]];
+        const Win* w = acquire_ptr(L.tile_map[H - 1][pm][b.lvl[i]]);
+        b.map[i] = w->rec;
+        b.map_base[i] = static_cast<uint32_t>(w->a0);
         b.map_ng = std::max(b.map_ng, L.tile_map_ng[H - 1][b.lvl[i]]);
     }
     b.flat = L.tile_flat[H - 1];
@@ -1635,6 +1681,17 @@ void build_tile_lists(aprgpu_ctx* ctx, DevAccess& a) {
     }
     a.tile_off[a.l_max + 1] = off;
     for (int l = 0; l < a.l_min; ++l) a.tile_off[l] = 0;
+    a.tile_zfirst.clear();
+    a.tile_zfirst_off.assign(a.l_max + 1, 0);
+    for (int l = a.l_min; l <= a.l_max; ++l) {
+        a.tile_zfirst_off[l] = a.tile_zfirst.size();
+        const uint64_t plane = static_cast<uint64_t>(a.tile_dims[3 * l + 1]) * a.tile_dims[3 * l + 2];
+        const std::vector<uint32_t>& t = per_level[l];
+        for (int tz = 0, i = 0; tz <= a.tile_dims[3 * l]; ++tz) {  // (ids ascending: z-rows in order)
+            while (i < static_cast<int>(t.size()) && t[i] / plane < static_cast<uint64_t>(tz)) ++i;
+            a.tile_zfirst.push_back(static_cast<uint32_t>(i));
+        }
+    }
     APR_CUDA(cudaMalloc(&a.tiles, 4 * off + 4));
     for (int l = a.l_min; l <= a.l_max; ++l)
         if (!per_level[l].empty())
@@ -1809,14 +1866,17 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
             b.meta = L.tile_meta;
             b.runs = L.tile_runs[H - 1];
             b.run_off = L.tile_run_off[H - 1];
-            int first = -1;  // the launch's first level with tiles (its tiles start the launch)
+            uint64_t rng[kMaxLevels][2];  // each segment's tiles (absolute; a slab's z-range of them)
             uint32_t total = 0;
             for (; l <= L.l_max && ok(l); ++l) {
                 done[l] = true;
                 if (l < slab.lc && !slab.rep) continue;  // (a replicated level another pass computes)
-                const uint32_t c = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
+                const auto r = tile_range(L, l, slab);
+                const uint32_t c = static_cast<uint32_t>(r.second - r.first);
                 if (!c) continue;
-                if (first < 0) first = l;
+                rng[b.n_levels][0] = r.first;
+                rng[b.n_levels][1] = r.second;
+                b.seg_shift[b.n_levels] = static_cast<uint32_t>(r.first - rng[0][0] - total);
                 total += c;
                 b.woff[b.n_levels] = pyr->off[l - pyr->l_min];
                 b.sep[b.n_levels] = pyr->sep_off[l - pyr->l_min] >= 0 ? pyr->sep_dev + pyr->sep_off[l - pyr->l_min]
@@ -1828,9 +1888,9 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
                 }
             }
             if (!total) continue;
-            b.tile_base = static_cast<uint32_t>(L.tile_off[first]);
-            const bool map = maps_enabled() && (H == 1 ? ensure_tile_maps<1>(apr, b, total, pad, s)
-                                                       : ensure_tile_maps<2>(apr, b, total, pad, s));
+            b.tile_base = static_cast<uint32_t>(rng[0][0]);
+            const bool map = maps_enabled() && (H == 1 ? ensure_tile_maps<1>(apr, b, rng, pad, s)
+                                                       : ensure_tile_maps<2>(apr, b, rng, pad, s));
             if (map) {
                 if (H == 1) {
                     if (exact) launch_map<double, 1>(apr->ctx, b, total, s); else launch_map<float, 1>(apr->ctx, b, total, s);

@@ -50,10 +50,18 @@ void DevAccess::release() {
         tile_flat_off[h] = nullptr;
         for (int pm = 0; pm < 2; ++pm)
             for (int l = 0; l < kMaxLevels; ++l) {
-                cudaFree(tile_map[h][pm][l]);
+                if (tile_map[h][pm][l]) {
+                    cudaFree(tile_map[h][pm][l]->rec);
+                    delete tile_map[h][pm][l];
+                }
                 tile_map[h][pm][l] = nullptr;
             }
     }
+    for (MapWin* w : tile_map_retired) {
+        cudaFree(w->rec);
+        delete w;
+    }
+    tile_map_retired.clear();
     y = nullptr;
     rb = nullptr;
     work = nullptr;

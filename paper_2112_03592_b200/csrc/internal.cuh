@@ -105,8 +105,18 @@ struct DevAccess {
     // per tile, the non-empty source rows of its (H = 1, 2) box: {first particle, row slot | count << 16}
     uint2* tile_runs[2] = {nullptr, nullptr};
     uint32_t* tile_run_off[2] = {nullptr, nullptr};  // n_tiles + 1 offsets into tile_runs
-    // resident gather maps of the box-tile kernel, [H-1][pad][level] (lazy; conv_tile.cu)
-    uint32_t* tile_map[2][2][kMaxLevels] = {};
+    // per level, for each tile z-row tz = 0 .. tzd: the first local index of a tile with z-row >= tz
+    // (tiles are ordered (tz, tx, ty)), so a z-slab's tiles are one contiguous range
+    std::vector<uint32_t> tile_zfirst;
+    std::vector<uint64_t> tile_zfirst_off;  // l_max+1 offsets into tile_zfirst
+    // resident gather maps of the box-tile kernel, [H-1][pad][level] (lazy; conv_tile.cu): records for the
+    // tiles [a0, a1) (absolute tile indices) -- a slab's launches build only the tiles they compute
+    struct MapWin {
+        uint32_t* rec = nullptr;
+        uint64_t a0 = 0, a1 = 0;
+    };
+    MapWin* tile_map[2][2][kMaxLevels] = {};
+    std::vector<MapWin*> tile_map_retired;  // windows a wider one replaced (in-flight launches may read them)
     // per H: every tile's flattened sources (leaf particles, then interior nodes), tiles padded to 4
     uint32_t* tile_flat[2] = {nullptr, nullptr};
     uint32_t* tile_flat_off[2] = {nullptr, nullptr};  // n_tiles + 1 offsets into tile_flat

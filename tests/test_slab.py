@@ -161,9 +161,14 @@ def test_slab_gpu_virtual_ranks_bit_identical(name, world, accum):
     dpyr = pyr.device(ctx)
     SlabConvolver([s for s, _ in states], LocalComm()).convolve(dpyr, pad, acc)
     torch.cuda.synchronize()
-    for st, _ in states:
+    for st, dev in states:
         own = _owned_mask(st.plan, "leaf", ref.size)
         assert np.array_equal(G.bits(st.out.cpu().numpy()[:ref.size][own]), G.bits(ref[own])), st.rank
+        # a rank's gather maps cover only the tiles its slab computes
+        built, n_tiles = dev.map_tiles()
+        assert 0 < built <= n_tiles, (st.rank, built, n_tiles)
+        if name == "c1_256":  # (the small cases' slabs all touch every tile row)
+            assert built < n_tiles, (st.rank, built, n_tiles)
         town = _owned_mask(st.plan, "tree", d["tree_values"].size)
         tv = st.tree.cpu().numpy()[:town.size]
         assert np.array_equal(G.bits(tv[town]), G.bits(d["tree_values"][town])), st.rank
