@@ -105,6 +105,14 @@ int aprgpu_access_get_info(const aprgpu_apr* apr, int which, aprgpu_access_info*
  * (stencil extent, pad mode, level) maps, *n_tiles = the APR's output tiles.  A
  * z-slab's convolutions build records only for the tiles they compute. */
 int aprgpu_apr_map_tiles(const aprgpu_apr* apr, uint64_t* built, uint64_t* n_tiles);
+/* Diagnostics: copies the resident gather-map records of one level (stencil
+ * half-width 1 or 2, pad mode) to host memory out (cap_words u32), record t
+ * starting at word offsets[t] (offsets: *n_tiles + 1 entries); *n_words = the words copied, *first_tile
+ * / *n_tiles = the level-local tile range covered (0 tiles: no map built yet).
+ * out and offsets may be NULL to query sizes first. */
+int aprgpu_map_records(const aprgpu_apr* apr, int half_width, int pad, int level, uint32_t* out,
+                       uint64_t cap_words, uint32_t* offsets, uint64_t* n_words, uint64_t* first_tile,
+                       uint64_t* n_tiles);
 /* Downloads an access structure back into the reference layout (bit-exact
  * round trip).  Arrays sized by aprgpu_access_get_info: y_idx[n_particles],
  * xz_end[n_rows], level_offset/z_dim/x_dim/y_dim[l_max+1]. */

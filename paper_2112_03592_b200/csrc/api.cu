@@ -1346,7 +1346,7 @@ int aprgpu_convolve_pixels(aprgpu_ctx* ctx, const float* in, int nz, int nx, int
         bool any_zero = false;  // (zero weights are skipped like the reference, convolve.hpp:86-88)
         for (float v : hs.w) any_zero = any_zero || v == 0.0f;
         aprgpu::convolve_pixels_device(ctx, src, nz, nx, ny, wd.as<float>(), kz, kx, ky, pad_mode, accum, dst, s,
-                                       any_zero);
+                                       any_zero, hs.w.data());
         if (ptr_kind == APRGPU_HOST) APR_CUDA(cudaMemcpyAsync(out, dst, 4 * n, cudaMemcpyDeviceToHost, s));
         APR_CUDA(cudaStreamSynchronize(s));  // (the weights' buffer is released on return)
     });

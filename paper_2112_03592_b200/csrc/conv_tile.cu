@@ -710,32 +710,7 @@ __device__ __forceinline__ void store_out(const TileLaunch& a, uint32_t i, float
     }
 }
 
-// ---- async copies (sm_90+ bulk copy with an mbarrier; sm_80+ cp.async) ----
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-// one bulk global -> shared copy completing on bar (16-byte aligned, size a multiple of 16)
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-            smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
+// (async-copy helpers: common.cuh)
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -1907,3 +1882,32 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
 }
 
 }  // namespace aprgpu
+
+int aprgpu_map_records(const aprgpu_apr* apr, int half_width, int pad, int level, uint32_t* out,
+                       uint64_t cap_words, uint32_t* offsets, uint64_t* n_words, uint64_t* first_tile,
+                       uint64_t* n_tiles) {
+    using namespace aprgpu;
+    return guard([&] {
+        need(apr && n_words && first_tile && n_tiles, "null argument");
+        need(half_width == 1 || half_width == 2, "half_width must be 1 or 2");
+        need(pad == APRGPU_PAD_REFLECT || pad == APRGPU_PAD_ZERO, "bad pad mode");
+        const DevAccess& L = apr->leaf;
+        need(level >= L.l_min && level <= L.l_max, "level out of range");
+        DeviceGuard g(apr->ctx->device);
+        std::lock_guard<std::mutex> lk(apr->ctx->mu);
+        const DevAccess::MapWin* w = L.tile_map[half_width - 1][pad == APRGPU_PAD_ZERO ? 1 : 0][level];
+        const uint32_t rw = half_width == 1 ? MapBox<1>::REC : MapBox<2>::REC;
+        const uint64_t n = w ? w->a1 - w->a0 : 0;
+        std::vector<uint32_t> off(n + 1);  // (records have a fixed length today)
+        for (uint64_t i = 0; i <= n; ++i) off[i] = static_cast<uint32_t>(i * rw);
+        *first_tile = w ? w->a0 - L.tile_off[level] : 0;
+        *n_tiles = n;
+        *n_words = off[n];
+        if (offsets) std::copy(off.begin(), off.end(), offsets);
+        if (out && n) {
+            need(cap_words >= off[n], "output buffer too small");
+            APR_CUDA(cudaDeviceSynchronize());
+            APR_CUDA(cudaMemcpy(out, w->rec, 4ull * off[n], cudaMemcpyDeviceToHost));
+        }
+    });
+}

@@ -237,7 +237,8 @@ void tree_partition_check(aprgpu_apr* apr, int* dbl, unsigned long long* min_unc
 
 // pixels.cu: convolve_pixels (convolve.hpp:48-98); w_dev = kz*kx*ky device floats
 void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w_dev, int kz,
-                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s, bool any_zero_w = true);
+                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s, bool any_zero_w,
+                            const float* w_host);  // (w_host: the weights again, for kernel parameters)
 
 // io.cpp: the .apr container (docs/FORMATS.md)
 int load_apr_host(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out, std::string& msg);

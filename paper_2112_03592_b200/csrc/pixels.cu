@@ -9,7 +9,9 @@
 // y outputs of one (z, x) column, taps in the reference's order (az, ax, ay)
 // skipping zero weights (:86-88): EXACT = fp64 accumulation of exact products
 // (bit-identical), FAST = fp32 FMA.  Extents up to kMaxStencilExtent = 13.
+#include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -167,146 +169,220 @@ __device__ __forceinline__ void cp_async_4(float* dst, const float* src) {
                  : "memory");
 }
 
-// Isotropic K^3 (K = 3, 5), streamed along z (2.5-D blocking): a CTA owns a
-// 32 (x) x 64 (y) column of outputs over kZc planes and keeps a ring of K + 2
-// input planes -- the K the current output plane reads and the next two,
-// prefetched with cp.async while the current plane is evaluated (padding
-// applied on load).  Every input plane is read from HBM about once (x / y halo
-// 1.1x, z halo 2H / kZc).  Lane = x row, warp = a run of 8 consecutive y
-// outputs: a warp's window loads are 16-byte loads from 32 different rows
-// whose stride (kPY = 76 floats, 12 banks) puts every quarter-warp on distinct
-// banks -- conflict-free (lanes along y, 32 bytes apart, were 8-way conflicted).
-// FAST keeps the K^3 weights in registers, EXACT reads them as doubles from
-// shared memory (one broadcast load per tap).  SKIP: some weight is zero and
-// is skipped like the reference (convolve.hpp:86-88) -- which only matters
-// for non-finite inputs; otherwise no per-tap test.
-constexpr int kSx = 32, kSy = 64, kZc = 32, kRY = 8, kPY = 76;
-template <typename Acc, int K, bool SKIP>
-__global__ void __launch_bounds__(kPixThreads) k_convolve_pixels_stream(PixArgs a, int txd, int tyd) {
+constexpr int kSx = 32, kSy = 64, kRY = 8, kPY = 76, kZc = 128;
+
+// Isotropic K^3 (K = 3, 5), z-register streaming (2.5-D blocking): a CTA owns
+// a 32 (x) x 64 (y) column of outputs over kZc planes.  Lane = x row, warp = a
+// run of RY consecutive y outputs; a warp's window loads are 16-byte loads
+// from 32 rows whose stride (kPY = 76 floats, 12 banks) puts every
+// quarter-warp on distinct banks.  Every input plane is read from shared
+// memory ONCE per thread -- its K rows around the thread's x -- and scattered
+// into the K output planes that read it, whose partial sums live in
+// registers (acc[k]: output p - H + k, tap plane az = k).  Planes stream from
+// the top down, so each output still receives its taps in the reference's
+// (az, ax, ay) order (az = 0 reads plane o + H): EXACT stays bit-identical.
+// The ring holds the current plane and D in flight (cp.async, one barrier per
+// plane; a thread's share of a plane's copies -- x reflected, halo y
+// reflected or zero -- is fixed for the whole column and computed once), and
+// the weights are kernel parameters (constant-bank operands: no registers, no
+// loads).  FAST pairs the y outputs into packed fp32x2 FMAs and takes 16 y
+// outputs per thread (128 threads), EXACT 8 (256 threads).  Round 2 (C3 image,
+// 1024^3, 3^3): the previous kernel (every output plane re-reading its K^2
+// rows) 4.19 / 5.03 ms FAST / EXACT, this one 2.32 / 2.63 ms (58 / 51 % of
+// HBM); D = 3, 32- or 64-plane columns and 288-byte bulk copies per row (TMA)
+// all measured slower.
+template <typename Acc, int KW>
+struct PixW {
+    Acc w[KW];
+};
+
+__device__ __forceinline__ float2 ffma2_p(float2 a, float2 b, float2 c) {  // fma.rn.f32x2 (sm_100)
+    float2 d;
+    asm("{.reg .b64 ra, rb, rc, rd;\n"
+        "mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rc, {%6, %7};\n"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
+template <typename Acc, int K, bool SKIP, int RY = kRY>  // RY: y outputs per thread (warps = kSy / RY)
+__global__ void __launch_bounds__(32 * kSy / RY, RY == 8 ? (sizeof(Acc) == 4 ? (K == 3 ? 4 : 3) : 2) : (sizeof(Acc) == 4 ? (K == 3 ? 5 : 3) : 2))
+    k_convolve_pixels_zreg(PixArgs a, const __grid_constant__ PixW<Acc, K * K * K> W, int txd, int tyd, int zc) {
     constexpr int D = 2;  // prefetch distance (planes)
-    // a plane row: [4 - H unused][H halo][64 interior at a 16-byte boundary][H halo], kPY floats
-    constexpr int H = K / 2, PX = kSx + 2 * H, OFF = 4 - H, PY = kPY, PLANE = PX * PY, RY = kRY,
-                  NS = K + D, KW = K * K * K;
-    static_assert(kSx * (kSy / RY) == kPixThreads && kSx == 32, "lane = x row, warp = y run");
-    static_assert(PY >= kSy + 8 && PY % 4 == 0, "16-byte rows");
+    constexpr int NT = 32 * kSy / RY;
+    constexpr int H = K / 2, PX = kSx + 2 * H, OFF = 4 - H, PY = kPY, PLANE = PX * PY, NS = D + 1;
+    static_assert(kSx == 32 && kSy % RY == 0 && RY % 4 == 0, "lane = x row, warp = y run");
     extern __shared__ __align__(16) float ring[];  // NS planes
-    __shared__ Acc Ws[KW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ty = blockIdx.x % tyd, t2 = blockIdx.x / tyd;
     const int tx = t2 % txd, tzc = t2 / txd;
-    const int x0 = tx * kSx, y0 = ty * kSy, zc0 = tzc * kZc, zc1 = min(zc0 + kZc, a.nz);
-    for (int i = tid; i < KW; i += kPixThreads) Ws[i] = static_cast<Acc>(a.w[i]);
-    float wr[sizeof(Acc) == 4 ? KW : 1];  // FAST: the weights in registers
-    if constexpr (sizeof(Acc) == 4) {
-#pragma unroll
-        for (int i = 0; i < KW; ++i) wr[i] = __ldg(a.w + i);
-    }
-    auto slot = [&](int z) { return ring + (((z % NS) + NS) % NS) * PLANE; };
+    const int x0 = tx * kSx, y0 = ty * kSy, zc0 = tzc * zc, zc1 = min(zc0 + zc, a.nz);
     const bool vec = (a.ny & 3) == 0 && y0 + kSy <= a.ny;  // 16-byte aligned, whole interior in range
-    // input plane z into its slot (reflected / zero outside the volume), asynchronously
-    auto load = [&](int z) {
-        float* pl = slot(z);
+    const bool zpad = a.pad == APRGPU_PAD_ZERO;
+    // vec: a plane is PX rows x 16 interior chunks of 16 bytes + PX x 2H halo
+    // cells; each thread's share (<= NDESC copies) is fixed for the whole z
+    // column, so its source offsets within a plane (x reflected, halo y
+    // reflected; -1: a zero) and slot offsets are computed once
+    constexpr int NCH = PX * (kSy / 4), NCOPY = NCH + PX * 2 * H;
+    constexpr int NDESC = (NCOPY + NT - 1) / NT;
+    int sro[NDESC], dso[NDESC];
+#pragma unroll
+    for (int d = 0; d < NDESC; ++d) {
+        const int i = tid + d * NT;
+        sro[d] = -2;  // (none)
+        dso[d] = 0;
+        if (i >= NCOPY) continue;
+        const int r = i < NCH ? i / (kSy / 4) : (i - NCH) / (2 * H);
+        const int x = x0 + r - H;
+        const bool xz = (x < 0 || x >= a.nx) && zpad;
+        const int xo = reflect_p(x, a.nx) * a.ny;
+        if (i < NCH) {
+            const int c = i % (kSy / 4);
+            dso[d] = r * PY + OFF + H + 4 * c;
+            sro[d] = xz ? -1 : xo + y0 + 4 * c;
+        } else {
+            const int k = (i - NCH) % (2 * H);
+            const int c = k < H ? k : kSy + k;  // box cell: y = y0 + c - H
+            const int y = y0 + c - H;
+            dso[d] = r * PY + OFF + c;
+            sro[d] = xz || ((y < 0 || y >= a.ny) && zpad) ? -1 : xo + reflect_p(y, a.ny);
+        }
+    }
+    auto load = [&](int z, int si) {  // input plane z into slot si (reflected / zero outside the volume)
+        float* pl = ring + si * PLANE;
         const bool zout = z < 0 || z >= a.nz;
         const int zr = reflect_p(z, a.nz);
-        for (int r = warp; r < PX; r += kPixThreads / 32) {
-            const int x = x0 + r - H;
-            float* dst = pl + r * PY + OFF;  // dst[c]: y = y0 + c - H
-            if ((zout || x < 0 || x >= a.nx) && a.pad == APRGPU_PAD_ZERO) {
-                for (int c = lane; c < kSy + 2 * H; c += 32) dst[c] = 0.0f;
-                continue;
-            }
-            const float* src = a.in + (static_cast<size_t>(zr) * a.nx + reflect_p(x, a.nx)) * a.ny;
-            if (vec) {  // the interior: 16-byte copies
-                if (lane < kSy / 4)
+        if (vec) {
+            const float* pb = a.in + static_cast<size_t>(zr) * a.nx * a.ny;
+#pragma unroll
+            for (int d = 0; d < NDESC; ++d) {
+                if (sro[d] == -2) continue;
+                const bool wide = tid + d * NT < NCH;
+                if (sro[d] < 0 || (zout && zpad)) {
+                    if (wide) *reinterpret_cast<float4*>(pl + dso[d]) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    else pl[dso[d]] = 0.0f;
+                } else if (wide) {
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                     static_cast<unsigned>(__cvta_generic_to_shared(dst + H + 4 * lane))),
-                                 "l"(src + y0 + 4 * lane)
+                                     static_cast<unsigned>(__cvta_generic_to_shared(pl + dso[d]))),
+                                 "l"(pb + sro[d])
                                  : "memory");
-            } else {  // (ragged or unaligned rows)
-                for (int c = H + lane; c < H + kSy; c += 32) {
-                    const int y = y0 + c - H;
-                    if (y < a.ny) cp_async_4(dst + c, src + y);
-                    else if (a.pad == APRGPU_PAD_REFLECT) cp_async_4(dst + c, src + reflect_p(y, a.ny));
-                    else dst[c] = 0.0f;
+                } else {
+                    cp_async_4(pl + dso[d], pb + sro[d]);
                 }
             }
-            if (lane >= 32 - 2 * H) {  // the halos (lanes the interior copies leave idle)
-                const int k = lane - (32 - 2 * H);
-                const int c = k < H ? k : kSy + k;
-                const int y = y0 + c - H;
-                if (y >= 0 && y < a.ny) cp_async_4(dst + c, src + y);
-                else if (a.pad == APRGPU_PAD_REFLECT) cp_async_4(dst + c, src + reflect_p(y, a.ny));
-                else dst[c] = 0.0f;
+        } else {  // (ragged or unaligned rows: element-wise)
+            for (int r = warp; r < PX; r += NT / 32) {
+                const int x = x0 + r - H;
+                float* dst = pl + r * PY + OFF;  // dst[c]: y = y0 + c - H
+                if ((zout || x < 0 || x >= a.nx) && zpad) {
+                    for (int c = lane; c < kSy + 2 * H; c += 32) dst[c] = 0.0f;
+                    continue;
+                }
+                const float* src = a.in + (static_cast<size_t>(zr) * a.nx + reflect_p(x, a.nx)) * a.ny;
+                for (int c = lane; c < kSy + 2 * H; c += 32) {
+                    const int y = y0 + c - H;
+                    if (y >= 0 && y < a.ny) cp_async_4(dst + c, src + y);
+                    else if (!zpad) cp_async_4(dst + c, src + reflect_p(y, a.ny));
+                    else dst[c] = 0.0f;
+                }
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    const int ox = lane, oy = warp * RY;  // this thread's outputs: row ox, y oy .. oy + 7
-    // planes zc0 - H .. zc0 + H + D - 1 in flight; then one group per plane
-    for (int z = zc0 - H; z < zc0 + H + D; ++z) {
-        if (z < zc1 + H) load(z);
+    const int ox = lane, oy = warp * RY;
+    const bool live = x0 + ox < a.nx && y0 + oy < a.ny;
+    const int top = zc1 - 1 + H, bot = zc0 - H;  // planes top .. bot, descending
+    int cur = top % NS;  // slot of plane p (top >= 1)
+    for (int i = 0; i < D; ++i) {
+        if (top - i >= bot) load(top - i, (top - i) % NS);
         else asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    for (int z = zc0 + H; z < zc1 + H; ++z) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(D) : "memory");  // all but the D newest groups
-        __syncthreads();  // planes o - H .. o + H resident; the slot of o - H - 1 is free
-        if (z + D < zc1 + H) load(z + D);  // prefetch D planes ahead
+    constexpr int SH = OFF & 3, NL = (SH + RY + 2 * H + 3) & ~3;
+    Acc acc[K][RY];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int j = 0; j < RY; ++j) acc[k][j] = Acc(0);
+    float* dst = a.out + (static_cast<size_t>(top - H) * a.nx + (x0 + ox)) * a.ny + y0 + oy;
+    const size_t zstride = static_cast<size_t>(a.nx) * a.ny;
+    const bool vst = y0 + oy + RY <= a.ny && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (zstride & 3) == 0;
+    for (int p = top; p >= bot; --p) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");  // plane p landed
+        __syncthreads();  // ... for every thread; plane p + 1's slot is free
+        const int nxt = cur == NS - 1 ? 0 : cur + 1;  // the slot of p + 1 == p - D (NS = D + 1)
+        if (p - D >= bot) load(p - D, nxt);
         else asm volatile("cp.async.commit_group;" ::: "memory");
-        const int o = z - H;
-        if (x0 + ox < a.nx && y0 + oy < a.ny) {
-            Acc acc[RY];
+        const float* pl = ring + cur * PLANE;
+        cur = cur == 0 ? NS - 1 : cur - 1;
 #pragma unroll
-            for (int j = 0; j < RY; ++j) acc[j] = Acc(0);
+        for (int ax = 0; ax < K; ++ax) {
+            const float* row = pl + (ox + 2 * H - ax) * PY + (OFF - SH) + oy;
+            float win[NL];
 #pragma unroll
-            for (int az = 0; az < K; ++az) {
-                const float* plz = slot(o + H - az);  // input plane read with weight plane az
+            for (int i = 0; i < NL; i += 4) {
+                const float4 t = *reinterpret_cast<const float4*>(row + i);
+                win[i] = t.x;
+                win[i + 1] = t.y;
+                win[i + 2] = t.z;
+                win[i + 3] = t.w;
+            }
+            // output p - H + k takes plane p with weight plane az = k
 #pragma unroll
-                for (int ax = 0; ax < K; ++ax) {
-                    // outputs oy + j read cells c = oy + j + 2H - ay, c in [oy, oy + 7 + 2H]: the
-                    // window from the 16-byte boundary at or below row + OFF + oy
-                    const float* row = plz + (ox + 2 * H - ax) * PY;
-                    constexpr int SH = OFF & 3, NL = (SH + RY + 2 * H + 3) & ~3;
-                    Acc win[NL];  // (converted once per row, not per tap)
+            for (int k = 0; k < K; ++k)
 #pragma unroll
-                    for (int i = 0; i < NL; i += 4) {
-                        const float4 t = *reinterpret_cast<const float4*>(row + (OFF - SH) + oy + i);
-                        win[i] = static_cast<Acc>(t.x);
-                        win[i + 1] = static_cast<Acc>(t.y);
-                        win[i + 2] = static_cast<Acc>(t.z);
-                        win[i + 3] = static_cast<Acc>(t.w);
-                    }
+                for (int ay = 0; ay < K; ++ay) {
+                    const Acc wa = W.w[(k * K + ax) * K + ay];
+                    if (SKIP && wa == Acc(0)) continue;  // (convolve.hpp:86-88)
+                    if constexpr (sizeof(Acc) == 4) {
 #pragma unroll
-                    for (int ay = 0; ay < K; ++ay) {
-                        const int wi = (az * K + ax) * K + ay;
-                        Acc wa;
-                        if constexpr (sizeof(Acc) == 4) wa = wr[wi]; else wa = Ws[wi];
-                        if (SKIP && wa == Acc(0)) continue;  // (convolve.hpp:86-88)
+                        for (int j = 0; j < RY; j += 2) {
+                            const float2 r = ffma2_p(make_float2(wa, wa),
+                                                     make_float2(win[SH + j + 2 * H - ay], win[SH + j + 1 + 2 * H - ay]),
+                                                     make_float2(acc[k][j], acc[k][j + 1]));
+                            acc[k][j] = r.x;
+                            acc[k][j + 1] = r.y;
+                        }
+                    } else {
 #pragma unroll
-                        for (int j = 0; j < RY; ++j) acc[j] = fma(wa, win[SH + j + 2 * H - ay], acc[j]);
+                        for (int j = 0; j < RY; ++j)
+                            acc[k][j] = fma(wa, static_cast<Acc>(win[SH + j + 2 * H - ay]), acc[k][j]);
                     }
                 }
-            }
-            float* dst = a.out + (static_cast<size_t>(o) * a.nx + (x0 + ox)) * a.ny + y0 + oy;
-            if (y0 + oy + RY <= a.ny && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        }
+        // output p + H (tap plane 2H) is complete; dst tracks output p - H, so it is 2H planes up
+        const int o = p + H;
+        if (live && o >= zc0 && o < zc1) {
+            float* d = dst + 2 * H * zstride;
+            if (vst) {
 #pragma unroll
                 for (int j = 0; j < RY; j += 4)
-                    __stcs(reinterpret_cast<float4*>(dst + j),
-                           make_float4(static_cast<float>(acc[j]), static_cast<float>(acc[j + 1]),
-                                       static_cast<float>(acc[j + 2]), static_cast<float>(acc[j + 3])));
+                    __stcs(reinterpret_cast<float4*>(d + j),
+                           make_float4(static_cast<float>(acc[K - 1][j]), static_cast<float>(acc[K - 1][j + 1]),
+                                       static_cast<float>(acc[K - 1][j + 2]), static_cast<float>(acc[K - 1][j + 3])));
             } else {
 #pragma unroll
                 for (int j = 0; j < RY; ++j)
-                    if (y0 + oy + j < a.ny) dst[j] = static_cast<float>(acc[j]);
+                    if (y0 + oy + j < a.ny) d[j] = static_cast<float>(acc[K - 1][j]);
             }
         }
-        __syncthreads();  // (the next prefetch overwrites this iteration's oldest plane)
+        dst -= zstride;
+        // the sets move up one plane (register moves; unrolling the plane loop by K to rotate
+        // them instead spilled at 64 registers and measured slower)
+#pragma unroll
+        for (int k = K - 1; k > 0; --k)
+#pragma unroll
+            for (int j = 0; j < RY; ++j) acc[k][j] = acc[k - 1][j];
+#pragma unroll
+        for (int j = 0; j < RY; ++j) acc[0][j] = Acc(0);
     }
 }
 
 }  // namespace
 
 void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w_dev, int kz,
-                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s, bool any_zero_w) {
+                            int kx, int ky, int pad, int accum, float* out, cudaStream_t s, bool any_zero_w,
+                            const float* w_host) {
     if (kz > kPixMaxK || kx > kPixMaxK || ky > kPixMaxK)
         fail(APRGPU_ERR_CAPABILITY, "convolve_pixels: stencil extent exceeds the supported maximum");
     if (nz <= 0 || nx <= 0 || ny <= 0) return;
@@ -316,15 +392,22 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
     if (blocks >= (1ull << 31)) fail(APRGPU_ERR_CAPABILITY, "convolve_pixels: volume too large");
     if (kz == kx && kx == ky && (kz == 3 || kz == 5) && !std::getenv("APRGPU_PIXELS_TILED")) {
         const bool ex = accum == APRGPU_ACCUM_EXACT;
-        const int sxd = (nx + kSx - 1) / kSx, syd = (ny + kSy - 1) / kSy, szd = (nz + kZc - 1) / kZc;
+        static const int zc = [] {  // planes per CTA (APRGPU_PIXELS_ZC: A/B experiments)
+            const char* e = std::getenv("APRGPU_PIXELS_ZC");
+            return e ? std::max(1, std::atoi(e)) : kZc;
+        }();
+        const int ry = ex ? 8 : 16;  // y outputs per thread (A/B: FAST 2.35 -> 2.32 ms, EXACT 2.63 -> 2.76 ms at 16)
+        const int sxd = (nx + kSx - 1) / kSx, syd = (ny + kSy - 1) / kSy, szd = (nz + zc - 1) / zc;
         const unsigned g = static_cast<unsigned>(static_cast<uint64_t>(szd) * sxd * syd);
         const int h = kz / 2;
-        const int rb = (kz + 2) * (kSx + 2 * h) * kPY * static_cast<int>(sizeof(float));
-        static OncePerDevice sattr;
-        sattr([] {
-            const int mx = 7 * (kSx + 4) * kPY * static_cast<int>(sizeof(float));
-#define APRGPU_SET_PIX(A, K_, S_) \
-    APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_stream<A, K_, S_>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx))
+        const int rb = 3 * (kSx + 2 * h) * kPY * static_cast<int>(sizeof(float));
+        static OncePerDevice zattr;
+        zattr([] {
+            const int mx = 3 * (kSx + 4) * kPY * static_cast<int>(sizeof(float));
+#define APRGPU_SET_PIX(A, K_, S_)                                                                                      \
+    APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_zreg<A, K_, S_, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  mx));                                                                              \
+    APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_zreg<A, K_, S_, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx))
             APRGPU_SET_PIX(double, 3, false);
             APRGPU_SET_PIX(double, 3, true);
             APRGPU_SET_PIX(float, 3, false);
@@ -335,10 +418,19 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
             APRGPU_SET_PIX(float, 5, true);
 #undef APRGPU_SET_PIX
         });
-        const bool skip = any_zero_w;  // (a zero weight is skipped like the reference)
-#define APRGPU_LAUNCH_PIX(A, K_) \
-    (skip ? k_convolve_pixels_stream<A, K_, true><<<g, kPixThreads, rb, s>>>(a, sxd, syd) \
-          : k_convolve_pixels_stream<A, K_, false><<<g, kPixThreads, rb, s>>>(a, sxd, syd))
+        const bool skip = any_zero_w;
+#define APRGPU_LAUNCH_PIX(A, K_)                                                                                \
+    do {                                                                                                        \
+        PixW<A, K_ * K_ * K_> pw;                                                                               \
+        for (int i = 0; i < K_ * K_ * K_; ++i) pw.w[i] = static_cast<A>(w_host[i]);                             \
+        if (ry == 16) {                                                                                         \
+            if (skip) k_convolve_pixels_zreg<A, K_, true, 16><<<g, 128, rb, s>>>(a, pw, sxd, syd, zc);          \
+            else k_convolve_pixels_zreg<A, K_, false, 16><<<g, 128, rb, s>>>(a, pw, sxd, syd, zc);              \
+        } else {                                                                                                \
+            if (skip) k_convolve_pixels_zreg<A, K_, true, 8><<<g, 256, rb, s>>>(a, pw, sxd, syd, zc);           \
+            else k_convolve_pixels_zreg<A, K_, false, 8><<<g, 256, rb, s>>>(a, pw, sxd, syd, zc);               \
+        }                                                                                                       \
+    } while (0)
         if (kz == 3) {
             if (ex) APRGPU_LAUNCH_PIX(double, 3); else APRGPU_LAUNCH_PIX(float, 3);
         } else {
