@@ -92,7 +92,7 @@ inline ParticleValues convolve_apr(const APR& apr, const ParticleValues& values,
         gpu::check(aprgpu_fill_tree(h, values.data(), tree_filled.data(), APRGPU_HOST, nullptr));
         tv = &tree_filled;
     }
-    ParticleValues out(values.size(), 0.0f);
+    ParticleValues out = gpu::result_vector(values.size());
     if (out.empty()) return out;
     // $APRGPU_DEVICES: z-slabs over several GPUs (halo = the largest half-width)
     int hw = 1;

@@ -24,7 +24,7 @@ inline ParticleValues rl_apr(const APR& apr, const ParticleValues& observed, con
     gpu::Runtime& rt = gpu::Runtime::get();
     const auto href_ = rt.upload(apr);
     aprgpu_apr* h = href_.get();
-    ParticleValues est(observed.size(), 0.0f);
+    ParticleValues est = gpu::result_vector(observed.size());
     if (est.empty()) return est;
     const Stencil& w = cfg.psf;
     const int every = (observer && cfg.record_metrics_every > 0) ? cfg.record_metrics_every : cfg.iterations;

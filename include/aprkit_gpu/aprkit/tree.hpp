@@ -33,7 +33,7 @@ inline ParticleValues fill_tree(const APR& apr, const ParticleValues& leaf_value
         throw RangeError("fill_tree: leaf value count does not match the APR");
     const auto href_ = gpu::Runtime::get().upload(apr);
     aprgpu_apr* h = href_.get();
-    ParticleValues out(gpu::count(h, APRGPU_TREE), 0.0f);
+    ParticleValues out = gpu::result_vector(gpu::count(h, APRGPU_TREE));
     if (out.empty() || leaf_values.empty()) return out;
     gpu::check(aprgpu_fill_tree(h, leaf_values.data(), out.data(), APRGPU_HOST, nullptr));
     return out;

@@ -3,6 +3,8 @@
 // and rl_apr.  Exceptions never cross this boundary; aprgpu::Error carries the
 // status code that the reference-side shim maps back to aprkit's exceptions.
 #include <algorithm>
+#include <thread>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -264,6 +266,56 @@ int env_int(const char* name, int dflt) {
     return e && *e ? std::atoi(e) : dflt;
 }
 
+}  // namespace
+
+namespace aprgpu {
+
+HostPool::HostPool(int n) {
+    for (int i = 0; i < n; ++i)
+        th_.emplace_back([this] {
+            uint64_t seen = 0;
+            for (;;) {
+                std::function<void()> job;
+                {
+                    std::unique_lock<std::mutex> lk(m_);
+                    cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                    if (stop_) return;
+                    seen = gen_;
+                    job = job_;
+                }
+                job();
+                std::lock_guard<std::mutex> lk(m_);
+                if (--busy_ == 0) done_.notify_all();
+            }
+        });
+}
+
+HostPool::~HostPool() {
+    {
+        std::lock_guard<std::mutex> lk(m_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+}
+
+void HostPool::start(std::function<void()> job) {
+    std::lock_guard<std::mutex> lk(m_);
+    job_ = std::move(job);
+    busy_ = static_cast<int>(th_.size());
+    ++gen_;
+    cv_.notify_all();
+}
+
+void HostPool::wait() {
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return busy_ == 0; });
+}
+
+}  // namespace aprgpu
+
+namespace {
+
 // The z-chunk plan of a host-pointer convolution (see convolve_host_pipelined).
 bool host_pipe_plan(aprgpu_apr* apr, int chunks, cudaStream_t s) {
     const aprgpu::DevAccess& L = apr->leaf;
@@ -335,18 +387,21 @@ bool host_pipe_plan(aprgpu_apr* apr, int chunks, cudaStream_t s) {
 // kernels.  Outputs are bit-identical to the one-shot path (every output is
 // computed from the same inputs by the same kernel; levels < lc, a few
 // thousand particles, are recomputed by every pass and copied back last).
-// Only page-locked buffers qualify (a pageable copy blocks the host); with
-// C3 on one B200 the call drops from 2.80 to 2.46 ms (PCIe: the two
-// directions share the link's budget, so the overlap is partial).
-// Returns false when the volume is too small to be worth chunking.
+// Page-locked buffers are copied directly.  Pageable ones (a std::vector: the
+// C++ drop-in) go through the context's pinned staging: its worker threads
+// copy chunk j in while the device already copies and convolves the chunks
+// before it, and copy chunk j's outputs out as soon as they have landed -- a
+// plain cudaMemcpy of pageable memory would serialise all of it.  C3 on one
+// B200: 2.80 ms one-shot -> 2.36 ms pinned (PCIe: the two directions share the
+// link's budget, so the overlap is partial).  Returns false when the volume
+// is too small to be worth chunking (or the staging would exceed
+// $APRGPU_STAGE_MAX_MB, default 4096).
 bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* tree_values,
                              const aprgpu_pyramid* pyr, int pad, int accum, float* out, cudaStream_t s) {
     const int chunks = env_int("APRGPU_HOST_CHUNKS", 8);
     const int min_np = env_int("APRGPU_HOST_PIPELINE_MIN", 1 << 20);
     const uint64_t np = apr->leaf.n_particles, nt = apr->tree.n_particles;
     if (chunks < 2 || np < static_cast<uint64_t>(std::max(min_np, 0)) || !s) return false;
-    // only page-locked host buffers copy asynchronously (a pageable copy blocks
-    // the host, which would serialise the pipeline)
     auto pinned = [](const void* p) {
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -355,7 +410,10 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
         }
         return at.type == cudaMemoryTypeHost;
     };
-    if (!pinned(values) || !pinned(out) || (nt && !pinned(tree_values))) return false;
+    const bool staged = !pinned(values) || !pinned(out) || (nt && !pinned(tree_values));
+    const size_t stage_need = 4 * (2 * np + nt);
+    if (staged && stage_need > static_cast<size_t>(std::max(env_int("APRGPU_STAGE_MAX_MB", 4096), 0)) << 20)
+        return false;
     aprgpu_ctx* ctx = apr->ctx;
     std::lock_guard<std::mutex> lk(ctx->pipe_mu);
     if (!host_pipe_plan(apr, chunks, s)) return false;
@@ -363,7 +421,7 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
     const int K = P.K;
     if (!ctx->copy_in) APR_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
     if (!ctx->copy_out) APR_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
-    while (ctx->events.size() < static_cast<size_t>(2 * K + 1)) {
+    while (ctx->events.size() < static_cast<size_t>(3 * K + 2)) {
         cudaEvent_t e;
         APR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         ctx->events.push_back(e);
@@ -371,6 +429,7 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
     cudaEvent_t start = ctx->events[0];
     cudaEvent_t* e_in = ctx->events.data() + 1;
     cudaEvent_t* e_conv = ctx->events.data() + 1 + K;
+    cudaEvent_t* e_out = ctx->events.data() + 1 + 2 * K;  // K + 1: each chunk's outputs, then the rest
     float* d_in = apr->h_in.as<float>();
     float* d_tree = apr->h_tree.as<float>();
     float* d_out = apr->h_out.as<float>();
@@ -378,34 +437,91 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
     const aprgpu::DevAccess& T = apr->tree;
     const int tlo = std::max(P.lc, T.l_min);
     const int ntl = nt ? std::max(T.l_max - tlo + 1, 0) : 0;
-    auto h2d = [&](float* d, const float* h, uint64_t b, uint64_t e) {
-        if (e > b) APR_CUDA(cudaMemcpyAsync(d + b, h + b, 4 * (e - b), cudaMemcpyHostToDevice, ctx->copy_in));
-    };
-    auto d2h = [&](uint64_t b, uint64_t e) {
-        if (e > b) APR_CUDA(cudaMemcpyAsync(out + b, d_out + b, 4 * (e - b), cudaMemcpyDeviceToHost, ctx->copy_out));
-    };
-    APR_CUDA(cudaEventRecord(start, s));
-    APR_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
-    APR_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+    // the host side of the copies: the caller's buffers, or the pinned staging
+    const float* h_val = values;
+    const float* h_tree = tree_values;
+    float* h_out = out;
+    if (staged) {
+        if (ctx->stage_bytes < stage_need) {
+            if (ctx->stage) cudaFreeHost(ctx->stage);
+            ctx->stage = nullptr;
+            ctx->stage_bytes = 0;
+            APR_CUDA(cudaHostAlloc(&ctx->stage, stage_need, cudaHostAllocDefault));
+            ctx->stage_bytes = stage_need;
+        }
+        if (!ctx->pool) {
+            const int hc = static_cast<int>(std::thread::hardware_concurrency());
+            ctx->pool = new aprgpu::HostPool(std::max(1, env_int("APRGPU_HOST_THREADS", std::min(8, std::max(1, hc / 2)))));
+        }
+        float* st = static_cast<float*>(ctx->stage);
+        h_val = st;
+        h_tree = st + np;
+        h_out = st + np + nt;
+    }
     // few, large copies: the finest level's rows carry ~90 % of the particles,
     // so chunk 0 takes every coarser level whole and each later chunk one
     // contiguous range of the finest level (leaf and interior alike); outputs
     // come back per chunk for the two finest levels, the rest at the end
     auto LB = [&](int l, int jj) { return P.leaf_b[(l - P.lc) * (K + 1) + jj]; };
     auto TB = [&](int jj) { return P.tree_b[(ntl - 1) * (K + 1) + jj]; };
-    for (int j = 0; j < K; ++j) {
-        h2d(d_in, values, j ? LB(L.l_max, j) : 0, LB(L.l_max, j + 1));
-        if (nt) {
-            if (ntl)
-                h2d(d_tree, tree_values, j ? TB(j) : 0, TB(j + 1));
-            else if (j == 0)
-                h2d(d_tree, tree_values, 0, nt);
-        }
-        APR_CUDA(cudaEventRecord(e_in[j], ctx->copy_in));
-    }
+    struct Range {
+        int arr;  // 0 leaf values, 1 tree values, 2 outputs
+        uint64_t b, e;
+    };
+    std::vector<std::vector<Range>> in_r(K), out_r(K + 1);
     const bool two = L.l_max - 1 >= P.lc;
-    aprgpu::EpiArgs epi;
     for (int j = 0; j < K; ++j) {
+        in_r[j].push_back({0, j ? LB(L.l_max, j) : 0, LB(L.l_max, j + 1)});
+        if (nt) {
+            if (ntl) in_r[j].push_back({1, j ? TB(j) : 0, TB(j + 1)});
+            else if (j == 0) in_r[j].push_back({1, 0, nt});
+        }
+        out_r[j].push_back({2, LB(L.l_max, j), LB(L.l_max, j + 1)});
+        if (two) out_r[j].push_back({2, LB(L.l_max - 1, j), LB(L.l_max - 1, j + 1)});
+    }
+    out_r[K].push_back({2, 0, two ? LB(L.l_max - 1, 0) : LB(L.l_max, 0)});
+    // staged: the host copies, as pieces of <= 1 MB in chunk order
+    struct Piece {
+        float* dst;
+        const float* src;
+        size_t n;
+        int chunk;
+    };
+    std::vector<Piece> pin, pout;
+    std::vector<std::atomic<int>> left(K);
+    if (staged) {
+        constexpr size_t kPiece = 1 << 18;  // floats
+        auto cut = [&](std::vector<Piece>& v, float* dst, const float* src, uint64_t b, uint64_t e, int c) {
+            for (uint64_t x = b; x < e; x += kPiece) v.push_back({dst + x, src + x, std::min<uint64_t>(kPiece, e - x), c});
+        };
+        for (int j = 0; j < K; ++j) {
+            const size_t n0 = pin.size();
+            for (const Range& r : in_r[j])
+                cut(pin, const_cast<float*>(r.arr == 0 ? h_val : h_tree), r.arr == 0 ? values : tree_values, r.b, r.e, j);
+            left[j].store(static_cast<int>(pin.size() - n0));
+        }
+        for (int j = 0; j <= K; ++j)
+            for (const Range& r : out_r[j]) cut(pout, out, h_out, r.b, r.e, j);
+    }
+    std::atomic<size_t> next{0};
+    struct Join {  // an error below must not leave the workers on this frame's pieces
+        aprgpu::HostPool* p;
+        ~Join() {
+            if (p) p->wait();
+        }
+    } join{staged ? ctx->pool : nullptr};
+    if (staged)
+        ctx->pool->start([&] {
+            for (size_t i; (i = next.fetch_add(1)) < pin.size();) {
+                std::memcpy(pin[i].dst, pin[i].src, 4 * pin[i].n);
+                left[pin[i].chunk].fetch_sub(1, std::memory_order_release);
+            }
+        });
+    APR_CUDA(cudaEventRecord(start, s));
+    APR_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
+    APR_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+    aprgpu::EpiArgs epi;
+    auto conv = [&](int j) {  // chunk j's tiles (inputs <= j+1 landed), then its outputs back
         APR_CUDA(cudaStreamWaitEvent(s, e_in[std::min(j + 1, K - 1)], 0));
         aprgpu::Slab slab;
         slab.lc = P.lc;
@@ -414,13 +530,46 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
         aprgpu::convolve_device(apr, d_in, d_tree, pyr, pad, accum, d_out, epi, s, slab);
         APR_CUDA(cudaEventRecord(e_conv[j], s));
         APR_CUDA(cudaStreamWaitEvent(ctx->copy_out, e_conv[j], 0));
-        d2h(LB(L.l_max, j), LB(L.l_max, j + 1));
-        if (two) d2h(LB(L.l_max - 1, j), LB(L.l_max - 1, j + 1));
+        for (const Range& r : out_r[j])
+            if (r.e > r.b)
+                APR_CUDA(cudaMemcpyAsync(h_out + r.b, d_out + r.b, 4 * (r.e - r.b), cudaMemcpyDeviceToHost, ctx->copy_out));
+        APR_CUDA(cudaEventRecord(e_out[j], ctx->copy_out));
+    };
+    for (int j = 0; j < K; ++j) {
+        if (staged)
+            while (left[j].load(std::memory_order_acquire) > 0) std::this_thread::yield();
+        for (const Range& r : in_r[j]) {
+            float* d = r.arr == 0 ? d_in : d_tree;
+            const float* h = r.arr == 0 ? h_val : h_tree;
+            if (r.e > r.b)
+                APR_CUDA(cudaMemcpyAsync(d + r.b, h + r.b, 4 * (r.e - r.b), cudaMemcpyHostToDevice, ctx->copy_in));
+        }
+        APR_CUDA(cudaEventRecord(e_in[j], ctx->copy_in));
+        if (j >= 1) conv(j - 1);
     }
-    d2h(0, two ? LB(L.l_max - 1, 0) : LB(L.l_max, 0));
+    conv(K - 1);
+    for (const Range& r : out_r[K])
+        if (r.e > r.b)
+            APR_CUDA(cudaMemcpyAsync(h_out + r.b, d_out + r.b, 4 * (r.e - r.b), cudaMemcpyDeviceToHost, ctx->copy_out));
+    APR_CUDA(cudaEventRecord(e_out[K], ctx->copy_out));
+    if (staged) {  // outputs out of the staging, chunk by chunk as they land
+        ctx->pool->wait();
+        next.store(0);
+        std::atomic<int> bad{0};
+        ctx->pool->start([&] {
+            for (size_t i; (i = next.fetch_add(1)) < pout.size();) {
+                if (cudaEventSynchronize(e_out[pout[i].chunk]) != cudaSuccess) {
+                    bad.store(1);
+                    continue;
+                }
+                std::memcpy(pout[i].dst, pout[i].src, 4 * pout[i].n);
+            }
+        });
+        ctx->pool->wait();
+        if (bad.load()) fail(APRGPU_ERR_CUDA, "pipelined convolve: a device-to-host copy failed");
+    }
     APR_CUDA(cudaStreamSynchronize(ctx->copy_out));
     APR_CUDA(cudaStreamSynchronize(s));
-
     return true;
 }
 
@@ -455,6 +604,8 @@ int aprgpu_ctx_free(aprgpu_ctx* ctx) {
         if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
         if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
         for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+        delete ctx->pool;
+        if (ctx->stage) cudaFreeHost(ctx->stage);
         delete ctx;
     });
 }

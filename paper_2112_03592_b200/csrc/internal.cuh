@@ -4,11 +4,14 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "aprgpu.h"
@@ -142,6 +145,29 @@ struct GpuBuf {  // owned device allocation (freed on release() or destruction; 
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Host worker threads of a context (api.cu): run one job at a time on every
+// worker, asynchronously to the caller (start ... wait).  Used by the
+// pageable host-pointer convolution to stage chunks through pinned memory.
+class HostPool {
+  public:
+    explicit HostPool(int n);
+    ~HostPool();
+    HostPool(const HostPool&) = delete;
+    HostPool& operator=(const HostPool&) = delete;
+    void start(std::function<void()> job);  // job() runs once on each worker
+    void wait();
+    int size() const { return static_cast<int>(th_.size()); }
+
+  private:
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    std::function<void()> job_;
+    uint64_t gen_ = 0;
+    int busy_ = 0;
+    bool stop_ = false;
+};
+
 }  // namespace aprgpu
 
 struct aprgpu_ctx {
@@ -151,6 +177,11 @@ struct aprgpu_ctx {
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> events;
     std::mutex pipe_mu;  // one pipelined call at a time per context (shares the streams and events)
+    // pageable host-pointer convolutions: pinned staging (inputs, then outputs) and the threads
+    // that copy through it (lazy; both under pipe_mu)
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+    aprgpu::HostPool* pool = nullptr;
     std::mutex mu;
     std::atomic<uint64_t> launches{0};
     int sm_count = 148;

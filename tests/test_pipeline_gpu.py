@@ -1,6 +1,8 @@
 """Host-pointer convolve_apr pipelined over z-chunks (api.cu,
 convolve_host_pipelined): with page-locked buffers the copies stream per chunk
-on two copy streams around per-chunk (Slab-restricted) passes.  The result must
+on two copy streams around per-chunk (Slab-restricted) passes; pageable
+buffers (numpy arrays here, std::vector in the C++ drop-in) are staged through
+pinned memory by the context's worker threads.  The result must
 be bit-identical to the device-pointer call, for every chunk count, both
 accumulation modes, the map and reconstruction tile paths, and the generic
 row kernel (anisotropic / 13^3 stencils)."""
@@ -24,6 +26,15 @@ def _host_call(dev, values, tree, dpyr, pad, accum):
     L.check(L.lib().aprgpu_convolve(dev.handle, hv.data_ptr(), ht.data_ptr() if tree.size else None, dpyr.handle,
                                     int(pad), accum, ho.data_ptr(), L.HOST, None))
     return ho.numpy().copy()
+
+
+def _pageable_call(dev, values, tree, dpyr, pad, accum):
+    hv = np.ascontiguousarray(values, np.float32)
+    ht = np.ascontiguousarray(tree, np.float32)
+    ho = np.full(dev.n_particles, np.nan, np.float32)
+    L.check(L.lib().aprgpu_convolve(dev.handle, hv.ctypes.data, ht.ctypes.data if ht.size else None, dpyr.handle,
+                                    int(pad), accum, ho.ctypes.data, L.HOST, None))
+    return ho
 
 
 def _device_call(dev, values, tree, dpyr, pad, accum):
@@ -61,6 +72,8 @@ def test_pipelined_host_convolve_bit_identical(name, chunks, monkeypatch):
                     got = _host_call(dev, values, tree, dpyr, pad, accum)
                     exp = _device_call(dev, values, tree, dpyr, pad, accum)
                     assert np.array_equal(G.bits(got), G.bits(exp)), (w.kz, accum, int(pad), path)
+                    got = _pageable_call(dev, values, tree, dpyr, pad, accum)
+                    assert np.array_equal(G.bits(got), G.bits(exp)), ("pageable", w.kz, accum, int(pad), path)
 
 
 def test_pipelined_host_convolve_c3(monkeypatch):
@@ -76,3 +89,5 @@ def test_pipelined_host_convolve_c3(monkeypatch):
             got = _host_call(dev, values, tree, dpyr, P.PadMode.Reflect, accum)
             exp = _device_call(dev, values, tree, dpyr, P.PadMode.Reflect, accum)
             assert np.array_equal(G.bits(got), G.bits(exp)), (k, accum)
+            got = _pageable_call(dev, values, tree, dpyr, P.PadMode.Reflect, accum)
+            assert np.array_equal(G.bits(got), G.bits(exp)), ("pageable", k, accum)
