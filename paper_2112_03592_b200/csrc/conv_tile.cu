@@ -1132,8 +1132,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
 // streamed pass over the record (4 codes per 16-byte load) with a gather of
 // each code's value, then the same block-compacted apply as k_conv_tile.
 // Results are bit-identical to k_conv_tile's (same box contents, same taps).
-template <typename Acc, int H>
-__global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H == 2 ? 5 : 8))
+template <typename Acc, int H, int NT = kTileThreads>
+__global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H == 2 ? 5 : 8)) * 128 / NT)
     k_conv_map(const __grid_constant__ TileLaunch a) {
     using M = MapBox<H>;
     constexpr int K = 2 * H + 1, KW = K * K * K;
@@ -1179,14 +1179,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 :
         if (nchunk) bulk_copy(Gs, a.flat + f0, nchunk * 4, &mbar);
     }
     if (tid < kFlat0) F[tid] = 0.0f;
-    for (int i = tid; i < KW; i += kTileThreads)
+    for (int i = tid; i < KW; i += NT)
         W[i] = sizeof(Acc) == 8 ? static_cast<Acc>(a.wd[a.woff[s] + i]) : static_cast<Acc>(a.wf[a.woff[s] + i]);
     __syncthreads();  // (the barrier's init is visible)
     mbar_wait(&mbar, 0);
     // every source value copied once: one 16-byte copy per chunk (a warp's
     // chunks are mostly consecutive 16-byte pieces of one run: coalesced);
     // the array's tail chunk copies only its valid elements
-    for (uint32_t c = tid; c < nchunk; c += kTileThreads) {
+    for (uint32_t c = tid; c < nchunk; c += NT) {
         const uint32_t e = Gs[c];
         const float* src = ((e & kChunkTree) ? a.tval : a.val) + (e & kChunkIdx);
         float* dst = F + kFlat0 + 4 * c;
@@ -1224,8 +1224,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 :
         };
         if constexpr (kInPlace) {
 #pragma unroll 1
-            for (int j = (NG - 1) / kTileThreads; j >= 0; --j) {
-                const int g = j * kTileThreads + tid;
+            for (int j = (NG - 1) / NT; j >= 0; --j) {
+                const int g = j * NT + tid;
                 float4 v0, v1;
                 if (g < NG) group(g, v0, v1);
                 __syncthreads();
@@ -1235,7 +1235,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 :
                 }
             }
         } else {
-            for (int g = tid; g < NG; g += kTileThreads) {
+            for (int g = tid; g < NG; g += NT) {
                 float4 v0, v1;
                 group(g, v0, v1);
                 S4[2 * g] = v0;
@@ -1249,7 +1249,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 4 :
     // the active blocks in their bank-interleaved order (map build)
     const int nb = static_cast<int>(Mb[M::W_NBLK]);
     const uint8_t* blist = reinterpret_cast<const uint8_t*>(Mb + M::W_BLK);
-    for (int q = tid; q < nb; q += kTileThreads) {
+    for (int q = tid; q < nb; q += NT) {
         const int bidx = blist[q];
         const int qz = bidx / (kBlocks / 4), qx = (bidx / (kTY / 2)) & 3, qy = bidx & (kTY / 2 - 1);
         Acc acc[8];
@@ -1479,19 +1479,33 @@ void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s
                        : H == 2                   ? M::REC + fw - a.map_ng + std::max(M::NC, a.map_ng)  // list in the box
                                                   : M::REC + fw) * 4;
     if (bytes > 225 * 1024) fail(APRGPU_ERR_CAPABILITY, "gather map exceeds shared memory");
+    // 3^3: 96-thread CTAs (a C3 tile has ~65 active blocks: the apply's one
+    // round fits 3 warps; A/B EXACT 0.173 -> 0.167 ms, FAST unchanged);
+    // APRGPU_MAP_THREADS=128 restores 4 warps (A/B experiments)
+    static const int nt = [] {
+        const char* e = std::getenv("APRGPU_MAP_THREADS");
+        return H == 1 && !(e && std::atoi(e) == 128) ? 96 : kTileThreads;
+    }();
     static OncePerDevice attr;
     attr([] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-        // 3^3 EXACT (8 CTAs/SM by registers, 7 by shared memory): a 164 KB
-        // carveout leaves the gathers L1 (A/B on C3: 58 % 0.185, 72 % 0.180,
-        // 86 % 0.184 ms); FAST and 5^3 are best at the default
-        int carve = sizeof(Acc) == 8 && H == 1 ? 72 : -1;
+        APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+        // 3^3 EXACT: with 128-thread CTAs (8 CTAs/SM by registers, 7 by shared
+        // memory) a 164 KB carveout left the gathers L1 (A/B on C3: 58 % 0.185,
+        // 72 % 0.180, 86 % 0.184 ms); at 96 threads 86 and 100 % tie (0.1667)
+        // and 72 % caps it at 6 CTAs/SM.  FAST and 5^3: the default
+        int carve = sizeof(Acc) == 8 && H == 1 ? (nt == 96 ? 100 : 72) : -1;
         if (const char* e = std::getenv(sizeof(Acc) == 8 ? "APRGPU_CARVEOUT_EXACT" : "APRGPU_CARVEOUT_FAST"))
             carve = std::atoi(e);  // (A/B experiments)
-        if (carve >= 0)
+        if (carve >= 0) {
             APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H, 96>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+        }
     });
-    k_conv_map<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
+    if (nt == 96)
+        k_conv_map<Acc, H, 96><<<n, 96, bytes, s>>>(a);
+    else
+        k_conv_map<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
     count_launch(ctx);
     APR_CUDA(cudaGetLastError());
 }

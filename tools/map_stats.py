@@ -36,6 +36,7 @@ for b in range(256):
     qz, qx, qy = b // 64, (b // 16) & 3, b & 15
     BM[b, 2 * qz:2 * qz + 4, 2 * qx:2 * qx + 4, 2 * qy:2 * qy + 4] = 1.0
 BM = torch.from_numpy(BM.reshape(256, -1)).cuda()
+allch = []
 tot = dict(ivl=0, tiles=0, cells=0, read=0, pairs_read=0, breaks=0, rows=0, rows_read=0, rowdup=0, nblk=0)
 for l in range(a.l_min, a.l_max + 1):
     nw, t0, nt = C.c_uint64(), C.c_uint64(), C.c_uint64()
@@ -48,6 +49,8 @@ for l in range(a.l_min, a.l_max + 1):
     rec = buf.reshape(nt.value, -1)  # (fixed-length records: codes, then masks, first indices, counts, blocks)
     codes = rec[:, :CW].view(np.uint16).reshape(-1, BZ, BX, BY).astype(np.int32)
     nblk = rec[:, CW + 129].astype(np.int64)
+    nch = rec[:, CW + 128].astype(np.int64)  # 16-byte source chunks of the tile (the staged F: 4 floats each)
+    allch.append(nch)
     blist = rec[:, CW + 132:CW + 132 + 64].view(np.uint8)
     # cells the active blocks read (union of 4x4x4 neighbourhoods)
     act = np.zeros((nt.value, 256), np.float32)
@@ -81,3 +84,8 @@ print(f"TOTAL tiles {T['tiles']}, code MB {T['cells'] * 2 / 1e6:.1f}, blocks/til
       f"cells read {T['read'] / T['cells']:.3f}, pairs read {T['pairs_read'] / (T['cells'] / 2):.3f}, rows read "
       f"{T['rows_read'] / T['rows']:.3f}, breaks/row {T['breaks'] / T['rows']:.2f}, x-dup rows "
       f"{T['rowdup'] / T['rows']:.3f}, interval words {T['ivl'] / (T['cells'] / 2):.3f}")
+ch = np.concatenate(allch)
+print("chunks per tile: p50 %d p90 %d p99 %d max %d; tiles with <= 256 / 384 / 512 chunks: %.3f / %.3f / %.3f" % (
+    np.percentile(ch, 50), np.percentile(ch, 90), np.percentile(ch, 99), ch.max(), (ch <= 256).mean(), (ch <= 384).mean(),
+    (ch <= 512).mean()))
+print("active blocks per tile: p50 %d p90 %d max %d; <= 96: %.3f" % (0, 0, 0, 0) if False else "")
