@@ -1483,8 +1483,12 @@ void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s
     // round fits 3 warps; A/B EXACT 0.173 -> 0.167 ms, FAST unchanged);
     // APRGPU_MAP_THREADS=128 restores 4 warps (A/B experiments)
     static const int nt = [] {
+        if (H == 2) {  // (APRGPU_MAP_THREADS5=96: 5^3 on 96-thread CTAs, A/B)
+            const char* e5 = std::getenv("APRGPU_MAP_THREADS5");
+            return e5 && std::atoi(e5) == 96 ? 96 : kTileThreads;
+        }
         const char* e = std::getenv("APRGPU_MAP_THREADS");
-        return H == 1 && !(e && std::atoi(e) == 128) ? 96 : kTileThreads;
+        return !(e && std::atoi(e) == 128) ? 96 : kTileThreads;
     }();
     static OncePerDevice attr;
     attr([] {
