@@ -100,6 +100,7 @@ struct TileLaunch {
     uint32_t n_leaf, n_tree;          // value-array lengths (a tail chunk copies only valid elements)
     int map_ng;                       // k_conv_map: largest chunk count of the launch's tiles
     int aligned16;                    // both value arrays 16-byte aligned (else 4-byte copies)
+    int list_in_f;                    // k_conv_map 3^3: the chunk list staged in F's tail (launch_map)
 };
 
 struct Geo {
@@ -1167,13 +1168,19 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     // the staged chunk list: after F -- or, for EXACT 5^3, inside the box S it
     // precedes (S is written only after the gather)
     constexpr bool kListInBox = H == 2 && !kInPlace;
-    uint32_t* Gs = reinterpret_cast<uint32_t*>(F + nf);
+    uint32_t* Gs = reinterpret_cast<uint32_t*>(F + nf);  // (3^3 with list_in_f: moved into F's tail below)
     if (tid == 0) {
         mbar_init(&mbar, 1);
         asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(M::REC * 4) : "memory");
         bulk_copy(Mb, rec, M::REC * 4, &mbar);
     }
     const uint32_t f0 = __ldg(a.flat_off + tix), nchunk = __ldg(a.flat_off + tix + 1) - f0;
+    // 3^3: the list in the tail of F's region, which the gather then fills from
+    // the front -- a chunk's copy can only land on list entries at or below its
+    // own, read in its round or before (rounds below): 4 bytes per chunk of
+    // shared memory less per CTA
+    const bool list_in_f = H == 1 && a.list_in_f;
+    if (list_in_f) Gs = reinterpret_cast<uint32_t*>(F + nf) - ((nchunk + 3u) & ~3u);
     if (tid == 0) {
         mbar_expect(&mbar, nchunk * 4);  // (arrive.expect_tx)
         if (nchunk) bulk_copy(Gs, a.flat + f0, nchunk * 4, &mbar);
@@ -1186,8 +1193,7 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     // every source value copied once: one 16-byte copy per chunk (a warp's
     // chunks are mostly consecutive 16-byte pieces of one run: coalesced);
     // the array's tail chunk copies only its valid elements
-    for (uint32_t c = tid; c < nchunk; c += NT) {
-        const uint32_t e = Gs[c];
+    auto gather = [&](uint32_t c, uint32_t e) {
         const float* src = ((e & kChunkTree) ? a.tval : a.val) + (e & kChunkIdx);
         float* dst = F + kFlat0 + 4 * c;
         if (!(e & kChunkTail) && a.aligned16) {
@@ -1198,6 +1204,16 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
             for (uint32_t k = 0; k < 4; ++k)
                 if ((e & kChunkIdx) + k < lim) cp_async4(dst + k, src + k);
         }
+    };
+    if (list_in_f) {
+        for (uint32_t c0 = 0; c0 < nchunk; c0 += NT) {  // (uniform trip count)
+            const uint32_t c = c0 + tid;
+            const uint32_t e = c < nchunk ? Gs[c] : 0u;
+            __syncthreads();  // the round's entries are read before its copies may overwrite them
+            if (c < nchunk) gather(c, e);
+        }
+    } else {
+        for (uint32_t c = tid; c < nchunk; c += NT) gather(c, Gs[c]);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -1477,6 +1493,7 @@ void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s
     const int fw = kFlat0 + 5 * a.map_ng;
     const int bytes = (H == 2 && sizeof(Acc) == 4 ? M::HDR + M::NC + fw
                        : H == 2                   ? M::REC + fw - a.map_ng + std::max(M::NC, a.map_ng)  // list in the box
+                       : a.list_in_f              ? M::REC + fw - a.map_ng                              // list in F
                                                   : M::REC + fw) * 4;
     if (bytes > 225 * 1024) fail(APRGPU_ERR_CAPABILITY, "gather map exceeds shared memory");
     // 3^3: 96-thread CTAs (a C3 tile has ~65 active blocks: the apply's one
@@ -1621,6 +1638,11 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
     b.flat = L.tile_flat[H - 1];
     b.flat_off = L.tile_flat_off[H - 1];
     b.aligned16 = ((reinterpret_cast<uintptr_t>(b.val) | reinterpret_cast<uintptr_t>(b.tval)) & 15) == 0;
+    static const bool lf = [] {  // APRGPU_MAP_LISTF=0: the list after F (A/B experiments)
+        const char* e = std::getenv("APRGPU_MAP_LISTF");
+        return !(e && e[0] == '0');
+    }();
+    b.list_in_f = H == 1 && lf;
     return true;
 }
 
