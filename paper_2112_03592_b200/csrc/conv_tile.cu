@@ -1179,7 +1179,7 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     // the front -- a chunk's copy can only land on list entries at or below its
     // own, read in its round or before (rounds below): 4 bytes per chunk of
     // shared memory less per CTA
-    const bool list_in_f = H == 1 && a.list_in_f;
+    const bool list_in_f = (H == 1 || kInPlace) && a.list_in_f;
     if (list_in_f) Gs = reinterpret_cast<uint32_t*>(F + nf) - ((nchunk + 3u) & ~3u);
     if (tid == 0) {
         mbar_expect(&mbar, nchunk * 4);  // (arrive.expect_tx)
@@ -1491,26 +1491,22 @@ void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s
     // [record (FAST 5^3: header + box)][F: kFlat0 + 4 chunks][chunk list][EXACT 5^3: box]
     using M = MapBox<H>;
     const int fw = kFlat0 + 5 * a.map_ng;
-    const int bytes = (H == 2 && sizeof(Acc) == 4 ? M::HDR + M::NC + fw
+    const int lf = a.list_in_f ? a.map_ng : 0;  // (the list in F's tail: no words of its own)
+    const int bytes = (H == 2 && sizeof(Acc) == 4 ? M::HDR + M::NC + fw - lf
                        : H == 2                   ? M::REC + fw - a.map_ng + std::max(M::NC, a.map_ng)  // list in the box
-                       : a.list_in_f              ? M::REC + fw - a.map_ng                              // list in F
-                                                  : M::REC + fw) * 4;
+                                                  : M::REC + fw - lf) * 4;
     if (bytes > 225 * 1024) fail(APRGPU_ERR_CAPABILITY, "gather map exceeds shared memory");
     // 3^3: 96-thread CTAs (a C3 tile has ~65 active blocks: the apply's one
     // round fits 3 warps; A/B EXACT 0.173 -> 0.167 ms, FAST unchanged);
     // APRGPU_MAP_THREADS=128 restores 4 warps (A/B experiments)
-    static const int nt = [] {
-        if (H == 2) {  // (APRGPU_MAP_THREADS5=96: 5^3 on 96-thread CTAs, A/B)
-            const char* e5 = std::getenv("APRGPU_MAP_THREADS5");
-            return e5 && std::atoi(e5) == 96 ? 96 : kTileThreads;
-        }
+    static const int nt = [] {  // (5^3 on 96 threads measured slower: 0.364 -> 0.376 ms EXACT)
         const char* e = std::getenv("APRGPU_MAP_THREADS");
-        return !(e && std::atoi(e) == 128) ? 96 : kTileThreads;
+        return H == 1 && !(e && std::atoi(e) == 128) ? 96 : kTileThreads;
     }();
     static OncePerDevice attr;
     attr([] {
         APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-        APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+        APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H, (H == 1 ? 96 : kTileThreads)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
         // 3^3 EXACT: with 128-thread CTAs (8 CTAs/SM by registers, 7 by shared
         // memory) a 164 KB carveout left the gathers L1 (A/B on C3: 58 % 0.185,
         // 72 % 0.180, 86 % 0.184 ms); at 96 threads 86 and 100 % tie (0.1667)
@@ -1520,11 +1516,11 @@ void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s
             carve = std::atoi(e);  // (A/B experiments)
         if (carve >= 0) {
             APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-            APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H, 96>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            APR_CUDA(cudaFuncSetAttribute(k_conv_map<Acc, H, (H == 1 ? 96 : kTileThreads)>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         }
     });
     if (nt == 96)
-        k_conv_map<Acc, H, 96><<<n, 96, bytes, s>>>(a);
+        k_conv_map<Acc, H, (H == 1 ? 96 : kTileThreads)><<<n, nt, bytes, s>>>(a);
     else
         k_conv_map<Acc, H><<<n, kTileThreads, bytes, s>>>(a);
     count_launch(ctx);
@@ -1642,7 +1638,7 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
         const char* e = std::getenv("APRGPU_MAP_LISTF");
         return !(e && e[0] == '0');
     }();
-    b.list_in_f = H == 1 && lf;
+    b.list_in_f = lf;  // (3^3 and FAST 5^3; EXACT 5^3 keeps its list inside the box)
     return true;
 }
 
