@@ -325,7 +325,7 @@ def test_nonempty_row_index_and_init_tree_front_doors():
     assert t.equals(apr.tree_access)
 
 
-@pytest.mark.parametrize("name", ["c1_256", "spheres64", "random_apr_03", "random_apr_09", "dense16"])
+@pytest.mark.parametrize("name", ["c1_256", "spheres64", "random_apr_03", "random_apr_09", "dense16", "C3"])
 def test_rebuild_index_equals_upload_lists(name, monkeypatch):
     """aprgpu_rebuild_index (the paper protocol's per-call index step): the
     non-empty row lists and occupied-tile lists it recomputes equal the ones
@@ -333,9 +333,13 @@ def test_rebuild_index_equals_upload_lists(name, monkeypatch):
     monkeypatch.setenv("APRGPU_VERIFY_INDEX", "1")
     import subprocess
     import sys
-    code = ("import sys; sys.path[:0]=['tests','.']; import goldens as G; d=G.load(%r); "
-            "a=G.product_apr(d).device(); a.rebuild_index_ptr(0); import torch; torch.cuda.synchronize(); print('ok')"
-            % name)
+    if name == "C3":  # (BASELINE config 3, built on the device)
+        make = ("from paper_2112_03592_b200 import synth; a=synth.build_spheres_apr(1024, count=48, rmin=24.0, "
+                "rmax=80.0, blur=2.0, seed=42, rel_error=0.1)[0].device(); ")
+    else:
+        make = "import goldens as G; a=G.product_apr(G.load(%r)).device(); " % name
+    code = ("import sys; sys.path[:0]=['tests','.']; " + make +
+            "a.rebuild_index_ptr(0); import torch; torch.cuda.synchronize(); print('ok')")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                        cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
