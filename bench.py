@@ -363,7 +363,7 @@ def run_ours(args, rank, world):
             tpx = min(pt[1:])
             pixels_conv = {"ms": round(tpx * 1e3, 4), "gbs_pixel_equiv": round(4 * n_pix / tpx / 1e9, 1),
                            "hbm_frac": round(8 * n_pix / tpx / 1e9 / peaks()[0], 4),
-                           "note": "convolve_pixels of the reconstructed image (k_convolve_pixels), best of 2 "
+                           "note": "convolve_pixels of the reconstructed image (k_convolve_pixels_zreg), best of 2 "
                                    "warm runs, same accumulation mode as the headline"}
         del img
 
@@ -696,6 +696,59 @@ def run_reference(args, rank, world):
             "e2e": {"value": v, "unit": "GB/s (pixel-equivalent)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+DIMS = {"c1": (256, 256, 256), "c3": (1024, 1024, 1024), "c4": (4096, 4096, 2048)}
+
+
+def write_bench_csv(path: str, res: dict, args) -> None:
+    """Appends the result as rows of the reference's bench CSV schema
+    (write_bench_csv, bench.hpp:33-42): image_id, dims, cr, op, stencil_size,
+    wall_time_s, effective_throughput_Bps (4 bytes per pixel / time,
+    metrics.hpp:15-21), memory_bytes_apr (particle in/out + interior values +
+    the u16 y indices; the row arrays are not counted), memory_bytes_pixels
+    (in + out), threads (host threads for CPU rows; 0 for GPU rows).  The op
+    names the protocol: conv_apr (conv-only, device-resident), conv_apr_e2e
+    (host buffers), conv_apr_paper (index + tree + conv), conv_pixels."""
+    cfg = res.get("config", {})
+    n_pix, n_p, n_t = cfg.get("pixels", 0), cfg.get("particles", 0), cfg.get("interior_nodes", 0)
+    dims = "x".join(str(d) for d in DIMS.get(args.config, (0, 0, 0)))
+    mem_apr, mem_pix = 8 * n_p + 4 * n_t + 2 * (n_p + n_t), 8 * n_pix
+    rows = []
+
+    def row(image, op, k, t_s, threads):
+        if t_s and t_s > 0:
+            rows.append(f"{image},{dims},{cfg.get('cr', 0)},{op},{k},{t_s:.9g},{4 * n_pix / t_s:.6g},{mem_apr},{mem_pix},"
+                        f"{threads}")
+
+    img = f"{args.config.upper()}"
+    k = args.stencil
+    if res.get("impl") == "reference":
+        cb = res.get("cpu_baseline") or {}
+        row(img + "/reference", "conv_apr", k, res.get("ms_per_step", 0) / 1e3, cb.get("cores", 0))
+    else:
+        row(f"{img}/{args.accum}", "conv_apr", k, res.get("ms_per_step", 0) / 1e3, 0)
+        for name, v in (res.get("variants") or {}).items():
+            kk, acc = name.split("_")
+            row(f"{img}/{acc}", "conv_apr", int(kk[1:]), v.get("ms_per_step", 0) / 1e3, 0)
+        e2e = res.get("e2e") or {}
+        row(f"{img}/{args.accum}", "conv_apr_e2e", k, e2e.get("ms_per_step", 0) / 1e3, 0)
+        pp = res.get("paper_protocol") or {}
+        row(f"{img}/{args.accum}", "conv_apr_paper", k, pp.get("ms_per_step", 0) / 1e3, 0)
+        px = res.get("convolve_pixels") or {}
+        row(f"{img}/{args.accum}", "conv_pixels", k, px.get("ms", 0) / 1e3, 0)
+        cb = res.get("cpu_baseline") or {}
+        if cb.get("ms_per_step"):
+            row(img + "/reference", "conv_apr", k, cb["ms_per_step"] / 1e3, cb.get("cores", 0))
+            st = cb.get("single_thread") or {}
+            row(img + "/reference", "conv_apr", k, st.get("ms_per_step", 0) / 1e3, st.get("cores", 0))
+    new = not os.path.exists(path)
+    with open(path, "a") as f:
+        if new:
+            f.write("image_id,dims,cr,op,stencil_size,wall_time_s,effective_throughput_Bps,memory_bytes_apr,"
+                    "memory_bytes_pixels,threads\n")
+        for r in rows:
+            f.write(r + "\n")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -708,6 +761,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rl-iters", type=int, default=10)
+    ap.add_argument("--csv", default=None, help="also append the result to this CSV (bench.hpp:33-42 schema)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -716,7 +770,10 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        print(json.dumps(run_reference(args, rank, world)), flush=True)
+        res = run_reference(args, rank, world)
+        print(json.dumps(res), flush=True)
+        if args.csv:
+            write_bench_csv(args.csv, res, args)
         return
     # APRGPU_BENCH_SLAB=1 runs the N > 1 path (NCCL, z-slabs) with whatever world
     # size torchrun gives, 1 included: how the slab path is exercised on one GPU
@@ -728,6 +785,8 @@ def main():
     res = run_slab(args, rank, world) if slab else run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(res), flush=True)
+        if args.csv:
+            write_bench_csv(args.csv, res, args)
     if slab:
         import torch
         torch.distributed.destroy_process_group()
