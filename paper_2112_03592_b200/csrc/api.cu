@@ -416,6 +416,7 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
         return false;
     aprgpu_ctx* ctx = apr->ctx;
     std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+    aprgpu::NvtxRange nr(staged ? "aprgpu: host pipeline (pageable, staged)" : "aprgpu: host pipeline (pinned)");
     if (!host_pipe_plan(apr, chunks, s)) return false;
     const auto& P = apr->host_pipe;
     const int K = P.K;
@@ -627,7 +628,7 @@ int aprgpu_launch_count(aprgpu_ctx* ctx, uint64_t* out) {
 int aprgpu_upload_access(aprgpu_ctx* ctx, const aprgpu_access_desc* leaf, const aprgpu_access_desc* tree,
                          const int32_t source_dims[3], aprgpu_apr** out) {
     aprgpu_apr* apr = nullptr;
-    int st = guard([&] {
+    int st = guard("aprgpu_upload_access", [&] {
         need(ctx && leaf && source_dims && out, "null argument");
         std::lock_guard<std::mutex> lk(ctx->mu);
         DeviceGuard g(ctx->device);
@@ -673,7 +674,7 @@ bool grids_match(const aprgpu_access_desc* d, const int32_t dims[3]) {
 int aprgpu_validate_access(aprgpu_ctx* ctx, const aprgpu_access_desc* d, const int32_t source_dims[3], int* ok,
                            char* msg, size_t msg_cap) {
     aprgpu_apr* tmp = nullptr;
-    int st = guard([&] {
+    int st = guard("aprgpu_validate_access", [&] {
         need(ctx && d && source_dims && ok, "null argument");
         std::string m;
         auto verdict = [&](std::string v) { m = std::move(v); };
@@ -861,7 +862,7 @@ int aprgpu_apr_map_tiles(const aprgpu_apr* apr, uint64_t* built, uint64_t* n_til
 
 int aprgpu_download_access(const aprgpu_apr* apr, int which, uint16_t* y_idx, uint64_t* xz_end,
                            uint64_t* level_offset, int32_t* z_dim, int32_t* x_dim, int32_t* y_dim) {
-    return guard([&] {
+    return guard("aprgpu_download_access", [&] {
         need(apr != nullptr, "null argument");
         need(which == APRGPU_LEAF || which == APRGPU_TREE, "bad access selector");
         DeviceGuard g(apr->ctx->device);
@@ -886,7 +887,7 @@ int aprgpu_download_access(const aprgpu_apr* apr, int which, uint16_t* y_idx, ui
 
 int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, uint16_t* y_min, uint16_t* y_max,
                      uint64_t cap, uint64_t* count) {
-    return guard([&] {
+    return guard("aprgpu_row_index", [&] {
         need(apr && count, "null argument");
         const aprgpu::DevAccess& a = apr->leaf;
         if (level < a.l_min || level > a.l_max) fail(APRGPU_ERR_RANGE, "row_index: level out of range");
@@ -897,7 +898,7 @@ int aprgpu_row_index(const aprgpu_apr* apr, int level, int32_t* z, int32_t* x, u
 }
 
 int aprgpu_rebuild_index(aprgpu_apr* apr, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_rebuild_index", [&] {
         need(apr, "null argument");
         DeviceGuard g(apr->ctx->device);
         cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
@@ -907,7 +908,7 @@ int aprgpu_rebuild_index(aprgpu_apr* apr, void* stream) {
 }
 
 int aprgpu_fill_tree(aprgpu_apr* apr, const float* leaf, float* tree, int ptr_kind, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_fill_tree", [&] {
         need(apr && leaf && (tree || apr->tree.n_particles == 0), "null argument");
         DeviceGuard g(apr->ctx->device);
         cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
@@ -1056,7 +1057,7 @@ int aprgpu_pyramid_level(const aprgpu_pyramid* p, int level, int32_t k3[3], floa
 
 int aprgpu_convolve(aprgpu_apr* apr, const float* values, const float* tree_values, const aprgpu_pyramid* pyr,
                     int pad_mode, int accum, float* out, int ptr_kind, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_convolve", [&] {
         need(apr && values && pyr && out, "null argument");
         need(tree_values || apr->tree.n_particles == 0, "tree values are required");
         need(pad_mode == APRGPU_PAD_ZERO || pad_mode == APRGPU_PAD_REFLECT, "bad pad mode");
@@ -1125,7 +1126,7 @@ extern "C" {
 
 int aprgpu_reconstruct_level(aprgpu_apr* apr, const float* values, const float* tree_values, int level, float* out,
                              int ptr_kind, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_reconstruct_level", [&] {
         need(apr != nullptr, "null argument");
         const aprgpu::DevAccess& L = apr->leaf;
         if (level < L.l_min || level > L.l_max) aprgpu::fail(APRGPU_ERR_RANGE, "reconstruct_level: level out of range");
@@ -1139,7 +1140,7 @@ int aprgpu_reconstruct_level(aprgpu_apr* apr, const float* values, const float* 
 
 int aprgpu_reconstruct_patch(aprgpu_apr* apr, const float* values, const float* tree_values,
                              const aprgpu_patch_spec* spec, float* out, int ptr_kind, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_reconstruct_patch", [&] {
         need(apr && spec, "null argument");
         const aprgpu::DevAccess& L = apr->leaf;
         const int l = spec->level;
@@ -1165,7 +1166,7 @@ int aprgpu_rl(aprgpu_apr* apr, const float* observed, const float* psf, int kz, 
 int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estimate_in, const float* psf, int kz,
                      int kx, int ky, int iterations, double epsilon, int accum, float* out, int ptr_kind,
                      void* stream) {
-    return guard([&] {
+    return guard("aprgpu_rl_resume", [&] {
         need(apr && observed && psf && out, "null argument");
         need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
         need(accum == APRGPU_ACCUM_EXACT || accum == APRGPU_ACCUM_FAST, "bad accumulation mode");
@@ -1315,7 +1316,7 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
 
 int aprgpu_fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi,
                           void* stream) {
-    return guard([&] {
+    return guard("aprgpu_fill_tree_sums", [&] {
         need(apr && (leaf || apr->leaf.n_particles == 0), "null argument");
         DeviceGuard g(apr->ctx->device);
         aprgpu::fill_tree_sums(apr, leaf, lt_lo, lt_hi, z_lo, z_hi, aprgpu::pick_stream(apr->ctx, stream));
@@ -1337,7 +1338,7 @@ int aprgpu_tree_scratch(aprgpu_apr* apr, double** vsum, double** wsum) {
 }
 
 int aprgpu_fill_tree_finalize(aprgpu_apr* apr, float* tree, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_fill_tree_finalize", [&] {
         need(apr && (tree || apr->tree.n_particles == 0), "null argument");
         DeviceGuard g(apr->ctx->device);
         aprgpu::fill_tree_finalize(apr, tree, aprgpu::pick_stream(apr->ctx, stream));
@@ -1352,7 +1353,7 @@ int aprgpu_convolve_slab(aprgpu_apr* apr, const float* values, const float* tree
 int aprgpu_convolve_slab_band(aprgpu_apr* apr, const float* values, const float* tree_values,
                               const aprgpu_pyramid* pyr, int pad_mode, int accum, int lc, int z_lo, int z_hi,
                               int replicated, float* out, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_convolve_slab_band", [&] {
         need(apr && values && pyr && out, "null argument");
         need(tree_values || apr->tree.n_particles == 0, "tree values are required");
         need(pad_mode == APRGPU_PAD_ZERO || pad_mode == APRGPU_PAD_REFLECT, "bad pad mode");
@@ -1374,7 +1375,7 @@ int aprgpu_convolve_slab_band(aprgpu_apr* apr, const float* values, const float*
 int aprgpu_generate_spheres(aprgpu_ctx* ctx, int nz, int nx, int ny, int count, double min_radius,
                             double max_radius, double background, double min_intensity, double max_intensity,
                             double blur_sigma, uint64_t seed, float* out, int ptr_kind) {
-    return guard([&] {
+    return guard("aprgpu_generate_spheres", [&] {
         need(ctx && out, "null argument");
         need(nz > 0 && nx > 0 && ny > 0 && count >= 0, "bad dimensions");
         DeviceGuard g(ctx->device);
@@ -1403,7 +1404,7 @@ int aprgpu_build_apr(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int n
 int aprgpu_build_apr_params(aprgpu_ctx* ctx, const float* volume, int nz, int nx, int ny,
                             const aprgpu_build_params* params, int ptr_kind, aprgpu_apr** out) {
     aprgpu_apr* apr = nullptr;
-    int st = guard([&] {
+    int st = guard("aprgpu_build_apr_params", [&] {
         need(ctx && volume && out, "null argument");
         DeviceGuard g(ctx->device);
         std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1439,7 +1440,7 @@ int aprgpu_build_apr_params(aprgpu_ctx* ctx, const float* volume, int nz, int nx
 
 int aprgpu_tile_apr(aprgpu_apr* src, int tz, int tx, int ty, aprgpu_apr** out) {
     aprgpu_apr* big = nullptr;
-    int st = guard([&] {
+    int st = guard("aprgpu_tile_apr", [&] {
         need(src && out && tz > 0 && tx > 0 && ty > 0, "bad argument");
         aprgpu_ctx* ctx = src->ctx;
         DeviceGuard g(ctx->device);
@@ -1458,7 +1459,7 @@ int aprgpu_tile_apr(aprgpu_apr* src, int tz, int tx, int ty, aprgpu_apr** out) {
 
 int aprgpu_tile_values(aprgpu_apr* src, aprgpu_apr* big, int tz, int tx, int ty, const float* src_values,
                        float* big_values) {
-    return guard([&] {
+    return guard("aprgpu_tile_values", [&] {
         need(src && big && src_values && big_values, "null argument");
         need(src->ctx == big->ctx, "APRs belong to different contexts");
         DeviceGuard g(src->ctx->device);
@@ -1470,7 +1471,7 @@ int aprgpu_tile_values(aprgpu_apr* src, aprgpu_apr* big, int tz, int tx, int ty,
 
 int aprgpu_convolve_pixels(aprgpu_ctx* ctx, const float* in, int nz, int nx, int ny, const float* w, int kz, int kx,
                            int ky, int pad_mode, int accum, float* out, int ptr_kind, void* stream) {
-    return guard([&] {
+    return guard("aprgpu_convolve_pixels", [&] {
         need(ctx && in && w && out, "null argument");
         need(pad_mode == APRGPU_PAD_ZERO || pad_mode == APRGPU_PAD_REFLECT, "bad pad mode");
         need(accum == APRGPU_ACCUM_EXACT || accum == APRGPU_ACCUM_FAST, "bad accumulation mode");
@@ -1504,7 +1505,7 @@ int aprgpu_convolve_pixels(aprgpu_ctx* ctx, const float* in, int nz, int nx, int
 }
 
 int aprgpu_load_apr(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out) {
-    return guard([&] {
+    return guard("aprgpu_load_apr", [&] {
         need(ctx && path && out, "null argument");
         DeviceGuard g(ctx->device);
         std::string msg;
@@ -1514,7 +1515,7 @@ int aprgpu_load_apr(aprgpu_ctx* ctx, const char* path, aprgpu_apr** out) {
 }
 
 int aprgpu_save_apr(aprgpu_apr* apr, const char* path, const float* values, int ptr_kind) {
-    return guard([&] {
+    return guard("aprgpu_save_apr", [&] {
         need(apr && path && (values || apr->leaf.n_particles == 0), "null argument");
         need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
         DeviceGuard g(apr->ctx->device);

@@ -1585,6 +1585,7 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
                     __atomic_store_n(&L.tile_map_fail[H - 1][pm][m.lvl[j]], 1, __ATOMIC_RELEASE);
                 return false;
             }
+            NvtxRange nr(H == 1 ? "aprgpu: gather-map build (3^3)" : "aprgpu: gather-map build (5^3)");
             ensure_tile_flat<H>(apr, s);
             // built into local buffers, published only after the build kernel
             // has completed and passed the overflow check

@@ -12,9 +12,11 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "aprgpu.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace aprgpu {
 
@@ -41,6 +43,17 @@ struct Error : std::runtime_error {
 // ---- C-ABI plumbing (api.cu, multi.cu) --------------------------------------
 std::string& last_error_slot();  // thread-local message of the last failed call
 
+// NVTX ranges (header-only NVTX 3: free unless a tool -- Nsight Systems,
+// `ncu --nvtx` -- is attached): one per compute entry point of the C-ABI,
+// named after it, and one per internal phase (gather-map builds, the host
+// pipeline's chunks, the multi-device passes), nested inside it.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Runs f, converting exceptions into the C-ABI status (and the thread's message).
 template <class F>
 int guard(F&& f) {
@@ -57,6 +70,13 @@ int guard(F&& f) {
         last_error_slot() = e.what();
         return APRGPU_ERR_INVALID;
     }
+}
+
+// guard() inside an NVTX range named after the entry point
+template <class F>
+int guard(const char* range, F&& f) {
+    NvtxRange r(range);
+    return guard(std::forward<F>(f));
 }
 
 inline void need(bool cond, const char* what) {

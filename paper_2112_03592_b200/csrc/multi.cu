@@ -162,7 +162,7 @@ int aprgpu_multi_create(const int* devices, int n_slabs, const aprgpu_access_des
                         const aprgpu_access_desc* tree, const int32_t source_dims[3], int halo, aprgpu_multi** out) {
     using namespace aprgpu;
     aprgpu_multi* m = nullptr;
-    const int st = guard([&] {
+    const int st = guard("aprgpu_multi_create", [&] {
         need(devices && leaf && source_dims && out && n_slabs >= 1, "null argument");
         need(halo >= 1 && halo <= 6, "halo must be 1..6 rows (half-width of a stencil <= 13)");
         m = new aprgpu_multi;
@@ -272,7 +272,7 @@ int aprgpu_multi_info(const aprgpu_multi* m, int* n_slabs, int* cut_level, int32
 int aprgpu_multi_convolve(aprgpu_multi* m, const float* values, const float* tree_values, const float* w,
                           const int32_t* k3, int l_min, int l_max, int pad_mode, int accum, float* out) {
     using namespace aprgpu;
-    return guard([&] {
+    return guard("aprgpu_multi_convolve", [&] {
         need(m && values && w && k3 && out, "null argument");
         need(tree_values || m->n_tree == 0, "tree values are required");
         need(pad_mode == APRGPU_PAD_ZERO || pad_mode == APRGPU_PAD_REFLECT, "bad pad mode");
@@ -314,6 +314,7 @@ int aprgpu_multi_convolve(aprgpu_multi* m, const float* values, const float* tre
                             d.out.as<float>(), epi, d.compute, slab);
         };
         // 1. uploads, then the interior of every slab
+        std::unique_ptr<NvtxRange> ph(new NvtxRange("aprgpu_multi: uploads + interior bands"));
         for (int s = 0; s < p.n; ++s) {
             SlabDev& d = m->slabs[s];
             DeviceGuard g(d.device);
@@ -327,6 +328,7 @@ int aprgpu_multi_convolve(aprgpu_multi* m, const float* values, const float* tre
             conv(s, lo, hi, true);
         }
         // 2. halos: each destination's copy stream waits for its source's upload
+        ph.reset(new NvtxRange("aprgpu_multi: halo exchange (peer copies)"));
         for (int s = 0; s < p.n; ++s) {
             SlabDev& d = m->slabs[s];
             DeviceGuard g(d.device);
@@ -341,6 +343,7 @@ int aprgpu_multi_convolve(aprgpu_multi* m, const float* values, const float* tre
             APR_CUDA(cudaEventRecord(d.halos, d.copy));
         }
         // 3. the boundary bands, 4. the owned outputs back
+        ph.reset(new NvtxRange("aprgpu_multi: boundary bands + download"));
         for (int s = 0; s < p.n; ++s) {
             SlabDev& d = m->slabs[s];
             DeviceGuard g(d.device);
