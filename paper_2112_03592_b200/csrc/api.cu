@@ -69,6 +69,7 @@ void upload_one(aprgpu_ctx* ctx, const aprgpu_access_desc* d, aprgpu::DevAccess&
 
 void free_apr(aprgpu_apr* apr) {
     if (apr->scratch_ev) cudaEventDestroy(apr->scratch_ev);
+    if (apr->index_ev) cudaEventDestroy(apr->index_ev);
     apr->scratch_ev = nullptr;
     apr->leaf.release();
     apr->tree.release();
@@ -83,15 +84,18 @@ void free_apr(aprgpu_apr* apr) {
 // fill on one stream completes before the next caller's kernels touch the sums).
 struct ScratchGuard {
     std::lock_guard<std::mutex> lk;
-    aprgpu_apr* apr;
+    cudaEvent_t& ev;
     cudaStream_t s;
-    ScratchGuard(aprgpu_apr* a, cudaStream_t st) : lk(a->exec_mu), apr(a), s(st) {
-        if (!a->scratch_ev)
-            APR_CUDA(cudaEventCreateWithFlags(&a->scratch_ev, cudaEventDisableTiming));
+    // the APR's shared scratch (fill_tree sums, host staging, RL state) by default;
+    // a scratch of its own (mutex + event) otherwise
+    ScratchGuard(aprgpu_apr* a, cudaStream_t st) : ScratchGuard(a->exec_mu, a->scratch_ev, st) {}
+    ScratchGuard(std::mutex& mu, cudaEvent_t& e, cudaStream_t st) : lk(mu), ev(e), s(st) {
+        if (!ev)
+            APR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         else
-            APR_CUDA(cudaStreamWaitEvent(s, a->scratch_ev, 0));
+            APR_CUDA(cudaStreamWaitEvent(s, ev, 0));
     }
-    ~ScratchGuard() { cudaEventRecord(apr->scratch_ev, s); }
+    ~ScratchGuard() { cudaEventRecord(ev, s); }
 };
 
 aprgpu::HostStencil make_host_stencil(const float* w, int kz, int kx, int ky) {
@@ -902,7 +906,8 @@ int aprgpu_rebuild_index(aprgpu_apr* apr, void* stream) {
         need(apr, "null argument");
         DeviceGuard g(apr->ctx->device);
         cudaStream_t s = aprgpu::pick_stream(apr->ctx, stream);
-        ScratchGuard sg(apr, s);
+        // (its own scratch: the index step may overlap fill_tree on another stream)
+        ScratchGuard sg(apr->index_mu, apr->index_ev, s);
         aprgpu::rebuild_index_device(apr, s);
     });
 }

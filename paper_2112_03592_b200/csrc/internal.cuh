@@ -226,6 +226,8 @@ struct aprgpu_apr {
     aprgpu::GpuBuf tmp;                    // misc
     aprgpu::GpuBuf built_values;           // leaf values sampled by aprgpu_build_apr / read by aprgpu_load_apr
     aprgpu::GpuBuf index_scratch;          // aprgpu_rebuild_index (the paper protocol's per-call index step)
+    std::mutex index_mu;                   // ... and its own scratch guard (api.cu ScratchGuard)
+    cudaEvent_t index_ev = nullptr;
     // z-chunk plan of host-pointer convolutions (api.cu, HostPipe): chunk of S
     // finest planes; levels >= lc split per chunk, [l - lc][j] = first particle
     // of chunk j's rows at level l (j = 0..K)

@@ -119,3 +119,34 @@ def test_concurrent_device_pointer_convolve_fresh_apr(name):
 
     for k, got in _run_threads(job, 6):
         assert np.array_equal(G.bits(got), G.bits(exp[k][1])), k
+
+
+@pytest.mark.parametrize("name", ["spheres64", "c1_256"])
+def test_index_step_beside_fill_tree(name):
+    """The paper protocol's index step (aprgpu_rebuild_index, its own scratch
+    guard) on one stream while fill_tree + convolve_apr run on another, as
+    bench.py's paper step does: the tree values and outputs stay bit-identical
+    to the reference golden ones."""
+    import torch
+    d = G.load(name)
+    apr = G.product_apr(d)
+    a = apr.access
+    dev = apr.device()
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, 3), a.l_min, a.l_max, P.PyramidMode.Restricted).device(dev.ctx)
+    v = torch.from_numpy(np.ascontiguousarray(d["values"], np.float32)).cuda()
+    tv = torch.empty(max(dev.n_tree, 1), dtype=torch.float32, device="cuda")
+    out = torch.empty(dev.n_particles, dtype=torch.float32, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ref = None
+    for i in range(20):
+        tv.fill_(float("nan"))
+        dev.rebuild_index_ptr(s2.cuda_stream)
+        dev.fill_tree_ptr(v.data_ptr(), tv.data_ptr(), s1.cuda_stream)
+        dev.convolve_ptr(v.data_ptr(), tv.data_ptr(), pyr, 1, L.ACCUM_EXACT, out.data_ptr(), s1.cuda_stream)
+        torch.cuda.synchronize()
+        t = tv.cpu().numpy()[:dev.n_tree]
+        assert np.array_equal(G.bits(t), G.bits(d["tree_values"])), i
+        o = out.cpu().numpy()
+        if ref is None:
+            ref = o.copy()
+        assert np.array_equal(G.bits(o), G.bits(ref)), i
