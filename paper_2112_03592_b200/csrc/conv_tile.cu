@@ -1731,17 +1731,19 @@ struct LevelTiles {
 // in flight (a warp per row is latency-bound on its work -> rb -> y chain);
 // a row's y are ascending, so a lane stores only where the tile changes from
 // its left neighbour (a shuffle, not a reload)
+template <int LPR>  // lanes per row (32 / LPR rows per warp)
 __global__ void k_mark_tiles_all(const uint32_t* __restrict__ work, const uint64_t* __restrict__ n_work_p,
                                  const __grid_constant__ LevelTiles lt, const uint32_t* __restrict__ rb,
                                  const uint16_t* __restrict__ y, uint8_t* __restrict__ flags) {
-    const int lane = threadIdx.x & 31, sub = lane >> 3, sl = lane & 7;
-    const unsigned grp = 0xffu << (8 * sub);
+    constexpr int RPW = 32 / LPR;
+    const int lane = threadIdx.x & 31, sub = lane / LPR, sl = lane % LPR;
+    const unsigned grp = static_cast<unsigned>((1ull << LPR) - 1) << (LPR * sub);
     const uint64_t n_work = *n_work_p;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t w0 = warp * 4; w0 < n_work; w0 += nw * 4) {
+    for (uint64_t w0 = warp * RPW; w0 < n_work; w0 += nw * RPW) {
         const uint64_t w = w0 + sub;
-        if (w >= n_work) continue;  // (whole 8-lane groups drop out together)
+        if (w >= n_work) continue;  // (whole lane groups drop out together)
         const uint32_t row = work[w];
         int l = lt.l_max;
         while (l > lt.l_min && row < lt.g[l].row0) --l;
@@ -1749,14 +1751,15 @@ __global__ void k_mark_tiles_all(const uint32_t* __restrict__ work, const uint64
         const int z = static_cast<int>(loc / lt.g[l].xd), x = static_cast<int>(loc % lt.g[l].xd);
         const uint64_t base = lt.fbase[l] + (static_cast<uint64_t>(z / kTZ) * lt.txd[l] + x / kTX) * lt.tyd[l];
         const uint32_t b = rb[row], e = rb[row + 1];
-        uint32_t prev = 0xffffffffu;  // the tile of the particle before this 8-lane chunk
-        for (uint32_t i0 = b; i0 < e; i0 += 8) {
+        // no value carried between chunks (the chunk's first lane reads its left
+        // neighbour's y itself): the chunks' loads pipeline
+#pragma unroll 4
+        for (uint32_t i0 = b; i0 < e; i0 += LPR) {
             const uint32_t i = i0 + sl;
             const uint32_t t = i < e ? static_cast<uint32_t>(y[i]) / kTY : 0xffffffffu;
-            const uint32_t left = __shfl_up_sync(grp, t, 1, 8);
-            if (i < e && t != (sl ? left : prev)) flags[base + t] = 1;
-            prev = __shfl_sync(grp, t, 7, 8);
-            if (prev == 0xffffffffu) break;
+            const uint32_t up = __shfl_up_sync(grp, t, 1, LPR);
+            const uint32_t left = sl ? up : (i > b && i < e ? static_cast<uint32_t>(y[i - 1]) / kTY : 0xfffffffeu);
+            if (i < e && t != left) flags[base + t] = 1;
         }
     }
 }
@@ -1805,7 +1808,8 @@ void rebuild_index_device(aprgpu_apr* apr, cudaStream_t s) {
     size_t tb = std::max(t1, t2);
     APR_CUDA(cub::DeviceSelect::If(temp, tb, it, work, cnt, static_cast<int64_t>(L.n_rows), RowNonEmpty{L.rb}, s));
     APR_CUDA(cudaMemsetAsync(flags, 0, nflags, s));
-    k_mark_tiles_all<<<apr->ctx->sm_count * 16, 256, 0, s>>>(work, cnt, lt, L.rb, L.y, flags);
+    // 8 lanes per row (A/B at C3: 4 lanes 95 us, 8 lanes 89 us, 16 lanes 104 us for the whole index step)
+    k_mark_tiles_all<8><<<apr->ctx->sm_count * 16, 256, 0, s>>>(work, cnt, lt, L.rb, L.y, flags);
     tb = std::max(t1, t2);
     APR_CUDA(cub::DeviceSelect::Flagged(temp, tb, it, flags, tiles, cnt + 1, static_cast<int64_t>(nflags), s));
     count_launch(apr->ctx, 3);
