@@ -101,6 +101,7 @@ struct TileLaunch {
     int map_ng;                       // k_conv_map: largest chunk count of the launch's tiles
     int aligned16;                    // both value arrays 16-byte aligned (else 4-byte copies)
     int list_in_f;                    // k_conv_map 3^3: the chunk list staged in F's tail (launch_map)
+    int l2hint;                       // k_conv_map: records and lists copied evict-first in L2
 };
 
 struct Geo {
@@ -1172,7 +1173,10 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     if (tid == 0) {
         mbar_init(&mbar, 1);
         asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(M::REC * 4) : "memory");
-        bulk_copy(Mb, rec, M::REC * 4, &mbar);
+        // (records and lists are read once per pass: evict-first, leaving L2 to
+        // the source values neighbouring tiles re-read)
+        if (a.l2hint) bulk_copy_hint(Mb, rec, M::REC * 4, &mbar, l2_evict_first());
+        else bulk_copy(Mb, rec, M::REC * 4, &mbar);
     }
     const uint32_t f0 = __ldg(a.flat_off + tix), nchunk = __ldg(a.flat_off + tix + 1) - f0;
     // 3^3: the list in the tail of F's region, which the gather then fills from
@@ -1183,7 +1187,10 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     if (list_in_f) Gs = reinterpret_cast<uint32_t*>(F + nf) - ((nchunk + 3u) & ~3u);
     if (tid == 0) {
         mbar_expect(&mbar, nchunk * 4);  // (arrive.expect_tx)
-        if (nchunk) bulk_copy(Gs, a.flat + f0, nchunk * 4, &mbar);
+        if (nchunk) {
+            if (a.l2hint) bulk_copy_hint(Gs, a.flat + f0, nchunk * 4, &mbar, l2_evict_first());
+            else bulk_copy(Gs, a.flat + f0, nchunk * 4, &mbar);
+        }
     }
     if (tid < kFlat0) F[tid] = 0.0f;
     for (int i = tid; i < KW; i += NT)
@@ -1639,7 +1646,12 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
         const char* e = std::getenv("APRGPU_MAP_LISTF");
         return !(e && e[0] == '0');
     }();
-    b.list_in_f = lf;  // (3^3 and FAST 5^3; EXACT 5^3 keeps its list inside the box)
+    b.list_in_f = lf;
+    static const bool hint = [] {  // APRGPU_L2HINT=0: no L2 eviction hints (A/B experiments)
+        const char* e = std::getenv("APRGPU_L2HINT");
+        return !(e && e[0] == '0');
+    }();
+    b.l2hint = hint;  // (3^3 and FAST 5^3; EXACT 5^3 keeps its list inside the box)
     return true;
 }
 
