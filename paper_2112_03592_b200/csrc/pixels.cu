@@ -13,6 +13,9 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace aprgpu {
@@ -206,20 +209,39 @@ __device__ __forceinline__ float2 ffma2_p(float2 a, float2 b, float2 c) {  // fm
     return d;
 }
 
+// a plane slot: PX rows of kPY floats, rounded to 128 bytes (TMA destinations)
+constexpr int plane_floats(int K) { return ((kSx + 2 * (K / 2)) * kPY + 31) & ~31; }
+
 template <typename Acc, int K, bool SKIP, int RY = kRY>  // RY: y outputs per thread (warps = kSy / RY)
 __global__ void __launch_bounds__(32 * kSy / RY, RY == 8 ? (sizeof(Acc) == 4 ? (K == 3 ? 4 : 3) : 2) : (sizeof(Acc) == 4 ? (K == 3 ? 5 : 3) : 2))
-    k_convolve_pixels_zreg(PixArgs a, const __grid_constant__ PixW<Acc, K * K * K> W, int txd, int tyd, int zc) {
+    k_convolve_pixels_zreg(PixArgs a, const __grid_constant__ PixW<Acc, K * K * K> W, int txd, int tyd, int zc,
+                           const __grid_constant__ CUtensorMap tmap, int use_tma) {
     constexpr int D = 2;  // prefetch distance (planes)
     constexpr int NT = 32 * kSy / RY;
-    constexpr int H = K / 2, PX = kSx + 2 * H, OFF = 4 - H, PY = kPY, PLANE = PX * PY, NS = D + 1;
+    constexpr int H = K / 2, PX = kSx + 2 * H, OFF = 4 - H, PY = kPY, PLANE = plane_floats(K), NS = D + 1;
     static_assert(kSx == 32 && kSy % RY == 0 && RY % 4 == 0, "lane = x row, warp = y run");
-    extern __shared__ __align__(16) float ring[];  // NS planes
+    extern __shared__ __align__(128) float ring[];  // NS planes
+    __shared__ __align__(8) uint64_t bars[NS];      // TMA planes: one mbarrier per slot
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ty = blockIdx.x % tyd, t2 = blockIdx.x / tyd;
     const int tx = t2 % txd, tzc = t2 / txd;
     const int x0 = tx * kSx, y0 = ty * kSy, zc0 = tzc * zc, zc1 = min(zc0 + zc, a.nz);
     const bool vec = (a.ny & 3) == 0 && y0 + kSy <= a.ny;  // 16-byte aligned, whole interior in range
     const bool zpad = a.pad == APRGPU_PAD_ZERO;
+    // TMA: ONE tensor copy per plane (the box of PX rows x kPY floats from
+    // (x0 - H, y0 - 4), the slot's exact layout), issued by one thread on the
+    // slot's mbarrier -- no per-thread copies through the LSU.  Its
+    // out-of-range cells read as zero: right for zero padding everywhere; with
+    // reflection only where every cell the outputs read is inside the volume
+    // (else the cp.async path reflects)
+    const bool tma_tile = use_tma && (zpad || (x0 - H >= 0 && x0 + kSx + H <= a.nx && y0 - H >= 0 &&
+                                               y0 + kSy + H <= a.ny));
+    auto tma_plane = [&](int z) { return tma_tile && (zpad || (z >= 0 && z < a.nz)); };
+    if (tma_tile && tid == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+    }
+    __syncthreads();
+    unsigned phase = 0;  // per slot: the parity of its next TMA completion
     // vec: a plane is PX rows x 16 interior chunks of 16 bytes + PX x 2H halo
     // cells; each thread's share (<= NDESC copies) is fixed for the whole z
     // column, so its source offsets within a plane (x reflected, halo y
@@ -253,7 +275,19 @@ __global__ void __launch_bounds__(32 * kSy / RY, RY == 8 ? (sizeof(Acc) == 4 ? (
         float* pl = ring + si * PLANE;
         const bool zout = z < 0 || z >= a.nz;
         const int zr = reflect_p(z, a.nz);
-        if (vec) {
+        if (tma_plane(z)) {
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (the slot's last reads)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[si])),
+                             "r"(static_cast<unsigned>(PX * PY * sizeof(float)))
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                    "%4}], [%5];" ::"r"(smem_u32(pl)),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(y0 - 4), "r"(x0 - H), "r"(z), "r"(smem_u32(&bars[si]))
+                    : "memory");
+            }
+        } else if (vec) {
             const float* pb = a.in + static_cast<size_t>(zr) * a.nx * a.ny;
 #pragma unroll
             for (int d = 0; d < NDESC; ++d) {
@@ -308,7 +342,11 @@ __global__ void __launch_bounds__(32 * kSy / RY, RY == 8 ? (sizeof(Acc) == 4 ? (
     const size_t zstride = static_cast<size_t>(a.nx) * a.ny;
     const bool vst = y0 + oy + RY <= a.ny && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (zstride & 3) == 0;
     for (int p = top; p >= bot; --p) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");  // plane p landed
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");  // plane p landed (cp.async planes)
+        if (tma_plane(p)) {  // (TMA planes)
+            mbar_wait(&bars[cur], (phase >> cur) & 1u);
+            phase ^= 1u << cur;
+        }
         __syncthreads();  // ... for every thread; plane p + 1's slot is free
         const int nxt = cur == NS - 1 ? 0 : cur + 1;  // the slot of p + 1 == p - D (NS = D + 1)
         if (p - D >= bot) load(p - D, nxt);
@@ -400,10 +438,37 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
         const int sxd = (nx + kSx - 1) / kSx, syd = (ny + kSy - 1) / kSy, szd = (nz + zc - 1) / zc;
         const unsigned g = static_cast<unsigned>(static_cast<uint64_t>(szd) * sxd * syd);
         const int h = kz / 2;
-        const int rb = 3 * (kSx + 2 * h) * kPY * static_cast<int>(sizeof(float));
+        const int rb = 3 * (kz == 3 ? plane_floats(3) : plane_floats(5)) * static_cast<int>(sizeof(float));
+        // the input as a 3-D tensor map for the TMA plane loads (ny * 4 bytes must be a 16-byte multiple)
+        CUtensorMap tm{};
+        int use_tma = 0;
+        static const bool tma_on = [] {  // APRGPU_PIXELS_TMA=0: cp.async planes only (A/B)
+            const char* e = std::getenv("APRGPU_PIXELS_TMA");
+            return !(e && e[0] == '0');
+        }();
+        static PFN_cuTensorMapEncodeTiled encode = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess) {
+                cudaGetLastError();
+                fn = nullptr;
+            }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+        }();
+        if (tma_on && encode && (ny & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+            const cuuint64_t dims[3] = {static_cast<cuuint64_t>(ny), static_cast<cuuint64_t>(nx),
+                                        static_cast<cuuint64_t>(nz)};
+            const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ny) * 4, static_cast<cuuint64_t>(nx) * ny * 4};
+            const cuuint32_t box[3] = {static_cast<cuuint32_t>(kPY), static_cast<cuuint32_t>(kSx + 2 * h), 1};
+            const cuuint32_t es[3] = {1, 1, 1};
+            use_tma = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
         static OncePerDevice zattr;
         zattr([] {
-            const int mx = 3 * (kSx + 4) * kPY * static_cast<int>(sizeof(float));
+            const int mx = 3 * plane_floats(5) * static_cast<int>(sizeof(float));
 #define APRGPU_SET_PIX(A, K_, S_)                                                                                      \
     APR_CUDA(cudaFuncSetAttribute(k_convolve_pixels_zreg<A, K_, S_, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                   mx));                                                                              \
@@ -424,11 +489,11 @@ void convolve_pixels_device(aprgpu_ctx* ctx, const float* in, int nz, int nx, in
         PixW<A, K_ * K_ * K_> pw;                                                                               \
         for (int i = 0; i < K_ * K_ * K_; ++i) pw.w[i] = static_cast<A>(w_host[i]);                             \
         if (ry == 16) {                                                                                         \
-            if (skip) k_convolve_pixels_zreg<A, K_, true, 16><<<g, 128, rb, s>>>(a, pw, sxd, syd, zc);          \
-            else k_convolve_pixels_zreg<A, K_, false, 16><<<g, 128, rb, s>>>(a, pw, sxd, syd, zc);              \
+            if (skip) k_convolve_pixels_zreg<A, K_, true, 16><<<g, 128, rb, s>>>(a, pw, sxd, syd, zc, tm, use_tma);          \
+            else k_convolve_pixels_zreg<A, K_, false, 16><<<g, 128, rb, s>>>(a, pw, sxd, syd, zc, tm, use_tma);              \
         } else {                                                                                                \
-            if (skip) k_convolve_pixels_zreg<A, K_, true, 8><<<g, 256, rb, s>>>(a, pw, sxd, syd, zc);           \
-            else k_convolve_pixels_zreg<A, K_, false, 8><<<g, 256, rb, s>>>(a, pw, sxd, syd, zc);               \
+            if (skip) k_convolve_pixels_zreg<A, K_, true, 8><<<g, 256, rb, s>>>(a, pw, sxd, syd, zc, tm, use_tma);           \
+            else k_convolve_pixels_zreg<A, K_, false, 8><<<g, 256, rb, s>>>(a, pw, sxd, syd, zc, tm, use_tma);               \
         }                                                                                                       \
     } while (0)
         if (kz == 3) {
