@@ -105,6 +105,12 @@ int aprgpu_access_get_info(const aprgpu_apr* apr, int which, aprgpu_access_info*
  * (stencil extent, pad mode, level) maps, *n_tiles = the APR's output tiles.  A
  * z-slab's convolutions build records only for the tiles they compute. */
 int aprgpu_apr_map_tiles(const aprgpu_apr* apr, uint64_t* built, uint64_t* n_tiles);
+/* Restricts the APR's per-tile convolution state (tile probe, source runs,
+ * staged-source lists, gather maps) to the tiles meeting finest-level planes
+ * [z_lo, z_hi) at levels >= cut_level (levels below whole): a z-slab rank
+ * builds and holds ~1/N of it.  Must precede the first convolution; a later
+ * convolution outside the slab fails with APRGPU_ERR_CAPABILITY. */
+int aprgpu_apr_restrict(aprgpu_apr* apr, int cut_level, int32_t z_lo, int32_t z_hi);
 /* Diagnostics: copies the resident gather-map records of one level (stencil
  * half-width 1 or 2, pad mode) to host memory out (cap_words u32), record t
  * starting at word offsets[t] (offsets: *n_tiles + 1 entries); *n_words = the words copied, *first_tile

@@ -58,6 +58,7 @@ _SIGS = {
     "aprgpu_apr_dims": [C.c_void_p, C.c_void_p],
     "aprgpu_access_get_info": [C.c_void_p, C.c_int, C.POINTER(AccessInfo)],
     "aprgpu_apr_map_tiles": [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
+    "aprgpu_apr_restrict": [C.c_void_p, C.c_int, C.c_int32, C.c_int32],
     "aprgpu_map_records": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p,
                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
     "aprgpu_download_access": [C.c_void_p, C.c_int] + [C.c_void_p] * 6,

@@ -561,6 +561,11 @@ class DeviceApr:
     def fill_tree_ptr(self, leaf_ptr: int, tree_ptr: int, stream: int = 0) -> None:
         L.check(L.lib().aprgpu_fill_tree(self.handle, leaf_ptr, tree_ptr, L.DEVICE, stream or None))
 
+    def restrict(self, cut_level: int, z_lo: int, z_hi: int) -> None:
+        """Per-tile state for the tiles meeting finest planes [z_lo, z_hi) at levels >= cut_level
+        only (aprgpu_apr_restrict; before the first convolution)."""
+        L.check(L.lib().aprgpu_apr_restrict(self.handle, int(cut_level), int(z_lo), int(z_hi)))
+
     def map_tiles(self) -> Tuple[int, int]:
         """(tile records held by the resident gather maps, output tiles of the APR)."""
         built, total = C.c_uint64(), C.c_uint64()

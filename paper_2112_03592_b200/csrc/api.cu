@@ -864,6 +864,23 @@ int aprgpu_apr_map_tiles(const aprgpu_apr* apr, uint64_t* built, uint64_t* n_til
     });
 }
 
+int aprgpu_apr_restrict(aprgpu_apr* apr, int cut_level, int32_t z_lo, int32_t z_hi) {
+    return guard([&] {
+        need(apr != nullptr, "null argument");
+        need(z_lo <= z_hi, "aprgpu_apr_restrict: empty plane range");
+        std::lock_guard<std::mutex> lk(apr->ctx->mu);
+        const aprgpu::DevAccess& L = apr->leaf;
+        bool built = L.tile_meta != nullptr || L.tile_runs[0] || L.tile_runs[1];
+        for (int h = 0; h < 2; ++h)
+            for (int pm = 0; pm < 2; ++pm)
+                for (int l = 0; l < aprgpu::kMaxLevels; ++l) built = built || L.tile_map[h][pm][l];
+        if (built) aprgpu::fail(APRGPU_ERR_RANGE, "aprgpu_apr_restrict: call before the first convolution");
+        apr->tile_slab.lc = cut_level;
+        apr->tile_slab.z_lo = z_lo;
+        apr->tile_slab.z_hi = z_hi;
+    });
+}
+
 int aprgpu_download_access(const aprgpu_apr* apr, int which, uint16_t* y_idx, uint64_t* xz_end,
                            uint64_t* level_offset, int32_t* z_dim, int32_t* x_dim, int32_t* y_dim) {
     return guard("aprgpu_download_access", [&] {

@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_probe(const __grid_consta
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
     const int l = a.lvl[s];
     const LevelG g = a.leaf.g[l];
-    const uint32_t tile = a.tile_base + blockIdx.x;
+    const uint32_t tile = a.tile_base + blockIdx.x + a.seg_shift[s];
     const Geo G = make_geo<kProbeH>(l, a.tiles[tile], a.tdim[s][1], a.tdim[s][2], g);
     for (int i = tid; i < B::NC; i += kTileThreads) cnt[i] = 0;
     if (tid < kMetaDepth + 2) hit[tid] = 0;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_runs(const __grid_constan
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
     const int l = a.lvl[s];
-    const uint32_t tix = a.tile_base + blockIdx.x;
+    const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
     const Geo G = make_geo<H>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], a.leaf.g[l]);
     const int tree = (l >= a.tree_lmin && l <= a.tree_lmax) ? 1 : 0;
     if (tid == 0) make_src_table<H>(G, a.meta[tix] & kMetaDepth, tree, T);
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_runs(const __grid_constan
         if (tid == 0) {
             int tot = 0;
             for (int w = 0; w < kTileThreads / 32; ++w) tot += wsum[w];
-            counts[blockIdx.x] = static_cast<uint32_t>(tot);
+            counts[tix] = static_cast<uint32_t>(tot);
         }
         return;
     }
@@ -1355,6 +1355,28 @@ std::pair<uint64_t, uint64_t> tile_range(const DevAccess& L, int l, const Slab& 
     return {b + zf[t0], b + zf[t1]};
 }
 
+// The per-tile state (probe, source runs, staged-source lists, gather maps)
+// is built for the tiles an APR's convolutions can touch: every tile, or --
+// once aprgpu_apr_restrict gave the APR a z-slab -- the tiles meeting the
+// slab's planes (levels below its cut whole).  Fills launch a with one segment
+// per level over those tiles; returns their count.
+uint32_t restricted_segments(const aprgpu_apr* apr, TileLaunch& a) {
+    const DevAccess& L = apr->leaf;
+    uint32_t total = 0;
+    uint64_t first = 0;
+    for (int l = L.l_min; l <= L.l_max; ++l) {
+        const auto r = tile_range(L, l, apr->tile_slab);
+        const uint32_t c = static_cast<uint32_t>(r.second - r.first);
+        if (!c) continue;
+        if (!a.n_levels) first = r.first;
+        a.seg_shift[a.n_levels] = static_cast<uint32_t>(r.first - first - total);
+        total += c;
+        set_level(a, L, l, total);
+    }
+    a.tile_base = static_cast<uint32_t>(first);
+    return total;
+}
+
 // First use of an APR by the tile path: probe every tile once.
 void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
     DevAccess& L = apr->leaf;
@@ -1364,17 +1386,11 @@ void ensure_tile_meta(aprgpu_apr* apr, cudaStream_t s) {
     const uint64_t n = L.tile_off[L.l_max + 1];
     uint8_t* meta = nullptr;
     APR_CUDA(cudaMalloc(&meta, n + 16));
+    APR_CUDA(cudaMemsetAsync(meta, 0, n + 16, s));
     TileLaunch a = base_launch(apr);
-    uint32_t total = 0;
-    for (int l = L.l_min; l <= L.l_max; ++l) {
-        const uint32_t c = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
-        if (!c) continue;
-        total += c;
-        set_level(a, L, l, total);
-    }
+    const uint32_t total = restricted_segments(apr, a);
     if (total) {
         a.tiles = L.tiles;
-        a.tile_base = static_cast<uint32_t>(L.tile_off[L.l_min]);
         a.meta = meta;
         k_tile_probe<<<total, kTileThreads, 0, s>>>(a);
         count_launch(apr->ctx);
@@ -1393,13 +1409,7 @@ void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
     if (L.tile_runs[H - 1]) return;
     const uint64_t n = L.tile_off[L.l_max + 1];
     TileLaunch a = base_launch(apr);
-    uint32_t total = 0;
-    for (int l = L.l_min; l <= L.l_max; ++l) {
-        const uint32_t c = static_cast<uint32_t>(L.tile_off[l + 1] - L.tile_off[l]);
-        if (!c) continue;
-        total += c;
-        set_level(a, L, l, total);
-    }
+    const uint32_t total = restricted_segments(apr, a);
     uint32_t* off = nullptr;
     APR_CUDA(cudaMalloc(&off, 4 * (n + 1)));
     APR_CUDA(cudaMemsetAsync(off, 0, 4 * (n + 1), s));
@@ -1408,11 +1418,10 @@ void ensure_tile_runs(aprgpu_apr* apr, cudaStream_t s) {
     if (total) {
         a.tiles = L.tiles;
         a.meta = L.tile_meta;
-        a.tile_base = static_cast<uint32_t>(L.tile_off[L.l_min]);
         GpuBuf counts, temp;
         counts.ensure(4 * (n + 1));
         APR_CUDA(cudaMemsetAsync(counts.p, 0, 4 * (n + 1), s));
-        k_tile_runs<H><<<total, kTileThreads, 0, s>>>(a, 0, counts.as<uint32_t>() + a.tile_base, nullptr);
+        k_tile_runs<H><<<total, kTileThreads, 0, s>>>(a, 0, counts.as<uint32_t>(), nullptr);
         count_launch(apr->ctx);
         APR_CUDA(cudaGetLastError());
         size_t tb = 0;
@@ -1902,6 +1911,9 @@ void conv_tile_levels(aprgpu_apr* apr, const aprgpu_pyramid* pyr, const float* v
                 const auto r = tile_range(L, l, slab);
                 const uint32_t c = static_cast<uint32_t>(r.second - r.first);
                 if (!c) continue;
+                const auto rr = tile_range(L, l, apr->tile_slab);
+                if (r.first < rr.first || r.second > rr.second)
+                    fail(APRGPU_ERR_CAPABILITY, "convolve: planes outside the APR's slab restriction (aprgpu_apr_restrict)");
                 rng[b.n_levels][0] = r.first;
                 rng[b.n_levels][1] = r.second;
                 b.seg_shift[b.n_levels] = static_cast<uint32_t>(r.first - rng[0][0] - total);

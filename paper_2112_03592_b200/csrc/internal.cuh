@@ -165,6 +165,14 @@ struct GpuBuf {  // owned device allocation (freed on release() or destruction; 
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// z-slab restriction of a convolution (DESIGN.md §6): levels >= lc compute only
+// the tiles / rows that touch finest-level pixel planes [z_lo, z_hi); coarser
+// levels are computed whole.  lc > l_max: no restriction.
+struct Slab {
+    int lc = 1 << 20, z_lo = 0, z_hi = 1 << 30;
+    bool rep = true;  // compute the replicated levels < lc too (multi.cu's boundary passes skip them)
+};
+
 // Host worker threads of a context (api.cu): run one job at a time on every
 // worker, asynchronously to the caller (start ... wait).  Used by the
 // pageable host-pointer convolution to stage chunks through pinned memory.
@@ -227,6 +235,8 @@ struct aprgpu_apr {
     aprgpu::GpuBuf built_values;           // leaf values sampled by aprgpu_build_apr / read by aprgpu_load_apr
     aprgpu::GpuBuf index_scratch;          // aprgpu_rebuild_index (the paper protocol's per-call index step)
     std::mutex index_mu;                   // ... and its own scratch guard (api.cu ScratchGuard)
+    // aprgpu_apr_restrict: the z-slab whose tiles this APR's per-tile state covers (default: all)
+    aprgpu::Slab tile_slab;
     cudaEvent_t index_ev = nullptr;
     // z-chunk plan of host-pointer convolutions (api.cu, HostPipe): chunk of S
     // finest planes; levels >= lc split per chunk, [l - lc][j] = first particle
@@ -305,13 +315,6 @@ void validate_rows_device(aprgpu_ctx* ctx, const DevAccess& L, const int dims[3]
 void validate_cover_device(aprgpu_ctx* ctx, const DevAccess& L, const int dims[3], int* dbl,
                            unsigned long long* min_unc, cudaStream_t s);
 
-// z-slab restriction of a convolution (DESIGN.md §6): levels >= lc compute only
-// the tiles / rows that touch finest-level pixel planes [z_lo, z_hi); coarser
-// levels are computed whole.  lc > l_max: no restriction.
-struct Slab {
-    int lc = 1 << 20, z_lo = 0, z_hi = 1 << 30;
-    bool rep = true;  // compute the replicated levels < lc too (multi.cu's boundary passes skip them)
-};
 
 // conv.cu
 enum Epilogue { EPI_STORE = 0, EPI_RL_RATIO = 1, EPI_RL_MULT = 2 };

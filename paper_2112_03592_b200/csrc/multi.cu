@@ -200,6 +200,8 @@ int aprgpu_multi_create(const int* devices, int n_slabs, const aprgpu_access_des
             d.device = devices[s];
             check(aprgpu_init(d.device, &d.ctx));
             check(aprgpu_upload_access(d.ctx, leaf, tree, source_dims, &d.apr));
+            // its per-tile state only for its own slab's tiles
+            check(aprgpu_apr_restrict(d.apr, p.lc, p.bounds[s].first, p.bounds[s].second));
             DeviceGuard g(d.device);
             APR_CUDA(cudaStreamCreateWithFlags(&d.compute, cudaStreamNonBlocking));
             APR_CUDA(cudaStreamCreateWithFlags(&d.copy, cudaStreamNonBlocking));

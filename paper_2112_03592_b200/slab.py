@@ -47,6 +47,7 @@ import numpy as np
 
 from . import _lib as L
 from .aprkit import LinearAccess
+from .errors import RangeError
 
 Range = Tuple[int, int]
 
@@ -258,6 +259,13 @@ class GpuRankState:
         self.values = torch.zeros(max(n_p, 1), dtype=torch.float32, device=self.device)
         self.tree = torch.zeros(max(n_t, 1), dtype=torch.float32, device=self.device)
         self.out = torch.zeros(max(n_p, 1), dtype=torch.float32, device=self.device)
+        # the APR's per-tile convolution state only for this rank's slab (before its first convolution;
+        # a handle that has already convolved keeps its whole-volume state)
+        try:
+            z_lo, z_hi = plan.bounds[plan.rank]
+            dev.restrict(plan.lc, z_lo, z_hi)
+        except RangeError:
+            pass
         vs, ws = C.c_void_p(), C.c_void_p()
         L.check(L.lib().aprgpu_tree_scratch(dev.handle, C.byref(vs), C.byref(ws)))
         self.vsum = torch.as_tensor(_CudaArray(vs.value, max(n_t, 1), "<f8"), device=self.device)

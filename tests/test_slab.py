@@ -252,3 +252,28 @@ def test_interior_bands_need_no_halo_gpu(name, world):
     for st in sts:
         own = _owned_mask(st.plan, "leaf", ref.size)
         assert np.array_equal(G.bits(st.out.cpu().numpy()[:ref.size][own]), G.bits(ref[own])), st.rank
+
+
+@pytest.mark.gpu
+def test_restricted_apr_refuses_planes_outside_its_slab():
+    """aprgpu_apr_restrict: the per-tile state is built for the slab's tiles
+    only, so a convolution reaching outside the slab fails loudly instead of
+    reading tiles that were never built; a restriction after the first
+    convolution is refused."""
+    d = G.load("c1_256")
+    apr = G.product_apr(d)
+    a = apr.access
+    ctx = P.default_context()
+    dev = P.DeviceApr.upload(ctx, apr)
+    lc = a.l_max - 2
+    dev.restrict(lc, 0, 128)
+    pyr = P.make_pyramid(P.gaussian_stencil(1.0, 3), a.l_min, a.l_max, P.PyramidMode.Restricted).device(ctx)
+    tv = P.fill_tree(apr, d["values"])
+    with pytest.raises(P.CapabilityError):
+        dev.convolve(d["values"], tv, pyr, 1, L.ACCUM_EXACT)  # (the whole volume)
+    built, n_tiles = dev.map_tiles()
+    assert built < n_tiles
+    fresh = P.DeviceApr.upload(ctx, apr)
+    fresh.convolve(d["values"], tv, pyr, 1, L.ACCUM_EXACT)
+    with pytest.raises(P.RangeError):
+        fresh.restrict(lc, 0, 128)
