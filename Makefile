@@ -12,7 +12,7 @@ LIB := $(PKG)/_lib/libaprgpu.so
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Iinclude -Xcompiler -fPIC,-ffp-contract=off,-fvisibility=hidden \
            -Xptxas -v --expt-relaxed-constexpr -diag-suppress 1444,2417
-CU_SRCS := $(SRC)/api.cu $(SRC)/index.cu $(SRC)/tree.cu $(SRC)/conv.cu $(SRC)/conv_tile.cu $(SRC)/build.cu $(SRC)/tile.cu $(SRC)/reconstruct.cu $(SRC)/validate.cu $(SRC)/pixels.cu $(SRC)/multi.cu
+CU_SRCS := $(SRC)/api.cu $(SRC)/index.cu $(SRC)/tree.cu $(SRC)/conv.cu $(SRC)/conv_tile.cu $(SRC)/build.cu $(SRC)/tile.cu $(SRC)/reconstruct.cu $(SRC)/validate.cu $(SRC)/pixels.cu $(SRC)/multi.cu $(SRC)/seqsum.cu
 CPP_SRCS := $(SRC)/stencil.cpp $(SRC)/io.cpp
 HDRS := $(SRC)/internal.cuh $(SRC)/common.cuh include/aprgpu.h
 OBJDIR := build/obj

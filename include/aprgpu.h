@@ -296,6 +296,12 @@ int aprgpu_multi_convolve(aprgpu_multi* m, const float* values, const float* tre
 int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estimate_in, const float* psf, int kz,
                      int kx, int ky, int iterations, double epsilon, int accum, float* out, int ptr_kind,
                      void* stream);
+/* rl_apr's observation sum (deconv.hpp:90-91: `double mean = 0; for (float v :
+ * u) mean += v;`) of n non-negative values, bit-identical to that sequential
+ * loop, computed on the device (the parallel replay rl_apr falls back to when
+ * its partial sums are not provably exact).  RANGE for a negative or non-finite
+ * value.  Synchronises the stream. */
+int aprgpu_sequential_sum(aprgpu_ctx* ctx, const float* values, uint64_t n, int ptr_kind, double* out, void* stream);
 
 /* ---- inputs: synthetic volumes and APR construction (input side of the path) */
 /* generate_spheres (synthetic.hpp:74-111, no noise) into out[nz*nx*ny] (z,x,y

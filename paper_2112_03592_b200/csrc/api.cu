@@ -256,6 +256,12 @@ __global__ void __launch_bounds__(256) k_mean_exact(const float* __restrict__ u,
     if (threadIdx.x == 0) atomicAdd(&st->isum, static_cast<unsigned long long>(acc));
 }
 
+// any value < 0 -> st->nonfinite = 1 (aprgpu_sequential_sum's argument check)
+__global__ void k_min_check(const float* __restrict__ u, uint64_t n, MeanStats* st) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        if (u[i] < 0.0f) st->nonfinite = 1;
+}
+
 }  // namespace
 
 namespace {
@@ -995,6 +1001,40 @@ int aprgpu_sobel_stencil(int axis, float* out) {
     });
 }
 
+int aprgpu_sequential_sum(aprgpu_ctx* ctx, const float* values, uint64_t n, int ptr_kind, double* out, void* stream) {
+    return guard("aprgpu_sequential_sum", [&] {
+        need(ctx && out && (values || n == 0), "null argument");
+        need(ptr_kind == APRGPU_HOST || ptr_kind == APRGPU_DEVICE, "bad pointer kind");
+        DeviceGuard g(ctx->device);
+        cudaStream_t s = aprgpu::pick_stream(ctx, stream);
+        aprgpu::GpuBuf staged, scratch;
+        const float* u = values;
+        if (ptr_kind == APRGPU_HOST && n) {
+            staged.ensure(4 * n);
+            APR_CUDA(cudaMemcpyAsync(staged.p, values, 4 * n, cudaMemcpyHostToDevice, s));
+            u = staged.as<float>();
+        }
+        if (n) {  // the same check as rl_apr's (non-negative, finite)
+            scratch.ensure(64);
+            MeanStats* ms = scratch.as<MeanStats>();
+            APR_CUDA(cudaMemsetAsync(ms, 0, sizeof(MeanStats), s));
+            const unsigned grid = std::min<unsigned>(aprgpu::blocks_for(n, 256), ctx->sm_count * 8);
+            k_mean_bound<<<grid, 256, 0, s>>>(u, n, ms);
+            aprgpu::count_launch(ctx);
+            MeanStats h{};
+            APR_CUDA(cudaMemcpyAsync(&h, ms, sizeof(MeanStats), cudaMemcpyDeviceToHost, s));
+            APR_CUDA(cudaStreamSynchronize(s));
+            if (h.nonfinite) fail(APRGPU_ERR_RANGE, "aprgpu_sequential_sum: non-finite value");
+            k_min_check<<<grid, 256, 0, s>>>(u, n, ms);
+            aprgpu::count_launch(ctx);
+            APR_CUDA(cudaMemcpyAsync(&h, ms, sizeof(MeanStats), cudaMemcpyDeviceToHost, s));
+            APR_CUDA(cudaStreamSynchronize(s));
+            if (h.nonfinite) fail(APRGPU_ERR_RANGE, "aprgpu_sequential_sum: negative value");
+        }
+        *out = aprgpu::sequential_sum_device(ctx, u, n, scratch, s);
+    });
+}
+
 int aprgpu_pyramid_create(aprgpu_ctx* ctx, const float* w, int kz, int kx, int ky, int l_min, int l_max, int mode,
                           aprgpu_pyramid** out) {
     aprgpu_pyramid* p = nullptr;
@@ -1247,7 +1287,8 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
         // (deconv.hpp:90-92).  When every partial sum of that double loop is
         // provably exact (all values are multiples of 2^g and sum|v| < 2^(53+g))
         // the sequential sum IS the exact sum, computed on the device as an
-        // order-free int64 sum of v / 2^g; otherwise the host replays the loop.
+        // order-free int64 sum of v / 2^g; otherwise the loop is replayed on the
+        // device (seqsum.cu), bit for bit.
         double mean = 0.0;
         if (epsilon <= 0.0) {
             apr->tmp.ensure(64);
@@ -1265,7 +1306,11 @@ int aprgpu_rl_resume(aprgpu_apr* apr, const float* observed, const float* estima
                                                 h.abs_sum < std::ldexp(1.0, 53 + g) * 0.999999);
             if (exact) {
                 mean = h.neg_gexp_max == 0 ? 0.0 : std::ldexp(static_cast<double>(static_cast<int64_t>(h.isum)), g);
-            } else {
+            } else if (!h.nonfinite) {
+                // the partial sums round: the loop replayed on the device (seqsum.cu)
+                aprgpu::GpuBuf scratch;
+                mean = aprgpu::sequential_sum_device(ctx, u, np, scratch, s);
+            } else {  // (NaN / inf observations: the loop on the host)
                 host_obs.resize(np);
                 APR_CUDA(cudaMemcpyAsync(host_obs.data(), u, 4 * np, cudaMemcpyDeviceToHost, s));
                 APR_CUDA(cudaStreamSynchronize(s));

@@ -292,6 +292,11 @@ void reconstruct_patch_device(aprgpu_apr* apr, const float* values, const float*
 void build_tree_structure(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void verify_tree_links(aprgpu_ctx* ctx, aprgpu_apr* apr);
 void fill_tree_device(aprgpu_apr* apr, const float* leaf, float* tree, cudaStream_t s);
+
+// seqsum.cu: the reference's sequential double sum (`double m = 0; for (float
+// v : u) m += v;`, deconv.hpp:90-91) of n non-negative finite device floats,
+// bit for bit (synchronises the stream; scratch grows to 16 B per 2048 values)
+double sequential_sum_device(aprgpu_ctx* ctx, const float* u, uint64_t n, GpuBuf& scratch, cudaStream_t s);
 void fill_tree_sums(aprgpu_apr* apr, const float* leaf, int lt_lo, int lt_hi, int z_lo, int z_hi, cudaStream_t s,
                     float* tree_out = nullptr);
 void fill_tree_finalize(aprgpu_apr* apr, float* tree, cudaStream_t s);
