@@ -1299,6 +1299,191 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     }
 }
 
+// Bank-aware placement of a 3^3 tile's staged chunks in F (run once per map
+// build, after it).  The apply's source loads (k_conv_map: one warp-load per
+// neighbourhood cell of its 32 blocks) gather from F through the codes, and a
+// warp-load costs as many shared-memory wavefronts as the most-requested bank
+// holds distinct words -- ~3.3 for the F order the build leaves (its banks are
+// as good as random).  A chunk's bank is fixed by its F position mod 8, and
+// permuting the chunks WITHIN each aligned group of 32 list entries changes
+// nothing else: a warp's gather copies the same 32 chunks (same cache lines,
+// lanes reordered) and the list-in-F rounds keep their invariant.  So: every
+// value-load instruction of the tile's apply is enumerated, and the chunks --
+// most-referenced first -- greedily take the colour (position mod 8) that
+// raises those instructions' bank maxima least, within their group's
+// capacity.  The list and the codes are then rewritten to the chosen
+// positions.  Only interior tiles (no padding cells) are permuted: their codes,
+// blocks and hence this deterministic placement are the same under both pad
+// modes, which share one chunk list.  Results are bit-identical (the same
+// values, elsewhere in F); tools/dump_maps.py + DESIGN §3 give the numbers.
+constexpr int kPlaceMaxRounds = 8;                        // kBlocks / 32 warp-rounds of apply blocks
+constexpr int kPlaceMaxI = 64 * kPlaceMaxRounds;          // value loads per warp-round: 16 rows x 4 cells
+constexpr int kPlaceFixed = 2 * MapBox<1>::NC + kBlocks + kPlaceMaxI * 32 + 4 * kPlaceMaxI + 2 * kPlaceMaxI * 32 + 4 * 64;
+__host__ __device__ constexpr int place_smem(int nch) {  // (per-chunk arrays after the fixed ones)
+    return kPlaceFixed + 4 * (nch + 1) + 4 * nch + 2 * nch + nch + 2 * nch + 8 * (nch / 32 + 1) + 16;
+}
+
+__global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLaunch a, const uint32_t* __restrict__ list_in) {
+    using M = MapBox<1>;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(16) unsigned char psm[];
+    uint16_t* C = reinterpret_cast<uint16_t*>(psm);                   // the codes (byte offsets into F)
+    uint8_t* BL = psm + 2 * M::NC;                                    // active blocks
+    uint8_t* Hh = BL + kBlocks;                                       // [I][32] distinct words per bank
+    uint32_t* cur = reinterpret_cast<uint32_t*>(Hh + kPlaceMaxI * 32);  // [I] bank maximum
+    uint16_t* refs = reinterpret_cast<uint16_t*>(cur + kPlaceMaxI);     // per chunk: (instruction << 2 | word)
+    uint32_t* bins = reinterpret_cast<uint32_t*>(refs + kPlaceMaxI * 32);
+    uint32_t* roff = bins + 64;
+    const int lane = threadIdx.x;
+    const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
+    const int l = a.lvl[s];
+    const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
+    uint32_t* rec = a.map[s] + static_cast<size_t>(tix - a.map_base[s]) * M::REC;
+    const uint32_t f0 = a.flat_off[tix];
+    const int nch = static_cast<int>(a.flat_off[tix + 1] - f0);
+    const int nb = static_cast<int>(rec[M::W_NBLK]);
+    const LevelG g = a.leaf.g[l];
+    const Geo G = make_geo<1>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], g);
+    const bool interior = G.z0 - 1 >= 0 && G.x0 - 1 >= 0 && G.y0 - 1 >= 0 && G.z0 + kTZ + 1 <= g.zd &&
+                          G.x0 + kTX + 1 <= g.xd && G.y0 + kTY + 1 <= g.yd;
+    if (!interior || nb == 0 || nch <= 8) {  // the build's order
+        for (int c = lane; c < nch; c += 32) a.flat[f0 + c] = list_in[f0 + c];
+        return;
+    }
+    uint32_t* cnt = roff + nch + 1;
+    uint16_t* order = reinterpret_cast<uint16_t*>(cnt + nch);
+    uint8_t* col = reinterpret_cast<uint8_t*>(order + nch);
+    uint16_t* npos = reinterpret_cast<uint16_t*>(col + ((nch + 1) & ~1));
+    uint8_t* cap = reinterpret_cast<uint8_t*>(npos + nch);
+    const int nwr = (nb + 31) >> 5, ni = 64 * nwr, ng = (nch + 31) >> 5;
+    for (int w = lane; w < M::CW; w += 32) reinterpret_cast<uint32_t*>(C)[w] = rec[w];
+    for (int q = lane; q < nb; q += 32) BL[q] = reinterpret_cast<const uint8_t*>(rec + M::W_BLK)[q];
+    for (int i = lane; i < ni * 32; i += 32) Hh[i] = 0;
+    for (int i = lane; i < ni; i += 32) cur[i] = 0;
+    for (int c = lane; c < nch; c += 32) cnt[c] = 0;
+    for (int k = lane; k < 64; k += 32) bins[k] = 0;
+    for (int i = lane; i < 8 * ng; i += 32) {
+        const int gi = i >> 3, k = i & 7, n_g = min(32, nch - 32 * gi);
+        cap[i] = static_cast<uint8_t>(k < n_g ? (n_g - k + 7) / 8 : 0);
+    }
+    __syncwarp();
+    // the apply's value loads: warp-round j = blocks [32j, 32j + 32) (k_conv_map's q loop), load t =
+    // (row nz, nx; pair pp; half h); each lane's slot (F word); distinct words counted once
+    auto each_load = [&](auto&& f) {
+        for (int j = 0; j < nwr; ++j) {
+            const int q = 32 * j + lane;
+            int base = -1;
+            if (q < nb) {
+                const int b = BL[q];
+                base = ((2 * (b / (kBlocks / 4))) * M::BX + 2 * ((b / (kTY / 2)) & 3)) * M::BY + 2 * (b & (kTY / 2 - 1));
+            }
+            for (int t = 0; t < 64; ++t) {
+                const int nz = t >> 4, nx = (t >> 2) & 3, pp = (t >> 1) & 1, h = t & 1;
+                const uint32_t slot = base >= 0 ? C[base + (nz * M::BX + nx) * M::BY + 2 * pp + h] >> 2 : 0xffffu;
+                const unsigned m = __match_any_sync(FULL, slot);
+                if (slot != 0xffffu && lane == __ffs(m) - 1) f(64 * j + t, slot);
+            }
+        }
+    };
+    each_load([&](int i, uint32_t slot) {
+        if (slot < kFlat0) Hh[i * 32 + ((M::REC + slot) & 31)] = 1;  // (the zero's 4 words: 4 banks)
+        else atomicAdd(&cnt[(slot - kFlat0) >> 2], 1u);
+    });
+    __syncwarp();
+    for (int i = 0; i < ni; ++i) {
+        const unsigned v = __reduce_max_sync(FULL, static_cast<unsigned>(Hh[i * 32 + lane]));
+        if (lane == 0) cur[i] = v;
+    }
+    // roff = exclusive scan of cnt; cnt becomes the fill cursor
+    uint32_t carry = 0;
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+        const int c = c0 + lane;
+        const uint32_t v = c < nch ? cnt[c] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, d);
+            if (lane >= d) x += y;
+        }
+        if (c < nch) roff[c] = carry + x - v;
+        carry += __shfl_sync(FULL, x, 31);
+    }
+    if (lane == 0) roff[nch] = carry;
+    __syncwarp();
+    for (int c = lane; c < nch; c += 32) cnt[c] = roff[c];
+    __syncwarp();
+    each_load([&](int i, uint32_t slot) {
+        if (slot >= kFlat0) {
+            const uint32_t c = (slot - kFlat0) >> 2;
+            refs[atomicAdd(&cnt[c], 1u)] = static_cast<uint16_t>(i << 2 | (slot & 3u));
+        }
+    });
+    __syncwarp();
+    // most-referenced chunks first (stable counting sort on min(refs, 63), descending)
+    auto key_of = [&](int c) { return 63 - min(static_cast<int>(roff[c + 1] - roff[c]), 63); };
+    for (int c = lane; c < nch; c += 32) atomicAdd(&bins[key_of(c)], 1u);
+    __syncwarp();
+    if (lane == 0)
+        for (int k = 0, acc = 0; k < 64; ++k) {
+            const int v = static_cast<int>(bins[k]);
+            bins[k] = acc;
+            acc += v;
+        }
+    __syncwarp();
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+        const int c = c0 + lane;
+        const int key = c < nch ? key_of(c) : 64 + lane;
+        const unsigned m = __match_any_sync(FULL, key);
+        if (c < nch) order[bins[key] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(c);
+        __syncwarp();
+        if (c < nch && lane == __ffs(m) - 1) bins[key] += __popc(m);
+        __syncwarp();
+    }
+    // greedy colours: lane = (colour k = lane & 7, a quarter of the chunk's references)
+    const int k = lane & 7;
+    for (int oi = 0; oi < nch; ++oi) {
+        const int c = order[oi], gi = c >> 5;
+        const uint32_t r0 = roff[c], r1 = roff[c + 1];
+        uint32_t cost = 0;
+        for (uint32_t r = r0 + (lane >> 3); r < r1; r += 4) {
+            const uint32_t e = refs[r], i = e >> 2;
+            const uint32_t h = Hh[i * 32 + ((M::REC + kFlat0 + (e & 3u) + 4u * k) & 31u)], cu = cur[i];
+            cost += max(cu, h + 1u) - cu;
+        }
+        cost += __shfl_xor_sync(FULL, cost, 8);
+        cost += __shfl_xor_sync(FULL, cost, 16);
+        const uint32_t key = cap[8 * gi + k] ? (cost << 3 | static_cast<uint32_t>(k)) : 0xffffffffu;
+        const int kb = static_cast<int>(__reduce_min_sync(FULL, key) & 7u);
+        __syncwarp();
+        if (lane == 0) {
+            --cap[8 * gi + kb];
+            col[c] = static_cast<uint8_t>(kb);
+        }
+        for (uint32_t r = r0 + lane; r < r1; r += 32) {  // (a chunk's words in one load: distinct banks)
+            const uint32_t e = refs[r], i = e >> 2;
+            uint8_t& h = Hh[i * 32 + ((M::REC + kFlat0 + (e & 3u) + 4u * kb) & 31u)];
+            h = static_cast<uint8_t>(h + 1);
+            atomicMax(&cur[i], static_cast<uint32_t>(h));
+        }
+        __syncwarp();
+    }
+    // positions: a group's chunks of colour k take its positions k, k + 8, ... in chunk order
+    for (int gi = 0; gi < ng; ++gi) {
+        const int c = 32 * gi + lane;
+        const int kk = c < nch ? col[c] : 8 + lane;
+        const unsigned m = __match_any_sync(FULL, kk);
+        if (c < nch) npos[c] = static_cast<uint16_t>(32 * gi + kk + 8 * __popc(m & ((1u << lane) - 1u)));
+    }
+    __syncwarp();
+    for (int c = lane; c < nch; c += 32) a.flat[f0 + npos[c]] = list_in[f0 + c];
+    auto moved = [&](uint32_t code) -> uint32_t {
+        const uint32_t slot = code >> 2;
+        if (slot < kFlat0) return code;
+        return (kFlat0 + 4u * npos[(slot - kFlat0) >> 2] + (slot & 3u)) << 2;
+    };
+    for (int w = lane; w < M::CW; w += 32) rec[w] = moved(C[2 * w]) | moved(C[2 * w + 1]) << 16;
+}
+
 // tile occupancy: mark (z/8, x/8, y/16) of every particle of the level
 __global__ void k_mark_tiles(const uint32_t* __restrict__ work, uint64_t n_work, LevelG g, const uint32_t* __restrict__ rb,
                              const uint16_t* __restrict__ y, int txd, int tyd, uint8_t* __restrict__ flags) {
@@ -1488,6 +1673,16 @@ void ensure_tile_flat(aprgpu_apr* apr, cudaStream_t s) {
     APR_CUDA(cudaMemsetAsync(flat, 0, 4ull * total + 16, s));  // padding entries: particle 0
     L.tile_flat_off[H - 1] = off;
     L.tile_flat[H - 1] = flat;
+    L.tile_flat_n[H - 1] = total;
+}
+
+// APRGPU_MAP_PLACE=0: keep the build's F order (A/B experiments)
+bool map_place_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("APRGPU_MAP_PLACE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 template <typename Acc, int H, bool MAP = false>
@@ -1613,7 +1808,15 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
                 m.map_base[j] = static_cast<uint32_t>(lo[j]);
                 m.seg_shift[j] = static_cast<uint32_t>(lo[j] - m.tile_base - (j ? m.seg_end[j - 1] : 0));
             }
-            m.flat = L.tile_flat[H - 1];
+            // 3^3: the build writes its chunk lists to scratch, k_map_place then
+            // writes them (and the codes) in their bank-aware order
+            const bool place = H == 1 && map_place_enabled();
+            GpuBuf list_scratch;
+            if (place) {  // (the build leaves a tile's padding entries alone: particle 0, like tile_flat's)
+                list_scratch.ensure(4 * L.tile_flat_n[H - 1] + 16);
+                APR_CUDA(cudaMemsetAsync(list_scratch.p, 0, 4 * L.tile_flat_n[H - 1] + 16, s));
+            }
+            m.flat = place ? list_scratch.as<uint32_t>() : L.tile_flat[H - 1];
             m.flat_off = L.tile_flat_off[H - 1];
             m.slab_lc = 1 << 20;  // every tile of the windows
             GpuBuf flag;
@@ -1631,6 +1834,16 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
                     __atomic_store_n(&L.tile_map_fail[H - 1][pm][m.lvl[j]], 1, __ATOMIC_RELEASE);
                 }
                 return false;
+            }
+            if (place) {
+                TileLaunch pl = m;
+                pl.flat = L.tile_flat[H - 1];
+                const int bytes = place_smem(fl[1]);
+                APR_CUDA(cudaFuncSetAttribute(k_map_place, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+                k_map_place<<<total, 32, bytes, s>>>(pl, list_scratch.as<uint32_t>());
+                count_launch(apr->ctx);
+                APR_CUDA(cudaGetLastError());
+                APR_CUDA(cudaStreamSynchronize(s));
             }
             for (int j = 0; j < m.n_levels; ++j) {
                 const int l = m.lvl[j];

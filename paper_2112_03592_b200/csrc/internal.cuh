@@ -143,6 +143,7 @@ struct DevAccess {
     // per H: every tile's flattened sources (leaf particles, then interior nodes), tiles padded to 4
     uint32_t* tile_flat[2] = {nullptr, nullptr};
     uint32_t* tile_flat_off[2] = {nullptr, nullptr};  // n_tiles + 1 offsets into tile_flat
+    uint64_t tile_flat_n[2] = {0, 0};                 // entries of tile_flat
     uint8_t tile_map_fail[2][2][kMaxLevels] = {};  // a level that reconstructs (no map)
     int tile_map_ng[2][kMaxLevels] = {};            // per H and level: largest per-tile chunk count
     AccessView view() const;
