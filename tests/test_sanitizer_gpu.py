@@ -16,7 +16,27 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 
-@pytest.mark.skipif(not os.path.exists(SAN), reason="compute-sanitizer not found")
+
+def _sanitizer_usable():
+    """The tool exists and runs here (some GPU pools disable it: their wrapper
+    prints why and exits non-zero -- the committed profiles/r02/sanitizer_*.log
+    runs stand then)."""
+    if not os.path.exists(SAN):
+        return False, "compute-sanitizer not found"
+    try:
+        r = subprocess.run([SAN, "--version"], capture_output=True, text=True, timeout=120)
+    except Exception as e:  # noqa: BLE001
+        return False, f"compute-sanitizer does not run: {e}"
+    out = (r.stdout + r.stderr).strip()
+    if r.returncode != 0 or "closed" in out.lower():
+        return False, f"compute-sanitizer unavailable on this machine: {out[:200]}"
+    return True, ""
+
+
+_OK, _WHY = _sanitizer_usable()
+
+
+@pytest.mark.skipif(not _OK, reason=_WHY or "compute-sanitizer unavailable")
 @pytest.mark.parametrize("tool,workload", [("memcheck", "all"), ("racecheck", "all"), ("synccheck", "all")])
 def test_compute_sanitizer_clean(tool, workload):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "9"]
