@@ -1316,15 +1316,20 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
 // blocks and hence this deterministic placement are the same under both pad
 // modes, which share one chunk list.  Results are bit-identical (the same
 // values, elsewhere in F); tools/dump_maps.py + DESIGN §3 give the numbers.
+// 5^3 (H = 2): the same for the loads of the box expansion (every box cell, 8
+// consecutive cells per lane; the apply then reads the expanded box).
 constexpr int kPlaceMaxRounds = 8;                        // kBlocks / 32 warp-rounds of apply blocks
-constexpr int kPlaceMaxI = 64 * kPlaceMaxRounds;          // value loads per warp-round: 16 rows x 4 cells
-constexpr int kPlaceFixed = 2 * MapBox<1>::NC + kBlocks + kPlaceMaxI * 32 + 4 * kPlaceMaxI + 2 * kPlaceMaxI * 32 + 4 * 64;
+constexpr int kPlaceMaxI = 64 * kPlaceMaxRounds;          // 3^3: 64 value loads per warp-round (5^3: 8 per round, 21 rounds)
+template <int H>
 __host__ __device__ constexpr int place_smem(int nch) {  // (per-chunk arrays after the fixed ones)
-    return kPlaceFixed + 4 * (nch + 1) + 4 * nch + 2 * nch + nch + 2 * nch + 8 * (nch / 32 + 1) + 16;
+    return 2 * MapBox<H>::NC + kBlocks + kPlaceMaxI * 32 + 4 * kPlaceMaxI + 2 * kPlaceMaxI * 32 + 4 * 64 +
+           4 * (nch + 1) + 4 * nch + 2 * nch + nch + 2 * nch + 8 * (nch / 32 + 1) + 16;
 }
 
+template <int H>
 __global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLaunch a, const uint32_t* __restrict__ list_in) {
-    using M = MapBox<1>;
+    using M = MapBox<H>;
+    static_assert(H == 1 || (M::NC / 8 + 31) / 32 * 8 <= kPlaceMaxI, "5^3 expansion loads");
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(16) unsigned char psm[];
     uint16_t* C = reinterpret_cast<uint16_t*>(psm);                   // the codes (byte offsets into F)
@@ -1343,9 +1348,9 @@ __global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLa
     const int nch = static_cast<int>(a.flat_off[tix + 1] - f0);
     const int nb = static_cast<int>(rec[M::W_NBLK]);
     const LevelG g = a.leaf.g[l];
-    const Geo G = make_geo<1>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], g);
-    const bool interior = G.z0 - 1 >= 0 && G.x0 - 1 >= 0 && G.y0 - 1 >= 0 && G.z0 + kTZ + 1 <= g.zd &&
-                          G.x0 + kTX + 1 <= g.xd && G.y0 + kTY + 1 <= g.yd;
+    const Geo G = make_geo<H>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], g);
+    const bool interior = G.z0 - H >= 0 && G.x0 - H >= 0 && G.y0 - H >= 0 && G.z0 + kTZ + H <= g.zd &&
+                          G.x0 + kTX + H <= g.xd && G.y0 + kTY + H <= g.yd;
     if (!interior || nb == 0 || nch <= 8) {  // the build's order
         for (int c = lane; c < nch; c += 32) a.flat[f0 + c] = list_in[f0 + c];
         return;
@@ -1355,8 +1360,9 @@ __global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLa
     uint8_t* col = reinterpret_cast<uint8_t*>(order + nch);
     uint16_t* npos = reinterpret_cast<uint16_t*>(col + ((nch + 1) & ~1));
     uint8_t* cap = reinterpret_cast<uint8_t*>(npos + nch);
-    const int nwr = (nb + 31) >> 5, ni = 64 * nwr, ng = (nch + 31) >> 5;
-    for (int w = lane; w < M::CW; w += 32) reinterpret_cast<uint32_t*>(C)[w] = rec[w];
+    constexpr int NG8 = M::NC / 8;  // 5^3: the expansion's 8-cell groups
+    const int nwr = H == 1 ? (nb + 31) >> 5 : (NG8 + 31) >> 5, ni = (H == 1 ? 64 : 8) * nwr, ng = (nch + 31) >> 5;
+    for (int w = lane; w < M::CW; w += 32) reinterpret_cast<uint32_t*>(C)[w] = rec[M::CODE0 + w];
     for (int q = lane; q < nb; q += 32) BL[q] = reinterpret_cast<const uint8_t*>(rec + M::W_BLK)[q];
     for (int i = lane; i < ni * 32; i += 32) Hh[i] = 0;
     for (int i = lane; i < ni; i += 32) cur[i] = 0;
@@ -1370,6 +1376,17 @@ __global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLa
     // the apply's value loads: warp-round j = blocks [32j, 32j + 32) (k_conv_map's q loop), load t =
     // (row nz, nx; pair pp; half h); each lane's slot (F word); distinct words counted once
     auto each_load = [&](auto&& f) {
+        if constexpr (H == 2) {  // group g = 32j + lane, load t: cell 8g + t
+            for (int j = 0; j < nwr; ++j) {
+                const int gq = 32 * j + lane;
+                for (int t = 0; t < 8; ++t) {
+                    const uint32_t slot = gq < NG8 ? C[8 * gq + t] >> 2 : 0xffffu;
+                    const unsigned m = __match_any_sync(FULL, slot);
+                    if (slot != 0xffffu && lane == __ffs(m) - 1) f(8 * j + t, slot);
+                }
+            }
+            return;
+        }
         for (int j = 0; j < nwr; ++j) {
             const int q = 32 * j + lane;
             int base = -1;
@@ -1481,7 +1498,7 @@ __global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLa
         if (slot < kFlat0) return code;
         return (kFlat0 + 4u * npos[(slot - kFlat0) >> 2] + (slot & 3u)) << 2;
     };
-    for (int w = lane; w < M::CW; w += 32) rec[w] = moved(C[2 * w]) | moved(C[2 * w + 1]) << 16;
+    for (int w = lane; w < M::CW; w += 32) rec[M::CODE0 + w] = moved(C[2 * w]) | moved(C[2 * w + 1]) << 16;
 }
 
 // tile occupancy: mark (z/8, x/8, y/16) of every particle of the level
@@ -1808,9 +1825,9 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
                 m.map_base[j] = static_cast<uint32_t>(lo[j]);
                 m.seg_shift[j] = static_cast<uint32_t>(lo[j] - m.tile_base - (j ? m.seg_end[j - 1] : 0));
             }
-            // 3^3: the build writes its chunk lists to scratch, k_map_place then
-            // writes them (and the codes) in their bank-aware order
-            const bool place = H == 1 && map_place_enabled();
+            // the build writes its chunk lists to scratch, k_map_place then writes
+            // them (and the codes) in their bank-aware order
+            const bool place = map_place_enabled();
             GpuBuf list_scratch;
             if (place) {  // (the build leaves a tile's padding entries alone: particle 0, like tile_flat's)
                 list_scratch.ensure(4 * L.tile_flat_n[H - 1] + 16);
@@ -1838,9 +1855,9 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
             if (place) {
                 TileLaunch pl = m;
                 pl.flat = L.tile_flat[H - 1];
-                const int bytes = place_smem(fl[1]);
-                APR_CUDA(cudaFuncSetAttribute(k_map_place, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-                k_map_place<<<total, 32, bytes, s>>>(pl, list_scratch.as<uint32_t>());
+                const int bytes = place_smem<H>(fl[1]);
+                APR_CUDA(cudaFuncSetAttribute(k_map_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+                k_map_place<H><<<total, 32, bytes, s>>>(pl, list_scratch.as<uint32_t>());
                 count_launch(apr->ctx);
                 APR_CUDA(cudaGetLastError());
                 APR_CUDA(cudaStreamSynchronize(s));
