@@ -568,23 +568,25 @@ __device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int q
                     r[2 * pp] = static_cast<Acc>(t2.x);
                     r[2 * pp + 1] = static_cast<Acc>(t2.y);
                 }
+                // ay outermost: the row's (up to 8) accumulator chains interleave
+                // (each still sees ay ascending -- the same order, bit-identical)
 #pragma unroll
-                for (int oz = 0; oz < 2; ++oz) {
-                    const int az = oz + 2 * H - nz;
-                    if (az < 0 || az > 2 * H) continue;
+                for (int ay = 0; ay < K; ++ay)
 #pragma unroll
-                    for (int ox = 0; ox < 2; ++ox) {
-                        const int ax = ox + 2 * H - nx;
-                        if (ax < 0 || ax > 2 * H) continue;
+                    for (int oz = 0; oz < 2; ++oz) {
+                        const int az = oz + 2 * H - nz;
+                        if (az < 0 || az > 2 * H) continue;
 #pragma unroll
-                        for (int oy = 0; oy < 2; ++oy)
+                        for (int ox = 0; ox < 2; ++ox) {
+                            const int ax = ox + 2 * H - nx;
+                            if (ax < 0 || ax > 2 * H) continue;
 #pragma unroll
-                            for (int ay = 0; ay < K; ++ay)
+                            for (int oy = 0; oy < 2; ++oy)
                                 acc[(oz * 2 + ox) * 2 + oy] = fma_t<Acc>(W[(az * K + ax) * K + ay],
                                                                          r[SH + oy + 2 * H - ay],
                                                                          acc[(oz * 2 + ox) * 2 + oy]);
+                        }
                     }
-                }
             }
     }
 }
@@ -1303,43 +1305,46 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
 // build, after it).  The apply's source loads (k_conv_map: one warp-load per
 // neighbourhood cell of its 32 blocks) gather from F through the codes, and a
 // warp-load costs as many shared-memory wavefronts as the most-requested bank
-// holds distinct words -- ~3.3 for the F order the build leaves (its banks are
-// as good as random).  A chunk's bank is fixed by its F position mod 8, and
+// holds distinct words; the build's F order leaves those banks as good as
+// random.  A chunk's bank is fixed by its F position mod 8 (its colour), and
 // permuting the chunks WITHIN each aligned group of 32 list entries changes
 // nothing else: a warp's gather copies the same 32 chunks (same cache lines,
-// lanes reordered) and the list-in-F rounds keep their invariant.  So: every
-// value-load instruction of the tile's apply is enumerated, and the chunks --
-// most-referenced first -- greedily take the colour (position mod 8) that
-// raises those instructions' bank maxima least, within their group's
-// capacity.  The list and the codes are then rewritten to the chosen
-// positions.  Only interior tiles (no padding cells) are permuted: their codes,
-// blocks and hence this deterministic placement are the same under both pad
-// modes, which share one chunk list.  Results are bit-identical (the same
-// values, elsewhere in F); tools/dump_maps.py + DESIGN §3 give the numbers.
+// lanes reordered) and the list-in-F rounds keep their invariant.  So every
+// value-load instruction of the tile's apply is enumerated, and the chunks
+// take colours greedily -- in steps: the r-th most-referenced chunk of each
+// group of one half of the groups picks, against the histogram as it stood at
+// the step's start, the colour (within its group's remaining capacity) that
+// raises those instructions' bank maxima least; then the step's picks are
+// added.  The list and the codes
+// are rewritten to the chosen positions.  Only interior tiles (no padding
+// cells) are permuted: their codes and blocks, and so this deterministic
+// placement, are the same under both pad modes, which share one chunk list.
+// Results are bit-identical (the same values, elsewhere in F).
 // 5^3 (H = 2): the same for the loads of the box expansion (every box cell, 8
 // consecutive cells per lane; the apply then reads the expanded box).
 constexpr int kPlaceMaxRounds = 8;                        // kBlocks / 32 warp-rounds of apply blocks
 constexpr int kPlaceMaxI = 64 * kPlaceMaxRounds;          // 3^3: 64 value loads per warp-round (5^3: 8 per round, 21 rounds)
+constexpr int kPlaceWarps = 16;
 template <int H>
 __host__ __device__ constexpr int place_smem(int nch) {  // (per-chunk arrays after the fixed ones)
-    return 2 * MapBox<H>::NC + kBlocks + kPlaceMaxI * 32 + 4 * kPlaceMaxI + 2 * kPlaceMaxI * 32 + 4 * 64 +
-           4 * (nch + 1) + 4 * nch + 2 * nch + nch + 2 * nch + 8 * (nch / 32 + 1) + 16;
+    return 2 * MapBox<H>::NC + kBlocks + kPlaceMaxI * 32 + 4 * kPlaceMaxI + 2 * kPlaceMaxI * 32 + 4 * (nch + 1) +
+           4 * nch + 2 * nch + 2 * nch + 11 * (nch / 32 + 1) + 16;
 }
 
 template <int H>
-__global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLaunch a, const uint32_t* __restrict__ list_in) {
+__global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_constant__ TileLaunch a,
+                                                                const uint32_t* __restrict__ list_in) {
     using M = MapBox<H>;
     static_assert(H == 1 || (M::NC / 8 + 31) / 32 * 8 <= kPlaceMaxI, "5^3 expansion loads");
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(16) unsigned char psm[];
-    uint16_t* C = reinterpret_cast<uint16_t*>(psm);                   // the codes (byte offsets into F)
-    uint8_t* BL = psm + 2 * M::NC;                                    // active blocks
-    uint8_t* Hh = BL + kBlocks;                                       // [I][32] distinct words per bank
-    uint32_t* cur = reinterpret_cast<uint32_t*>(Hh + kPlaceMaxI * 32);  // [I] bank maximum
-    uint16_t* refs = reinterpret_cast<uint16_t*>(cur + kPlaceMaxI);     // per chunk: (instruction << 2 | word)
-    uint32_t* bins = reinterpret_cast<uint32_t*>(refs + kPlaceMaxI * 32);
-    uint32_t* roff = bins + 64;
-    const int lane = threadIdx.x;
+    uint16_t* C = reinterpret_cast<uint16_t*>(psm);                       // the codes (byte offsets into F)
+    uint8_t* BL = psm + 2 * M::NC;                                        // active blocks
+    uint32_t* Hh = reinterpret_cast<uint32_t*>(BL + kBlocks);             // [I][32] u8: distinct words per bank
+    uint32_t* cur = Hh + kPlaceMaxI * 8;                                  // [I] bank maximum
+    uint16_t* refs = reinterpret_cast<uint16_t*>(cur + kPlaceMaxI);        // per chunk: (instruction << 2 | word)
+    uint32_t* roff = reinterpret_cast<uint32_t*>(refs + kPlaceMaxI * 32);  // [nch + 1]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int s = seg_of(a.seg_end, a.n_levels, blockIdx.x);
     const int l = a.lvl[s];
     const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
@@ -1352,153 +1357,162 @@ __global__ void __launch_bounds__(32) k_map_place(const __grid_constant__ TileLa
     const bool interior = G.z0 - H >= 0 && G.x0 - H >= 0 && G.y0 - H >= 0 && G.z0 + kTZ + H <= g.zd &&
                           G.x0 + kTX + H <= g.xd && G.y0 + kTY + H <= g.yd;
     if (!interior || nb == 0 || nch <= 8) {  // the build's order
-        for (int c = lane; c < nch; c += 32) a.flat[f0 + c] = list_in[f0 + c];
+        for (int c = threadIdx.x; c < nch; c += blockDim.x) a.flat[f0 + c] = list_in[f0 + c];
         return;
     }
     uint32_t* cnt = roff + nch + 1;
-    uint16_t* order = reinterpret_cast<uint16_t*>(cnt + nch);
-    uint8_t* col = reinterpret_cast<uint8_t*>(order + nch);
-    uint16_t* npos = reinterpret_cast<uint16_t*>(col + ((nch + 1) & ~1));
-    uint8_t* cap = reinterpret_cast<uint8_t*>(npos + nch);
-    constexpr int NG8 = M::NC / 8;  // 5^3: the expansion's 8-cell groups
+    uint16_t* order = reinterpret_cast<uint16_t*>(cnt + nch);  // per group: its chunks, most-referenced first
+    uint16_t* npos = order + nch;
+    uint16_t* pick = npos + nch;                             // per group: this round's chunk and colour
+    uint8_t* cap = reinterpret_cast<uint8_t*>(pick + ((nch + 31) >> 5));  // [group][colour] positions left
+    uint8_t* pk = cap + 8 * ((nch + 31) >> 5);
+    constexpr int NG8 = M::NC / 8;                           // 5^3: the expansion's 8-cell groups
     const int nwr = H == 1 ? (nb + 31) >> 5 : (NG8 + 31) >> 5, ni = (H == 1 ? 64 : 8) * nwr, ng = (nch + 31) >> 5;
-    for (int w = lane; w < M::CW; w += 32) reinterpret_cast<uint32_t*>(C)[w] = rec[M::CODE0 + w];
-    for (int q = lane; q < nb; q += 32) BL[q] = reinterpret_cast<const uint8_t*>(rec + M::W_BLK)[q];
-    for (int i = lane; i < ni * 32; i += 32) Hh[i] = 0;
-    for (int i = lane; i < ni; i += 32) cur[i] = 0;
-    for (int c = lane; c < nch; c += 32) cnt[c] = 0;
-    for (int k = lane; k < 64; k += 32) bins[k] = 0;
-    for (int i = lane; i < 8 * ng; i += 32) {
+    for (int w = threadIdx.x; w < M::CW; w += blockDim.x) reinterpret_cast<uint32_t*>(C)[w] = rec[M::CODE0 + w];
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) BL[q] = reinterpret_cast<const uint8_t*>(rec + M::W_BLK)[q];
+    for (int i = threadIdx.x; i < ni * 8; i += blockDim.x) Hh[i] = 0;
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) cnt[c] = 0;
+    for (int i = threadIdx.x; i < 8 * ng; i += blockDim.x) {
         const int gi = i >> 3, k = i & 7, n_g = min(32, nch - 32 * gi);
         cap[i] = static_cast<uint8_t>(k < n_g ? (n_g - k + 7) / 8 : 0);
     }
-    __syncwarp();
-    // the apply's value loads: warp-round j = blocks [32j, 32j + 32) (k_conv_map's q loop), load t =
-    // (row nz, nx; pair pp; half h); each lane's slot (F word); distinct words counted once
+    __syncthreads();
+    auto hinc = [&](int i, uint32_t b) {  // one more distinct word in bank b of load i; returns the new count
+        const uint32_t sh = 8 * (b & 3);
+        return ((atomicAdd(&Hh[i * 8 + (b >> 2)], 1u << sh) >> sh) & 0xffu) + 1u;
+    };
+    auto hget = [&](int i, uint32_t b) { return (Hh[i * 8 + (b >> 2)] >> (8 * (b & 3))) & 0xffu; };
+    // the loads: 3^3 warp-round j = apply blocks [32j, 32j + 32) (k_conv_map's q loop), load t = (row
+    // nz, nx; pair pp; half h); 5^3 round j = expansion groups [32j, 32j + 32), load t = cell 8g + t.
+    // Each lane's slot (F word); distinct words counted once.  Warp w takes rounds w, w + nw, ...
     auto each_load = [&](auto&& f) {
-        if constexpr (H == 2) {  // group g = 32j + lane, load t: cell 8g + t
-            for (int j = 0; j < nwr; ++j) {
+        for (int j = warp; j < nwr; j += nw) {
+            if constexpr (H == 2) {
                 const int gq = 32 * j + lane;
                 for (int t = 0; t < 8; ++t) {
                     const uint32_t slot = gq < NG8 ? C[8 * gq + t] >> 2 : 0xffffu;
                     const unsigned m = __match_any_sync(FULL, slot);
                     if (slot != 0xffffu && lane == __ffs(m) - 1) f(8 * j + t, slot);
                 }
-            }
-            return;
-        }
-        for (int j = 0; j < nwr; ++j) {
-            const int q = 32 * j + lane;
-            int base = -1;
-            if (q < nb) {
-                const int b = BL[q];
-                base = ((2 * (b / (kBlocks / 4))) * M::BX + 2 * ((b / (kTY / 2)) & 3)) * M::BY + 2 * (b & (kTY / 2 - 1));
-            }
-            for (int t = 0; t < 64; ++t) {
-                const int nz = t >> 4, nx = (t >> 2) & 3, pp = (t >> 1) & 1, h = t & 1;
-                const uint32_t slot = base >= 0 ? C[base + (nz * M::BX + nx) * M::BY + 2 * pp + h] >> 2 : 0xffffu;
-                const unsigned m = __match_any_sync(FULL, slot);
-                if (slot != 0xffffu && lane == __ffs(m) - 1) f(64 * j + t, slot);
+            } else {
+                const int q = 32 * j + lane;
+                int base = -1;
+                if (q < nb) {
+                    const int b = BL[q];
+                    base = ((2 * (b / (kBlocks / 4))) * M::BX + 2 * ((b / (kTY / 2)) & 3)) * M::BY +
+                           2 * (b & (kTY / 2 - 1));
+                }
+                for (int t = 0; t < 64; ++t) {
+                    const int nz = t >> 4, nx = (t >> 2) & 3, pp = (t >> 1) & 1, h = t & 1;
+                    const uint32_t slot = base >= 0 ? C[base + (nz * M::BX + nx) * M::BY + 2 * pp + h] >> 2 : 0xffffu;
+                    const unsigned m = __match_any_sync(FULL, slot);
+                    if (slot != 0xffffu && lane == __ffs(m) - 1) f(64 * j + t, slot);
+                }
             }
         }
     };
     each_load([&](int i, uint32_t slot) {
-        if (slot < kFlat0) Hh[i * 32 + ((M::REC + slot) & 31)] = 1;  // (the zero's 4 words: 4 banks)
+        if (slot < kFlat0) hinc(i, (M::REC + slot) & 31);  // (the zero's 4 words: 4 banks)
         else atomicAdd(&cnt[(slot - kFlat0) >> 2], 1u);
     });
-    __syncwarp();
-    for (int i = 0; i < ni; ++i) {
-        const unsigned v = __reduce_max_sync(FULL, static_cast<unsigned>(Hh[i * 32 + lane]));
+    __syncthreads();
+    for (int i = warp; i < ni; i += nw) {
+        const unsigned v = __reduce_max_sync(FULL, hget(i, lane));
         if (lane == 0) cur[i] = v;
     }
-    // roff = exclusive scan of cnt; cnt becomes the fill cursor
-    uint32_t carry = 0;
-    for (int c0 = 0; c0 < nch; c0 += 32) {
-        const int c = c0 + lane;
-        const uint32_t v = c < nch ? cnt[c] : 0u;
-        uint32_t x = v;
+    if (warp == 0) {  // roff = exclusive scan of cnt
+        uint32_t carry = 0;
+        for (int c0 = 0; c0 < nch; c0 += 32) {
+            const int c = c0 + lane;
+            const uint32_t v = c < nch ? cnt[c] : 0u;
+            uint32_t x = v;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, x, d);
-            if (lane >= d) x += y;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, x, d);
+                if (lane >= d) x += y;
+            }
+            if (c < nch) roff[c] = carry + x - v;
+            carry += __shfl_sync(FULL, x, 31);
         }
-        if (c < nch) roff[c] = carry + x - v;
-        carry += __shfl_sync(FULL, x, 31);
+        if (lane == 0) roff[nch] = carry;
     }
-    if (lane == 0) roff[nch] = carry;
-    __syncwarp();
-    for (int c = lane; c < nch; c += 32) cnt[c] = roff[c];
-    __syncwarp();
+    __syncthreads();
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) cnt[c] = roff[c];  // (the fill cursors)
+    __syncthreads();
     each_load([&](int i, uint32_t slot) {
         if (slot >= kFlat0) {
             const uint32_t c = (slot - kFlat0) >> 2;
             refs[atomicAdd(&cnt[c], 1u)] = static_cast<uint16_t>(i << 2 | (slot & 3u));
         }
     });
-    __syncwarp();
-    // most-referenced chunks first (stable counting sort on min(refs, 63), descending)
-    auto key_of = [&](int c) { return 63 - min(static_cast<int>(roff[c + 1] - roff[c]), 63); };
-    for (int c = lane; c < nch; c += 32) atomicAdd(&bins[key_of(c)], 1u);
-    __syncwarp();
-    if (lane == 0)
-        for (int k = 0, acc = 0; k < 64; ++k) {
-            const int v = static_cast<int>(bins[k]);
-            bins[k] = acc;
-            acc += v;
+    // per group: its chunks by reference count, descending (ties: chunk order)
+    for (int gi = warp; gi < ng; gi += nw) {
+        const int c = 32 * gi + lane;
+        const uint32_t nr = c < nch ? roff[c + 1] - roff[c] : 0u;
+        int rank = 0;
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t o = __shfl_sync(FULL, nr, j);
+            rank += (o > nr || (o == nr && j < lane)) ? 1 : 0;
         }
-    __syncwarp();
-    for (int c0 = 0; c0 < nch; c0 += 32) {
-        const int c = c0 + lane;
-        const int key = c < nch ? key_of(c) : 64 + lane;
-        const unsigned m = __match_any_sync(FULL, key);
-        if (c < nch) order[bins[key] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(c);
-        __syncwarp();
-        if (c < nch && lane == __ffs(m) - 1) bins[key] += __popc(m);
-        __syncwarp();
+        if (c < nch) order[32 * gi + rank] = static_cast<uint16_t>(c);
     }
-    // greedy colours: lane = (colour k = lane & 7, a quarter of the chunk's references)
+    __syncthreads();
+    // greedy colours in rounds: lane = (colour k = lane & 7, a quarter of the chunk's references)
     const int k = lane & 7;
-    for (int oi = 0; oi < nch; ++oi) {
-        const int c = order[oi], gi = c >> 5;
-        const uint32_t r0 = roff[c], r1 = roff[c + 1];
-        uint32_t cost = 0;
-        for (uint32_t r = r0 + (lane >> 3); r < r1; r += 4) {
-            const uint32_t e = refs[r], i = e >> 2;
-            const uint32_t h = Hh[i * 32 + ((M::REC + kFlat0 + (e & 3u) + 4u * k) & 31u)], cu = cur[i];
-            cost += max(cu, h + 1u) - cu;
+    // (half of the groups per step: picks made together do not see each other,
+    // and fewer of them keep the greedy close to one-at-a-time)
+    for (int rr = 0; rr < 2 * 32; ++rr) {
+        const int r = rr >> 1, part = rr & 1;
+        for (int gi = 2 * warp + part; gi < ng; gi += 2 * nw) {
+            if (32 * gi + r >= nch) continue;
+            const int c = order[32 * gi + r];
+            const uint32_t r0 = roff[c], r1 = roff[c + 1];
+            uint32_t cost = 0;
+            for (uint32_t e0 = r0 + (lane >> 3); e0 < r1; e0 += 4) {
+                const uint32_t e = refs[e0], i = e >> 2;
+                const uint32_t h = hget(i, (M::REC + kFlat0 + (e & 3u) + 4u * k) & 31u), cu = cur[i];
+                cost += max(cu, h + 1u) - cu;
+            }
+            cost += __shfl_xor_sync(FULL, cost, 8);
+            cost += __shfl_xor_sync(FULL, cost, 16);
+            const uint32_t key = cap[8 * gi + k] ? (cost << 3 | static_cast<uint32_t>(k)) : 0xffffffffu;
+            const int kb = static_cast<int>(__reduce_min_sync(FULL, key) & 7u);
+            if (lane == 0) {
+                pick[gi] = static_cast<uint16_t>(c);
+                pk[gi] = static_cast<uint8_t>(kb);
+            }
         }
-        cost += __shfl_xor_sync(FULL, cost, 8);
-        cost += __shfl_xor_sync(FULL, cost, 16);
-        const uint32_t key = cap[8 * gi + k] ? (cost << 3 | static_cast<uint32_t>(k)) : 0xffffffffu;
-        const int kb = static_cast<int>(__reduce_min_sync(FULL, key) & 7u);
-        __syncwarp();
-        if (lane == 0) {
-            --cap[8 * gi + kb];
-            col[c] = static_cast<uint8_t>(kb);
+        __syncthreads();  // (every pick of the step made against the same histogram)
+        for (int gi = 2 * warp + part; gi < ng; gi += 2 * nw) {
+            if (32 * gi + r >= nch) continue;
+            const int c = pick[gi], kb = pk[gi];
+            if (lane == 0) {
+                --cap[8 * gi + kb];
+                npos[c] = static_cast<uint16_t>(kb);  // (the colour; positions below)
+            }
+            for (uint32_t e0 = roff[c] + lane; e0 < roff[c + 1]; e0 += 32) {
+                const uint32_t e = refs[e0], i = e >> 2;
+                atomicMax(&cur[i], hinc(i, (M::REC + kFlat0 + (e & 3u) + 4u * kb) & 31u));
+            }
         }
-        for (uint32_t r = r0 + lane; r < r1; r += 32) {  // (a chunk's words in one load: distinct banks)
-            const uint32_t e = refs[r], i = e >> 2;
-            uint8_t& h = Hh[i * 32 + ((M::REC + kFlat0 + (e & 3u) + 4u * kb) & 31u)];
-            h = static_cast<uint8_t>(h + 1);
-            atomicMax(&cur[i], static_cast<uint32_t>(h));
-        }
-        __syncwarp();
+        __syncthreads();
     }
     // positions: a group's chunks of colour k take its positions k, k + 8, ... in chunk order
-    for (int gi = 0; gi < ng; ++gi) {
+    for (int gi = warp; gi < ng; gi += nw) {
         const int c = 32 * gi + lane;
-        const int kk = c < nch ? col[c] : 8 + lane;
+        const int kk = c < nch ? npos[c] : 8 + lane;
         const unsigned m = __match_any_sync(FULL, kk);
         if (c < nch) npos[c] = static_cast<uint16_t>(32 * gi + kk + 8 * __popc(m & ((1u << lane) - 1u)));
     }
-    __syncwarp();
-    for (int c = lane; c < nch; c += 32) a.flat[f0 + npos[c]] = list_in[f0 + c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) a.flat[f0 + npos[c]] = list_in[f0 + c];
     auto moved = [&](uint32_t code) -> uint32_t {
         const uint32_t slot = code >> 2;
         if (slot < kFlat0) return code;
         return (kFlat0 + 4u * npos[(slot - kFlat0) >> 2] + (slot & 3u)) << 2;
     };
-    for (int w = lane; w < M::CW; w += 32) rec[M::CODE0 + w] = moved(C[2 * w]) | moved(C[2 * w + 1]) << 16;
+    for (int w = threadIdx.x; w < M::CW; w += blockDim.x)
+        rec[M::CODE0 + w] = moved(C[2 * w]) | moved(C[2 * w + 1]) << 16;
 }
 
 // tile occupancy: mark (z/8, x/8, y/16) of every particle of the level
@@ -1857,7 +1871,7 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
                 pl.flat = L.tile_flat[H - 1];
                 const int bytes = place_smem<H>(fl[1]);
                 APR_CUDA(cudaFuncSetAttribute(k_map_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-                k_map_place<H><<<total, 32, bytes, s>>>(pl, list_scratch.as<uint32_t>());
+                k_map_place<H><<<total, 32 * kPlaceWarps, bytes, s>>>(pl, list_scratch.as<uint32_t>());
                 count_launch(apr->ctx);
                 APR_CUDA(cudaGetLastError());
                 APR_CUDA(cudaStreamSynchronize(s));
