@@ -82,6 +82,14 @@ typedef struct {
     uint64_t n_particles, n_rows;
 } aprgpu_access_info;
 
+/* Page-locked host memory for callers' copy buffers (cudaHostAlloc,
+ * portable): host-pointer calls copy such buffers directly instead of through
+ * the context's staging -- per array, so pageable inputs with a page-locked
+ * output (or the reverse) stage only the pageable side (new, no reference
+ * counterpart). */
+int aprgpu_host_alloc(uint64_t bytes, void** out);
+int aprgpu_host_free(void* p);
+
 /* ---- context ------------------------------------------------------------- */
 int aprgpu_init(int device, aprgpu_ctx** out);
 int aprgpu_ctx_free(aprgpu_ctx* ctx);

@@ -82,6 +82,8 @@ _SIGS = {
                   C.c_void_p, C.c_int, C.c_void_p],
     "aprgpu_rl_resume": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                          C.c_double, C.c_int, C.c_void_p, C.c_int, C.c_void_p],
+    "aprgpu_host_alloc": [C.c_uint64, C.POINTER(C.c_void_p)],
+    "aprgpu_host_free": [C.c_void_p],
     "aprgpu_sequential_sum": [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_double), C.c_void_p],
     "aprgpu_fill_tree_sums": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p],
     "aprgpu_tree_scratch": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],

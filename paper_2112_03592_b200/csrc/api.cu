@@ -420,7 +420,11 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
         }
         return at.type == cudaMemoryTypeHost;
     };
-    const bool staged = !pinned(values) || !pinned(out) || (nt && !pinned(tree_values));
+    // staging per array: a page-locked array is copied directly, a pageable one
+    // through the pinned staging (the C++ drop-in hands in pageable inputs and a
+    // page-locked output buffer)
+    const bool st_val = !pinned(values), st_tree = nt && !pinned(tree_values), st_out = !pinned(out);
+    const bool staged = st_val || st_tree || st_out;
     const size_t stage_need = 4 * (2 * np + nt);
     if (staged && stage_need > static_cast<size_t>(std::max(env_int("APRGPU_STAGE_MAX_MB", 4096), 0)) << 20)
         return false;
@@ -465,9 +469,9 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
             ctx->pool = new aprgpu::HostPool(std::max(1, env_int("APRGPU_HOST_THREADS", std::min(8, std::max(1, hc / 2)))));
         }
         float* st = static_cast<float*>(ctx->stage);
-        h_val = st;
-        h_tree = st + np;
-        h_out = st + np + nt;
+        if (st_val) h_val = st;
+        if (st_tree) h_tree = st + np;
+        if (st_out) h_out = st + np + nt;
     }
     // few, large copies: the finest level's rows carry ~90 % of the particles,
     // so chunk 0 takes every coarser level whole and each later chunk one
@@ -508,11 +512,14 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
         for (int j = 0; j < K; ++j) {
             const size_t n0 = pin.size();
             for (const Range& r : in_r[j])
-                cut(pin, const_cast<float*>(r.arr == 0 ? h_val : h_tree), r.arr == 0 ? values : tree_values, r.b, r.e, j);
+                if (r.arr == 0 ? st_val : st_tree)
+                    cut(pin, const_cast<float*>(r.arr == 0 ? h_val : h_tree), r.arr == 0 ? values : tree_values, r.b,
+                        r.e, j);
             left[j].store(static_cast<int>(pin.size() - n0));
         }
-        for (int j = 0; j <= K; ++j)
-            for (const Range& r : out_r[j]) cut(pout, out, h_out, r.b, r.e, j);
+        if (st_out)
+            for (int j = 0; j <= K; ++j)
+                for (const Range& r : out_r[j]) cut(pout, out, h_out, r.b, r.e, j);
     }
     std::atomic<size_t> next{0};
     struct Join {  // an error below must not leave the workers on this frame's pieces
@@ -589,6 +596,20 @@ bool convolve_host_pipelined(aprgpu_apr* apr, const float* values, const float* 
 extern "C" {
 
 const char* aprgpu_last_error(void) { return g_last_error.c_str(); }
+
+int aprgpu_host_alloc(uint64_t bytes, void** out) {
+    return guard([&] {
+        need(out != nullptr, "null out");
+        *out = nullptr;
+        if (bytes) APR_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+    });
+}
+
+int aprgpu_host_free(void* p) {
+    return guard([&] {
+        if (p) APR_CUDA(cudaFreeHost(p));
+    });
+}
 int aprgpu_version(void) { return 1; }
 
 int aprgpu_init(int device, aprgpu_ctx** out) {

@@ -37,6 +37,26 @@ def _pageable_call(dev, values, tree, dpyr, pad, accum):
     return ho
 
 
+def _mixed_call(dev, values, tree, dpyr, pad, accum, pinned_out):
+    """Per-array staging: pageable inputs with a page-locked output (the C++
+    drop-in's convolve_apr), or page-locked inputs with a pageable output."""
+    import torch
+    if pinned_out:
+        hv = np.ascontiguousarray(values, np.float32)
+        ht = np.ascontiguousarray(tree, np.float32)
+        vp, tp = hv.ctypes.data, (ht.ctypes.data if ht.size else None)
+        ho = torch.full((dev.n_particles,), float("nan"), dtype=torch.float32).pin_memory()
+        op = ho.data_ptr()
+    else:
+        hv = torch.from_numpy(np.ascontiguousarray(values, np.float32)).pin_memory()
+        ht = torch.from_numpy(np.ascontiguousarray(tree, np.float32) if tree.size else np.zeros(1, np.float32)).pin_memory()
+        vp, tp = hv.data_ptr(), (ht.data_ptr() if tree.size else None)
+        ho = np.full(dev.n_particles, np.nan, np.float32)
+        op = ho.ctypes.data
+    L.check(L.lib().aprgpu_convolve(dev.handle, vp, tp, dpyr.handle, int(pad), accum, op, L.HOST, None))
+    return ho.numpy().copy() if pinned_out else ho
+
+
 def _device_call(dev, values, tree, dpyr, pad, accum):
     import torch
     v = torch.from_numpy(np.ascontiguousarray(values, np.float32)).cuda()
@@ -74,6 +94,9 @@ def test_pipelined_host_convolve_bit_identical(name, chunks, monkeypatch):
                     assert np.array_equal(G.bits(got), G.bits(exp)), (w.kz, accum, int(pad), path)
                     got = _pageable_call(dev, values, tree, dpyr, pad, accum)
                     assert np.array_equal(G.bits(got), G.bits(exp)), ("pageable", w.kz, accum, int(pad), path)
+                    for po in (True, False):
+                        got = _mixed_call(dev, values, tree, dpyr, pad, accum, po)
+                        assert np.array_equal(G.bits(got), G.bits(exp)), ("mixed", po, w.kz, accum, int(pad), path)
 
 
 def test_pipelined_host_convolve_c3(monkeypatch):
@@ -91,3 +114,5 @@ def test_pipelined_host_convolve_c3(monkeypatch):
             assert np.array_equal(G.bits(got), G.bits(exp)), (k, accum)
             got = _pageable_call(dev, values, tree, dpyr, P.PadMode.Reflect, accum)
             assert np.array_equal(G.bits(got), G.bits(exp)), ("pageable", k, accum)
+            got = _mixed_call(dev, values, tree, dpyr, P.PadMode.Reflect, accum, True)
+            assert np.array_equal(G.bits(got), G.bits(exp)), ("mixed", k, accum)

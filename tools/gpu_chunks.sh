@@ -1,0 +1,6 @@
+# e2e (pinned host buffers, pipelined over z-chunks) vs APRGPU_HOST_CHUNKS
+mkdir -p gpurun_out
+for c in 8 12 16 24 8; do
+APRGPU_HOST_CHUNKS=$c timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/chunks_$c.json 2>/dev/null
+python -c "import json; d=json.load(open('gpurun_out/chunks_$c.json')); print('chunks', $c, 'e2e ms', d['e2e']['ms_per_step'], 'conv', d['ms_per_step'])"
+done
