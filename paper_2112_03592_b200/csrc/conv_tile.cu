@@ -1160,10 +1160,16 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     if (kSepOk && sep && tid < 3 * K) SF[tid] = a.sep[s][tid];
     const int l = a.lvl[s];
     const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
-    const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
-    const RowRange rr = slab_rows(a, l, z0);
-    if (rr.lo >= rr.hi) return;  // slab decomposition: no row of this tile is in the slab
     const uint32_t* rec = a.map[s] + static_cast<size_t>(tix - a.map_base[s]) * M::REC;
+    // a slab launch's tiles straddling the slab: the row range needs the tile's
+    // z (a load); other launches decide nothing from it, so the record's copy
+    // is issued first
+    RowRange rr{0, kTZ};
+    if (l >= a.slab_lc) {
+        const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
+        rr = slab_rows(a, l, z0);
+        if (rr.lo >= rr.hi) return;  // slab decomposition: no row of this tile is in the slab
+    }
     // the record and the tile's chunk list stream in by two bulk copies; the
     // record's is issued before the list's extent is known (its bytes are
     // expected without an arrival; the one arrival comes with the list's)
