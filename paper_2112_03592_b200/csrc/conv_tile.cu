@@ -95,6 +95,7 @@ struct TileLaunch {
     uint32_t map_base[kMaxLevels];    // per segment: the tile whose record is map[s][0]
     uint32_t* flat;                   // per H flattened source lists (DevAccess::tile_flat)
     const uint32_t* flat_off;         // n_tiles + 1 offsets into flat
+    int place_drop;                   // k_map_place: drop the chunks no active block reads (3^3)
     int* map_overflow;                // set by the build when a tile has > MapBox::NC sources
     int* map_maxg;                    // the build's largest per-tile chunk count (atomicMax)
     uint32_t n_leaf, n_tree;          // value-array lengths (a tail chunk copies only valid elements)
@@ -1220,15 +1221,18 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
                 if ((e & kChunkIdx) + k < lim) cp_async4(dst + k, src + k);
         }
     };
+    // the chunks to gather: the record's count (3^3: the placement pass drops
+    // chunks no active block reads, so it can be below the list's extent)
+    const uint32_t ng = Mb[M::W_NLEAF];
     if (list_in_f) {
-        for (uint32_t c0 = 0; c0 < nchunk; c0 += NT) {  // (uniform trip count)
+        for (uint32_t c0 = 0; c0 < ng; c0 += NT) {  // (uniform trip count)
             const uint32_t c = c0 + tid;
-            const uint32_t e = c < nchunk ? Gs[c] : 0u;
+            const uint32_t e = c < ng ? Gs[c] : 0u;
             __syncthreads();  // the round's entries are read before its copies may overwrite them
-            if (c < nchunk) gather(c, e);
+            if (c < ng) gather(c, e);
         }
     } else {
-        for (uint32_t c = tid; c < nchunk; c += NT) gather(c, Gs[c]);
+        for (uint32_t c = tid; c < ng; c += NT) gather(c, Gs[c]);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -1334,7 +1338,7 @@ constexpr int kPlaceWarps = 16;
 template <int H>
 __host__ __device__ constexpr int place_smem(int nch) {  // (per-chunk arrays after the fixed ones)
     return 2 * MapBox<H>::NC + kBlocks + kPlaceMaxI * 32 + 4 * kPlaceMaxI + 2 * kPlaceMaxI * 32 + 4 * (nch + 1) +
-           4 * nch + 2 * nch + 2 * nch + 11 * (nch / 32 + 1) + 16;
+           4 * nch + 2 * nch + 2 * nch + 2 * nch + 2 * nch + 11 * (nch / 32 + 1) + 32;
 }
 
 template <int H>
@@ -1369,19 +1373,18 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_con
     uint32_t* cnt = roff + nch + 1;
     uint16_t* order = reinterpret_cast<uint16_t*>(cnt + nch);  // per group: its chunks, most-referenced first
     uint16_t* npos = order + nch;
-    uint16_t* pick = npos + nch;                             // per group: this round's chunk and colour
+    uint16_t* kidx = npos + nch;  // 3^3: a chunk's position among the kept ones (0xffff: dropped)
+    uint16_t* kc = kidx + nch;    // the kept chunks in order
+    uint16_t* pick = kc + nch;    // per group: this round's chunk and colour
     uint8_t* cap = reinterpret_cast<uint8_t*>(pick + ((nch + 31) >> 5));  // [group][colour] positions left
     uint8_t* pk = cap + 8 * ((nch + 31) >> 5);
+    __shared__ int nkeep_s;
     constexpr int NG8 = M::NC / 8;                           // 5^3: the expansion's 8-cell groups
-    const int nwr = H == 1 ? (nb + 31) >> 5 : (NG8 + 31) >> 5, ni = (H == 1 ? 64 : 8) * nwr, ng = (nch + 31) >> 5;
+    const int nwr = H == 1 ? (nb + 31) >> 5 : (NG8 + 31) >> 5, ni = (H == 1 ? 64 : 8) * nwr;
     for (int w = threadIdx.x; w < M::CW; w += blockDim.x) reinterpret_cast<uint32_t*>(C)[w] = rec[M::CODE0 + w];
     for (int q = threadIdx.x; q < nb; q += blockDim.x) BL[q] = reinterpret_cast<const uint8_t*>(rec + M::W_BLK)[q];
     for (int i = threadIdx.x; i < ni * 8; i += blockDim.x) Hh[i] = 0;
     for (int c = threadIdx.x; c < nch; c += blockDim.x) cnt[c] = 0;
-    for (int i = threadIdx.x; i < 8 * ng; i += blockDim.x) {
-        const int gi = i >> 3, k = i & 7, n_g = min(32, nch - 32 * gi);
-        cap[i] = static_cast<uint8_t>(k < n_g ? (n_g - k + 7) / 8 : 0);
-    }
     __syncthreads();
     auto hinc = [&](int i, uint32_t b) {  // one more distinct word in bank b of load i; returns the new count
         const uint32_t sh = 8 * (b & 3);
@@ -1426,6 +1429,23 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_con
         const unsigned v = __reduce_max_sync(FULL, hget(i, lane));
         if (lane == 0) cur[i] = v;
     }
+    // 3^3: chunks no load references (sources only inactive regions read) are
+    // dropped -- kidx = their rank among the kept ones; groups, colours and
+    // positions below are over the kept chunks (5^3's expansion reads every
+    // box cell: every chunk is kept)
+    if (warp == 1 || nw == 1) {
+        int carry = 0;
+        for (int c0 = 0; c0 < nch; c0 += 32) {
+            const int c = c0 + lane;
+            const bool keep = c < nch && (H == 2 || !a.place_drop || cnt[c] > 0);
+            const unsigned b = __ballot_sync(FULL, keep);
+            const int p = carry + __popc(b & ((1u << lane) - 1u));
+            if (c < nch) kidx[c] = static_cast<uint16_t>(keep ? p : 0xffff);
+            if (keep) kc[p] = static_cast<uint16_t>(c);
+            carry += __popc(b);
+        }
+        if (lane == 0) nkeep_s = carry;
+    }
     if (warp == 0) {  // roff = exclusive scan of cnt
         uint32_t carry = 0;
         for (int c0 = 0; c0 < nch; c0 += 32) {
@@ -1451,16 +1471,22 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_con
             refs[atomicAdd(&cnt[c], 1u)] = static_cast<uint16_t>(i << 2 | (slot & 3u));
         }
     });
+    const int nk = nkeep_s, ngk = (nk + 31) >> 5;  // kept chunks, their groups of 32
+    for (int i = threadIdx.x; i < 8 * ngk; i += blockDim.x) {
+        const int gi = i >> 3, k = i & 7, n_g = min(32, nk - 32 * gi);
+        cap[i] = static_cast<uint8_t>(k < n_g ? (n_g - k + 7) / 8 : 0);
+    }
     // per group: its chunks by reference count, descending (ties: chunk order)
-    for (int gi = warp; gi < ng; gi += nw) {
-        const int c = 32 * gi + lane;
-        const uint32_t nr = c < nch ? roff[c + 1] - roff[c] : 0u;
+    for (int gi = warp; gi < ngk; gi += nw) {
+        const int p = 32 * gi + lane;
+        const int c = p < nk ? kc[p] : 0;
+        const uint32_t nr = p < nk ? roff[c + 1] - roff[c] : 0u;
         int rank = 0;
         for (int j = 0; j < 32; ++j) {
             const uint32_t o = __shfl_sync(FULL, nr, j);
             rank += (o > nr || (o == nr && j < lane)) ? 1 : 0;
         }
-        if (c < nch) order[32 * gi + rank] = static_cast<uint16_t>(c);
+        if (p < nk) order[32 * gi + rank] = static_cast<uint16_t>(c);
     }
     __syncthreads();
     // greedy colours in rounds: lane = (colour k = lane & 7, a quarter of the chunk's references)
@@ -1469,8 +1495,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_con
     // and fewer of them keep the greedy close to one-at-a-time)
     for (int rr = 0; rr < 2 * 32; ++rr) {
         const int r = rr >> 1, part = rr & 1;
-        for (int gi = 2 * warp + part; gi < ng; gi += 2 * nw) {
-            if (32 * gi + r >= nch) continue;
+        for (int gi = 2 * warp + part; gi < ngk; gi += 2 * nw) {
+            if (32 * gi + r >= nk) continue;
             const int c = order[32 * gi + r];
             const uint32_t r0 = roff[c], r1 = roff[c + 1];
             uint32_t cost = 0;
@@ -1489,8 +1515,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_con
             }
         }
         __syncthreads();  // (every pick of the step made against the same histogram)
-        for (int gi = 2 * warp + part; gi < ng; gi += 2 * nw) {
-            if (32 * gi + r >= nch) continue;
+        for (int gi = 2 * warp + part; gi < ngk; gi += 2 * nw) {
+            if (32 * gi + r >= nk) continue;
             const int c = pick[gi], kb = pk[gi];
             if (lane == 0) {
                 --cap[8 * gi + kb];
@@ -1504,21 +1530,27 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_con
         __syncthreads();
     }
     // positions: a group's chunks of colour k take its positions k, k + 8, ... in chunk order
-    for (int gi = warp; gi < ng; gi += nw) {
-        const int c = 32 * gi + lane;
-        const int kk = c < nch ? npos[c] : 8 + lane;
+    for (int gi = warp; gi < ngk; gi += nw) {
+        const int p = 32 * gi + lane;
+        const int c = p < nk ? kc[p] : 0;
+        const int kk = p < nk ? npos[c] : 8 + lane;
         const unsigned m = __match_any_sync(FULL, kk);
-        if (c < nch) npos[c] = static_cast<uint16_t>(32 * gi + kk + 8 * __popc(m & ((1u << lane) - 1u)));
+        if (p < nk) npos[c] = static_cast<uint16_t>(32 * gi + kk + 8 * __popc(m & ((1u << lane) - 1u)));
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) a.flat[f0 + npos[c]] = list_in[f0 + c];
+    for (int c = threadIdx.x; c < nch; c += blockDim.x)
+        if (kidx[c] != 0xffff) a.flat[f0 + npos[c]] = list_in[f0 + c];
+    for (int p = nk + threadIdx.x; p < nch; p += blockDim.x) a.flat[f0 + p] = 0u;  // (the dropped tail: particle 0)
     auto moved = [&](uint32_t code) -> uint32_t {
         const uint32_t slot = code >> 2;
         if (slot < kFlat0) return code;
-        return (kFlat0 + 4u * npos[(slot - kFlat0) >> 2] + (slot & 3u)) << 2;
+        const uint32_t c = (slot - kFlat0) >> 2;
+        if (kidx[c] == 0xffff) return 0u;  // (a cell no active block reads: the zero)
+        return (kFlat0 + 4u * npos[c] + (slot & 3u)) << 2;
     };
     for (int w = threadIdx.x; w < M::CW; w += blockDim.x)
         rec[M::CODE0 + w] = moved(C[2 * w]) | moved(C[2 * w + 1]) << 16;
+    if (threadIdx.x == 0) rec[M::W_NLEAF] = static_cast<uint32_t>(nk);  // (the chunks k_conv_map gathers)
 }
 
 // tile occupancy: mark (z/8, x/8, y/16) of every particle of the level
@@ -1713,6 +1745,15 @@ void ensure_tile_flat(aprgpu_apr* apr, cudaStream_t s) {
     L.tile_flat_n[H - 1] = total;
 }
 
+// APRGPU_MAP_DROP=0: the placement pass keeps chunks no active block reads (A/B experiments)
+bool map_drop_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("APRGPU_MAP_DROP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // APRGPU_MAP_PLACE=0: keep the build's F order (A/B experiments)
 bool map_place_enabled() {
     static const bool on = [] {
@@ -1875,6 +1916,7 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
             if (place) {
                 TileLaunch pl = m;
                 pl.flat = L.tile_flat[H - 1];
+                pl.place_drop = map_drop_enabled();
                 const int bytes = place_smem<H>(fl[1]);
                 APR_CUDA(cudaFuncSetAttribute(k_map_place<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
                 k_map_place<H><<<total, 32 * kPlaceWarps, bytes, s>>>(pl, list_scratch.as<uint32_t>());
