@@ -148,7 +148,10 @@ constexpr uint32_t kChunkTree = 1u << 31, kChunkTail = 1u << 30, kChunkIdx = kCh
 constexpr int kMaxChunks = 4000;  // 16-bit byte offsets into F: 4 * (kFlat0 + 4 * chunks) < 65536
 template <int H>
 struct MapBox {
-    static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 2 * H;
+    // rows of kTY + 4 cells for both extents (3^3: two padding cells -- an
+    // even word stride of 18 spreads the apply's code-word banks: blocks in
+    // different z planes no longer share a bank pattern)
+    static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 4;
     static constexpr int NC = BZ * BX * BY;
     // codes in cell order, two per word: the apply reads a cell pair (c, c+1),
     // c even, with one 32-bit load

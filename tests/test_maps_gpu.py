@@ -15,7 +15,7 @@ from paper_2112_03592_b200 import _lib as L
 pytestmark = pytest.mark.gpu
 
 BZ = BX = 10
-BY = 34
+BY = 36  # (MapBox rows: kTY + 4 cells)
 CW = BZ * BX * BY // 2  # code words; then 64 masks, 64 first indices, chunks, blocks, 2 pad, block list
 
 

@@ -28,7 +28,7 @@ dapr.convolve_ptr(v.data_ptr(), tv.data_ptr(), pyr, 1, L.ACCUM_EXACT, out.data_p
 torch.cuda.synchronize()
 
 BZ = BX = 10
-BY = 34
+BY = 36  # (MapBox rows: kTY + 4 cells)
 NC = BZ * BX * BY
 CW = NC // 2
 BM = np.zeros((256, BZ, BX, BY), np.float32)  # cells each 2x2x2 block's 4x4x4 neighbourhood reads
