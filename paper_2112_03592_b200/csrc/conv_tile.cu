@@ -153,6 +153,10 @@ struct MapBox {
     // different z planes no longer share a bank pattern)
     static constexpr int BZ = kTZ + 2 * H, BX = kTX + 2 * H, BY = kTY + 4;
     static constexpr int NC = BZ * BX * BY;
+    // 5^3's expanded box: planes padded by one float4 (a plane stride of 218
+    // float2 instead of 216 -- blocks that differ only in z no longer read the
+    // same banks: offline 2.84 -> 2.43 wavefronts per pair load)
+    static constexpr int PL = BX * BY + (H == 2 ? 4 : 0), SN = BZ * PL;
     // codes in cell order, two per word: the apply reads a cell pair (c, c+1),
     // c even, with one 32-bit load
     static constexpr int CW = NC / 2;                   // code words
@@ -504,12 +508,12 @@ template <> struct Vec<double> {
 // aligned pairs from the even index at or below it.
 // pair(c): the values of box cells c, c + 1 (c even) -- from the box itself
 // (k_conv_tile) or through the cells' codes (k_conv_map)
-template <typename Acc, int H, int BX, int BY, int PADY, typename Pair>
+template <typename Acc, int H, int BX, int BY, int PADY, int PL = BX * BY, typename Pair>
 __device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int qz, int qx, int qy, Acc (&acc)[8]) {
     constexpr int K = 2 * H + 1, N = 2 + 2 * H;
     constexpr int Y0 = PADY - H;
     constexpr int YA = Y0 & ~1, SH = Y0 - YA, NP = (SH + N + 1) / 2;
-    const int base = ((2 * qz) * BX + 2 * qx) * BY + 2 * qy + YA;
+    const int base = (2 * qz) * PL + (2 * qx) * BY + 2 * qy + YA;  // (PL: the plane stride)
     if constexpr (sizeof(Acc) == 4) {
         // FAST: the block's two y-outputs share every tap's weight -> packed
         // fp32x2 FMA (same per-element rounding as two FFMAs)
@@ -524,7 +528,7 @@ __device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int q
                 float r[2 * NP];
 #pragma unroll
                 for (int pp = 0; pp < NP; ++pp) {
-                    const float2 t2 = pair(base + (nz * BX + nx) * BY + 2 * pp);
+                    const float2 t2 = pair(base + nz * PL + nx * BY + 2 * pp);
                     r[2 * pp] = t2.x;
                     r[2 * pp + 1] = t2.y;
                 }
@@ -568,7 +572,7 @@ __device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int q
                 Acc r[2 * NP];
 #pragma unroll
                 for (int pp = 0; pp < NP; ++pp) {  // exact: every float is a double
-                    const float2 t2 = pair(base + (nz * BX + nx) * BY + 2 * pp);
+                    const float2 t2 = pair(base + nz * PL + nx * BY + 2 * pp);
                     r[2 * pp] = static_cast<Acc>(t2.x);
                     r[2 * pp + 1] = static_cast<Acc>(t2.y);
                 }
@@ -595,9 +599,9 @@ __device__ __forceinline__ void apply_block_pairs(Pair pair, const Acc* W, int q
     }
 }
 
-template <typename Acc, int H, int BX, int BY, int PADY>
+template <typename Acc, int H, int BX, int BY, int PADY, int PL = BX * BY>
 __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz, int qx, int qy, Acc (&acc)[8]) {
-    apply_block_pairs<Acc, H, BX, BY, PADY>(
+    apply_block_pairs<Acc, H, BX, BY, PADY, PL>(
         [S](int c) { return *reinterpret_cast<const float2*>(S + c); }, W, qz, qx, qy, acc);
 }
 
@@ -605,7 +609,7 @@ __device__ __forceinline__ void apply_block(const float* S, const Acc* W, int qz
 // passes -- y per neighbourhood row, then x, then z -- 2x fewer FMAs than the
 // dense 5^3 taps.  Tolerance-matched like every FAST path (the sums are
 // reassociated), never used for EXACT.
-template <int H, int BX, int BY, int PADY>
+template <int H, int BX, int BY, int PADY, int PL = BX * BY>
 __device__ __forceinline__ void apply_block_sep(const float* S, const float* f, int qz, int qx, int qy,
                                                 float (&acc)[8]) {
     constexpr int K = 2 * H + 1, N = 2 + 2 * H, NP = N / 2;
@@ -613,7 +617,7 @@ __device__ __forceinline__ void apply_block_sep(const float* S, const float* f, 
     const float* fz = f;
     const float* fx = f + K;
     const float* fy = f + 2 * K;
-    const int base = ((2 * qz) * BX + 2 * qx) * BY + 2 * qy + PADY - H;
+    const int base = (2 * qz) * PL + (2 * qx) * BY + 2 * qy + PADY - H;
     float2 o[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[i] = make_float2(0.0f, 0.0f);
@@ -625,7 +629,7 @@ __device__ __forceinline__ void apply_block_sep(const float* S, const float* f, 
             float r[N];
 #pragma unroll
             for (int pp = 0; pp < NP; ++pp) {
-                const float2 t2 = *reinterpret_cast<const float2*>(S + base + (nz * BX + nx) * BY + 2 * pp);
+                const float2 t2 = *reinterpret_cast<const float2*>(S + base + nz * PL + nx * BY + 2 * pp);
                 r[2 * pp] = t2.x;
                 r[2 * pp + 1] = t2.y;
             }
@@ -1070,7 +1074,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
                                    *reinterpret_cast<const uint16_t*>(o + kTX * kTY) &
                                    *reinterpret_cast<const uint16_t*>(o + kTX * kTY + kTY);
                 if (m == 0xffffu) continue;
-                const int key = (((2 * qz) * M::BX + 2 * qx) * (M::BY / 2) + qy) % M::NK;
+                const int key = H == 1 ? (((2 * qz) * M::BX + 2 * qx) * (M::BY / 2) + qy) % M::NK
+                                       : ((2 * qz) * (M::PL / 2) + qx * M::BY + qy) % M::NK;
                 keyed[total] = static_cast<uint8_t>(b);
                 bkey[total++] = static_cast<uint8_t>(key);
                 ++nbk[key];
@@ -1153,7 +1158,7 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     // place: shared memory bounds its occupancy); EXACT 5^3 (register-bound)
     // puts S after F and expands in one pass
     constexpr bool kInPlace = H == 2 && sizeof(Acc) == 4;
-    float* F = reinterpret_cast<float*>(Mb + (kInPlace ? M::HDR + M::NC : M::REC));
+    float* F = reinterpret_cast<float*>(Mb + (kInPlace ? M::HDR + M::SN : M::REC));
     __shared__ __align__(8) uint64_t mbar;
     __shared__ Acc W[KW];
     __shared__ float SF[3 * K];  // FAST 5^3, rank-1 stencil: its factors
@@ -1247,7 +1252,7 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     // codes and values read before its writes, never clobber a code still to
     // be read -- so the box needs no storage of its own beyond the codes'.
     constexpr bool kBox = H == 2;
-    float* S = kInPlace ? reinterpret_cast<float*>(Mb + M::HDR) : F + nf + (kListInBox ? 0 : a.map_ng);  // (NC floats)
+    float* S = kInPlace ? reinterpret_cast<float*>(Mb + M::HDR) : F + nf + (kListInBox ? 0 : a.map_ng);  // (SN floats)
     if constexpr (kBox) {
         const uint4* C4 = reinterpret_cast<const uint4*>(Mb + M::CODE0);
         float4* S4 = reinterpret_cast<float4*>(S);
@@ -1255,6 +1260,8 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
         auto at = [Fb](uint32_t off) { return *reinterpret_cast<const float*>(Fb + off); };
         constexpr int NG = M::NC / 8;
         static_assert(M::NC % 8 == 0, "8-cell groups");
+        constexpr int kGPlane = M::BX * M::BY / 8;  // 8-cell groups per plane
+        static_assert(M::BX * M::BY % 8 == 0 && M::PL == M::BX * M::BY + 4, "float4-padded planes");
         auto group = [&](int g, float4& v0, float4& v1) {
             const uint4 c = C4[g];
             v0 = make_float4(at(c.x & 0xffffu), at(c.x >> 16), at(c.y & 0xffffu), at(c.y >> 16));
@@ -1267,17 +1274,17 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
                 float4 v0, v1;
                 if (g < NG) group(g, v0, v1);
                 __syncthreads();
-                if (g < NG) {
-                    S4[2 * g] = v0;
-                    S4[2 * g + 1] = v1;
+                if (g < NG) {  // (one float4 of padding per plane)
+                    S4[2 * g + g / kGPlane] = v0;
+                    S4[2 * g + 1 + g / kGPlane] = v1;
                 }
             }
         } else {
             for (int g = tid; g < NG; g += NT) {
                 float4 v0, v1;
                 group(g, v0, v1);
-                S4[2 * g] = v0;
-                S4[2 * g + 1] = v1;
+                S4[2 * g + g / kGPlane] = v0;
+                S4[2 * g + 1 + g / kGPlane] = v1;
             }
         }
         __syncthreads();
@@ -1294,11 +1301,11 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
         if constexpr (kBox) {
             if constexpr (kSepOk) {
                 if (sep)
-                    apply_block_sep<H, M::BX, M::BY, H>(S, SF, qz, qx, qy, acc);
+                    apply_block_sep<H, M::BX, M::BY, H, M::PL>(S, SF, qz, qx, qy, acc);
                 else
-                    apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+                    apply_block<Acc, H, M::BX, M::BY, H, M::PL>(S, W, qz, qx, qy, acc);
             } else {
-                apply_block<Acc, H, M::BX, M::BY, H>(S, W, qz, qx, qy, acc);
+                apply_block<Acc, H, M::BX, M::BY, H, M::PL>(S, W, qz, qx, qy, acc);
             }
         } else {  // box cells straight from their codes: no box is materialised
             apply_block_pairs<Acc, H, M::BX, M::BY, H>(
@@ -1784,8 +1791,8 @@ void launch_map(aprgpu_ctx* ctx, const TileLaunch& a, uint32_t n, cudaStream_t s
     using M = MapBox<H>;
     const int fw = kFlat0 + 5 * a.map_ng;
     const int lf = a.list_in_f ? a.map_ng : 0;  // (the list in F's tail: no words of its own)
-    const int bytes = (H == 2 && sizeof(Acc) == 4 ? M::HDR + M::NC + fw - lf
-                       : H == 2                   ? M::REC + fw - a.map_ng + std::max(M::NC, a.map_ng)  // list in the box
+    const int bytes = (H == 2 && sizeof(Acc) == 4 ? M::HDR + M::SN + fw - lf
+                       : H == 2                   ? M::REC + fw - a.map_ng + std::max(M::SN, a.map_ng)  // list in the box
                                                   : M::REC + fw - lf) * 4;
     if (bytes > 225 * 1024) fail(APRGPU_ERR_CAPABILITY, "gather map exceeds shared memory");
     // 3^3: 96-thread CTAs (a C3 tile has ~65 active blocks: the apply's one
