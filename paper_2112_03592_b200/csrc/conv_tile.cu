@@ -94,7 +94,8 @@ struct TileLaunch {
     uint32_t* map[kMaxLevels];        // per segment: gather-map records (k_conv_map), or the build target
     uint32_t map_base[kMaxLevels];    // per segment: the tile whose record is map[s][0]
     uint32_t* flat;                   // per H flattened source lists (DevAccess::tile_flat)
-    const uint32_t* flat_off;         // n_tiles + 1 offsets into flat
+    const uint32_t* flat_off;         // n_tiles + 1 exact offsets (chunk counts; the lists sit at tix * flat_cap)
+    uint32_t flat_cap;                // entries per tile in flat (the largest tile's chunk count)
     int place_drop;                   // k_map_place: drop the chunks no active block reads (3^3)
     int* map_overflow;                // set by the build when a tile has > MapBox::NC sources
     int* map_maxg;                    // the build's largest per-tile chunk count (atomicMax)
@@ -890,7 +891,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(Acc) == 8 ? (H == 2 ? 3 :
     __syncthreads();
 
     // ---- fill: one thread per source particle
-    const uint32_t flat0 = MAP ? a.flat_off[tix] : 0;
+    const uint32_t flat0 = MAP ? tix * a.flat_cap : 0;
     int chunk0 = 0;  // first flattened index of the current rid chunk
     auto put = [&](int p) {
         const int t = rid[p - chunk0];
@@ -1171,42 +1172,40 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
     const uint32_t* rec = a.map[s] + static_cast<size_t>(tix - a.map_base[s]) * M::REC;
     // a slab launch's tiles straddling the slab: the row range needs the tile's
-    // z (a load); other launches decide nothing from it, so the record's copy
-    // is issued first
+    // z (a load); other launches decide nothing from it
     RowRange rr{0, kTZ};
     if (l >= a.slab_lc) {
         const int z0 = static_cast<int>(a.tiles[tix] / (static_cast<uint32_t>(a.tdim[s][1]) * a.tdim[s][2])) * kTZ;
         rr = slab_rows(a, l, z0);
         if (rr.lo >= rr.hi) return;  // slab decomposition: no row of this tile is in the slab
     }
-    // the record and the tile's chunk list stream in by two bulk copies; the
-    // record's is issued before the list's extent is known (its bytes are
-    // expected without an arrival; the one arrival comes with the list's)
+    // the record and the tile's chunk list stream in by two bulk copies, both
+    // issued before the CTA loads anything: the lists sit at a fixed stride
+    // (tix * flat_cap) and are copied at the launch's largest extent (map_ng
+    // entries; the tile's own count arrives with the record)
     const int nf = kFlat0 + 4 * a.map_ng;  // F floats of this launch
     // the staged chunk list: after F -- or, for EXACT 5^3, inside the box S it
-    // precedes (S is written only after the gather)
+    // precedes (S is written only after the gather).  3^3 and FAST 5^3: in the
+    // tail of F's region, which the gather then fills from the front -- a
+    // chunk's copy can only land on list entries at or below its own, read in
+    // its round or before (rounds below): 4 bytes per chunk of shared memory
+    // less per CTA
     constexpr bool kListInBox = H == 2 && !kInPlace;
-    uint32_t* Gs = reinterpret_cast<uint32_t*>(F + nf);  // (3^3 with list_in_f: moved into F's tail below)
+    const bool list_in_f = (H == 1 || kInPlace) && a.list_in_f;
+    uint32_t* Gs = reinterpret_cast<uint32_t*>(F + nf) - (list_in_f ? a.map_ng : 0);
     if (tid == 0) {
         mbar_init(&mbar, 1);
-        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(M::REC * 4) : "memory");
+        mbar_expect(&mbar, (M::REC + a.map_ng) * 4);  // (arrive.expect_tx)
         // (records and lists are read once per pass: evict-first, leaving L2 to
         // the source values neighbouring tiles re-read)
-        if (a.l2hint) bulk_copy_hint(Mb, rec, M::REC * 4, &mbar, l2_evict_first());
-        else bulk_copy(Mb, rec, M::REC * 4, &mbar);
-    }
-    const uint32_t f0 = __ldg(a.flat_off + tix), nchunk = __ldg(a.flat_off + tix + 1) - f0;
-    // 3^3: the list in the tail of F's region, which the gather then fills from
-    // the front -- a chunk's copy can only land on list entries at or below its
-    // own, read in its round or before (rounds below): 4 bytes per chunk of
-    // shared memory less per CTA
-    const bool list_in_f = (H == 1 || kInPlace) && a.list_in_f;
-    if (list_in_f) Gs = reinterpret_cast<uint32_t*>(F + nf) - ((nchunk + 3u) & ~3u);
-    if (tid == 0) {
-        mbar_expect(&mbar, nchunk * 4);  // (arrive.expect_tx)
-        if (nchunk) {
-            if (a.l2hint) bulk_copy_hint(Gs, a.flat + f0, nchunk * 4, &mbar, l2_evict_first());
-            else bulk_copy(Gs, a.flat + f0, nchunk * 4, &mbar);
+        const uint32_t* lst = a.flat + static_cast<size_t>(tix) * a.flat_cap;
+        if (a.l2hint) {
+            const uint64_t pol = l2_evict_first();
+            bulk_copy_hint(Mb, rec, M::REC * 4, &mbar, pol);
+            if (a.map_ng) bulk_copy_hint(Gs, lst, a.map_ng * 4, &mbar, pol);
+        } else {
+            bulk_copy(Mb, rec, M::REC * 4, &mbar);
+            if (a.map_ng) bulk_copy(Gs, lst, a.map_ng * 4, &mbar);
         }
     }
     if (tid < kFlat0) F[tid] = 0.0f;
@@ -1369,8 +1368,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps) k_map_place(const __grid_con
     const int l = a.lvl[s];
     const uint32_t tix = a.tile_base + blockIdx.x + a.seg_shift[s];
     uint32_t* rec = a.map[s] + static_cast<size_t>(tix - a.map_base[s]) * M::REC;
-    const uint32_t f0 = a.flat_off[tix];
-    const int nch = static_cast<int>(a.flat_off[tix + 1] - f0);
+    const uint32_t f0 = tix * a.flat_cap;
+    const int nch = static_cast<int>(a.flat_off[tix + 1] - a.flat_off[tix]);
     const int nb = static_cast<int>(rec[M::W_NBLK]);
     const LevelG g = a.leaf.g[l];
     const Geo G = make_geo<H>(l, a.tiles[tix], a.tdim[s][1], a.tdim[s][2], g);
@@ -1722,6 +1721,14 @@ __global__ void k_tile_nflat(const uint32_t* __restrict__ run_off, const uint2* 
 
 // The flattened source lists' layout for half-width H (allocated zeroed; the
 // map build writes them).
+__global__ void k_max_u32(const uint32_t* __restrict__ v, uint64_t n, uint32_t* out) {
+    uint32_t m = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        m = max(m, v[i]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 template <int H>
 void ensure_tile_flat(aprgpu_apr* apr, cudaStream_t s) {
     DevAccess& L = apr->leaf;
@@ -1744,15 +1751,28 @@ void ensure_tile_flat(aprgpu_apr* apr, cudaStream_t s) {
     tb = temp.bytes;
     APR_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, counts.as<uint32_t>(), off, static_cast<int64_t>(n + 1), s));
     count_launch(apr->ctx);
-    uint32_t total = 0;
-    APR_CUDA(cudaMemcpyAsync(&total, off + n, 4, cudaMemcpyDeviceToHost, s));
-    APR_CUDA(cudaStreamSynchronize(s));
+    // the lists at a fixed stride: the largest tile's chunk count (a multiple of 4)
+    uint32_t cap = 0;
+    if (n) {
+        GpuBuf mx;
+        mx.ensure(16);
+        APR_CUDA(cudaMemsetAsync(mx.p, 0, 4, s));
+        k_max_u32<<<std::min<unsigned>(blocks_for(n, 256), apr->ctx->sm_count * 8), 256, 0, s>>>(counts.as<uint32_t>(), n,
+                                                                                                 mx.as<uint32_t>());
+        count_launch(apr->ctx);
+        APR_CUDA(cudaGetLastError());
+        APR_CUDA(cudaMemcpyAsync(&cap, mx.p, 4, cudaMemcpyDeviceToHost, s));
+        APR_CUDA(cudaStreamSynchronize(s));
+    }
+    cap = std::max<uint32_t>((cap + 3u) & ~3u, 4u);
+    if (static_cast<uint64_t>(n) * cap >= (1ull << 32)) fail(APRGPU_ERR_CAPABILITY, "chunk lists exceed u32 offsets");
     uint32_t* flat = nullptr;
-    APR_CUDA(cudaMalloc(&flat, 4ull * total + 16));
-    APR_CUDA(cudaMemsetAsync(flat, 0, 4ull * total + 16, s));  // padding entries: particle 0
+    APR_CUDA(cudaMalloc(&flat, 4ull * n * cap + 16));
+    APR_CUDA(cudaMemsetAsync(flat, 0, 4ull * n * cap + 16, s));  // padding entries: particle 0
     L.tile_flat_off[H - 1] = off;
     L.tile_flat[H - 1] = flat;
-    L.tile_flat_n[H - 1] = total;
+    L.tile_flat_n[H - 1] = static_cast<uint64_t>(n) * cap;
+    L.tile_flat_cap[H - 1] = cap;
 }
 
 // APRGPU_MAP_DROP=0: the placement pass keeps chunks no active block reads (A/B experiments)
@@ -1906,6 +1926,7 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
             }
             m.flat = place ? list_scratch.as<uint32_t>() : L.tile_flat[H - 1];
             m.flat_off = L.tile_flat_off[H - 1];
+            m.flat_cap = L.tile_flat_cap[H - 1];
             m.slab_lc = 1 << 20;  // every tile of the windows
             GpuBuf flag;
             flag.ensure(16);
@@ -1952,6 +1973,7 @@ bool ensure_tile_maps(aprgpu_apr* apr, TileLaunch& b, const uint64_t (*rng)[2], 
     }
     b.flat = L.tile_flat[H - 1];
     b.flat_off = L.tile_flat_off[H - 1];
+    b.flat_cap = L.tile_flat_cap[H - 1];
     b.aligned16 = ((reinterpret_cast<uintptr_t>(b.val) | reinterpret_cast<uintptr_t>(b.tval)) & 15) == 0;
     static const bool lf = [] {  // APRGPU_MAP_LISTF=0: the list after F (A/B experiments)
         const char* e = std::getenv("APRGPU_MAP_LISTF");

@@ -144,6 +144,7 @@ struct DevAccess {
     uint32_t* tile_flat[2] = {nullptr, nullptr};
     uint32_t* tile_flat_off[2] = {nullptr, nullptr};  // n_tiles + 1 offsets into tile_flat
     uint64_t tile_flat_n[2] = {0, 0};                 // entries of tile_flat
+    uint32_t tile_flat_cap[2] = {0, 0};               // its per-tile stride (the largest tile's chunks)
     uint8_t tile_map_fail[2][2][kMaxLevels] = {};  // a level that reconstructs (no map)
     int tile_map_ng[2][kMaxLevels] = {};            // per H and level: largest per-tile chunk count
     AccessView view() const;
