@@ -1232,11 +1232,22 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     // chunks no active block reads, so it can be below the list's extent)
     const uint32_t ng = Mb[M::W_NLEAF];
     if (list_in_f) {
-        for (uint32_t c0 = 0; c0 < ng; c0 += NT) {  // (uniform trip count)
-            const uint32_t c = c0 + tid;
-            const uint32_t e = c < ng ? Gs[c] : 0u;
-            __syncthreads();  // the round's entries are read before its copies may overwrite them
-            if (c < ng) gather(c, e);
+        // rounds of 4 * NT chunks: every entry a round's copies may overwrite
+        // (at or below their own) is read before its barrier
+        constexpr int KR = 4;
+        for (uint32_t c0 = 0; c0 < ng; c0 += KR * NT) {  // (uniform trip count)
+            uint32_t e[KR];
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const uint32_t c = c0 + k * NT + tid;
+                e[k] = c < ng ? Gs[c] : 0u;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const uint32_t c = c0 + k * NT + tid;
+                if (c < ng) gather(c, e[k]);
+            }
         }
     } else {
         for (uint32_t c = tid; c < ng; c += NT) gather(c, Gs[c]);
