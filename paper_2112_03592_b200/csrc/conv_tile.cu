@@ -146,6 +146,7 @@ constexpr int kFlat0 = 4;  // F[0 .. 3]: the zero (and 16-byte alignment of the 
 // elements are copied).  A tile's chunk count is padded to 4 (16-byte bulk
 // copies of the list).
 constexpr uint32_t kChunkTree = 1u << 31, kChunkTail = 1u << 30, kChunkIdx = kChunkTail - 1;
+constexpr uint32_t kListHead = 512;  // 3^3 chunk-list entries copied with the record (k_conv_map)
 constexpr int kMaxChunks = 4000;  // 16-bit byte offsets into F: 4 * (kFlat0 + 4 * chunks) < 65536
 template <int H>
 struct MapBox {
@@ -1193,19 +1194,23 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
     constexpr bool kListInBox = H == 2 && !kInPlace;
     const bool list_in_f = (H == 1 || kInPlace) && a.list_in_f;
     uint32_t* Gs = reinterpret_cast<uint32_t*>(F + nf) - (list_in_f ? a.map_ng : 0);
+    // the list's head (most tiles' whole list) comes with the record; a longer
+    // list's rest follows once the record has brought its count
+    const uint32_t* lst = a.flat + static_cast<size_t>(tix) * a.flat_cap;
+    // (5^3 lists are longer: most would need the second copy, so they come whole)
+    const uint32_t head = H == 1 ? min(static_cast<uint32_t>(a.map_ng), kListHead) : static_cast<uint32_t>(a.map_ng);
     if (tid == 0) {
         mbar_init(&mbar, 1);
-        mbar_expect(&mbar, (M::REC + a.map_ng) * 4);  // (arrive.expect_tx)
+        mbar_expect(&mbar, (M::REC + head) * 4);  // (arrive.expect_tx)
         // (records and lists are read once per pass: evict-first, leaving L2 to
         // the source values neighbouring tiles re-read)
-        const uint32_t* lst = a.flat + static_cast<size_t>(tix) * a.flat_cap;
         if (a.l2hint) {
             const uint64_t pol = l2_evict_first();
             bulk_copy_hint(Mb, rec, M::REC * 4, &mbar, pol);
-            if (a.map_ng) bulk_copy_hint(Gs, lst, a.map_ng * 4, &mbar, pol);
+            if (head) bulk_copy_hint(Gs, lst, head * 4, &mbar, pol);
         } else {
             bulk_copy(Mb, rec, M::REC * 4, &mbar);
-            if (a.map_ng) bulk_copy(Gs, lst, a.map_ng * 4, &mbar);
+            if (head) bulk_copy(Gs, lst, head * 4, &mbar);
         }
     }
     if (tid < kFlat0) F[tid] = 0.0f;
@@ -1213,6 +1218,18 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
         W[i] = sizeof(Acc) == 8 ? static_cast<Acc>(a.wd[a.woff[s] + i]) : static_cast<Acc>(a.wf[a.woff[s] + i]);
     __syncthreads();  // (the barrier's init is visible)
     mbar_wait(&mbar, 0);
+    // the chunks to gather: the record's count (3^3: the placement pass drops
+    // chunks no active block reads, so it can be below the list's extent)
+    const uint32_t ng = Mb[M::W_NLEAF];
+    if (ng > head) {  // (uniform) the list's rest, in whole 16-byte units (the entries past ng are zeros)
+        if (tid == 0) {
+            const uint32_t n4 = (ng + 3u) & ~3u;
+            mbar_expect(&mbar, (n4 - head) * 4);
+            if (a.l2hint) bulk_copy_hint(Gs + head, lst + head, (n4 - head) * 4, &mbar, l2_evict_first());
+            else bulk_copy(Gs + head, lst + head, (n4 - head) * 4, &mbar);
+        }
+        mbar_wait(&mbar, 1);
+    }
     // every source value copied once: one 16-byte copy per chunk (a warp's
     // chunks are mostly consecutive 16-byte pieces of one run: coalesced);
     // the array's tail chunk copies only its valid elements
@@ -1228,9 +1245,6 @@ __global__ void __launch_bounds__(NT, (sizeof(Acc) == 8 ? (H == 2 ? 4 : 8) : (H 
                 if ((e & kChunkIdx) + k < lim) cp_async4(dst + k, src + k);
         }
     };
-    // the chunks to gather: the record's count (3^3: the placement pass drops
-    // chunks no active block reads, so it can be below the list's extent)
-    const uint32_t ng = Mb[M::W_NLEAF];
     if (list_in_f) {
         // rounds of 4 * NT chunks: every entry a round's copies may overwrite
         // (at or below their own) is read before its barrier
